@@ -1,0 +1,147 @@
+"""Patch-wise Vanka smoother, Algorithm 1 (oracle; test infrastructure only).
+
+P:L449-453 (Eq:DefPlm): one patch per grid vertex, the cells whose closure contains the vertex.
+P:L454-466: Z_l(P) = all global DoFs of the patch cells, for all k+1 Radau nodes, fields and components
+(reading A11: closure); local order (m, f, c, node lexicographic in the patch node box) (reading A12).
+P:L469-485 (Def:VankaOP): S_P(d) = R_P d + omega A_P^{-1} R_P (b - A_l d), A_P = A_l[Z(P), Z(P)].
+P:L486: omega = 0.7, explicit inverse (reading A18), here LU with partial pivoting from LAPACK (library
+primitive numpy.linalg.inv) after power-of-2 symmetric equilibration s_i = 2^-round(log2 sqrt|a_ii|)
+(readings A19): Ainv = S (S A S)^{-1} S.
+P:L488-524 (alg:smoother): additive patch loop with counters p and accumulator z, averaging after the loop.
+Main form (reading A17): d <- d + omega * (sum_P E_P A_P^{-1} R_P r) / p, patches accumulated in
+lexicographic vertex order; the literal form d <- (sum_P E_P S_P(d)) / p is ``sweep_literal``.
+Class sharing: A_P depends only on the per-axis class of the vertex index
+({0}, {1}, {2..n-2}, {n-1}, {n} for n >= 4; every index its own class for n < 4).
+"""
+import itertools
+import numpy as np
+from .mesh import FIELD_V, FIELD_U, FIELD_P
+
+
+def axis_class(v, n):
+    if n < 4:
+        return v
+    if v == 0:
+        return 0
+    if v == 1:
+        return 1
+    if v == n:
+        return 4
+    if v == n - 1:
+        return 3
+    return 2
+
+
+def equilibrated_inverse(A):
+    """Ainv = S (S A S)^{-1} S with power-of-two s_i (exact scaling), LU with partial pivoting (LAPACK)."""
+    dg = np.abs(np.diag(A))
+    if np.any(dg == 0.0):
+        raise np.linalg.LinAlgError("zero diagonal")
+    s = np.exp2(-np.round(0.5 * np.log2(dg)))
+    As = A * s[:, None] * s[None, :]
+    inv = np.linalg.inv(As)
+    return inv * s[:, None] * s[None, :]
+
+
+class Patches:
+    """Vertex patches of one level with their DoF index sets Z(P) in local order."""
+
+    def __init__(self, lev):
+        self.lev = lev
+        d, r = lev.d, lev.r
+        self.verts = [tuple(reversed(t)) for t in itertools.product(*[range(n + 1) for n in reversed(lev.n)])]
+        self.dofs = []
+        self.keys = []
+        for v in self.verts:
+            lo_c = [max(v[a] - 1, 0) for a in range(d)]
+            hi_c = [min(v[a], lev.n[a] - 1) for a in range(d)]       # inclusive cell range
+            qbox = [np.arange(r * lo_c[a], r * (hi_c[a] + 1) + 1) for a in range(d)]
+            pbox = [np.arange((r - 1) * lo_c[a], (r - 1) * (hi_c[a] + 1) + 1) for a in range(d)]
+            qn = self._lex(qbox, lev.q_strides)
+            pn = self._lex(pbox, lev.p_strides)
+            idx = []
+            for m in range(lev.k + 1):
+                for c in range(d):
+                    idx.append(lev.offset(m, FIELD_V, c) + qn)
+                for c in range(d):
+                    idx.append(lev.offset(m, FIELD_U, c) + qn)
+                idx.append(lev.offset(m, FIELD_P) + pn)
+            self.dofs.append(np.concatenate(idx))
+            self.keys.append(tuple(axis_class(v[a], lev.n[a]) for a in range(d)))
+        self.classes = sorted(set(self.keys))
+        self.members = {c: [i for i, kk in enumerate(self.keys) if kk == c] for c in self.classes}
+        cnt = np.zeros(lev.N)
+        for idx in self.dofs:
+            np.add.at(cnt, idx, 1.0)
+        self.p = cnt
+        self.flat_idx = np.concatenate(self.dofs)
+
+    @staticmethod
+    def _lex(boxes, strides):
+        grids = np.meshgrid(*[b * strides[a] for a, b in enumerate(boxes)], indexing="ij")
+        return sum(grids).ravel(order="F").astype(np.int64)   # axis 0 fastest
+
+    def extract(self, A, i):
+        """A_P = A_l[Z(P), Z(P)], dense."""
+        z = self.dofs[i]
+        return A[z][:, z].toarray()
+
+
+class VankaSmoother:
+    """Algorithm 1 on one level with per-class (or per-patch) equilibrated inverses."""
+
+    def __init__(self, A, patches, omega=0.7, share_classes=True):
+        self.A = A
+        self.P = patches
+        self.omega = omega
+        self.share = share_classes
+        self.inv = {}
+        if share_classes:
+            for c in patches.classes:
+                rep = patches.members[c][0]                     # lexicographically first patch of the class
+                Ainv = equilibrated_inverse(patches.extract(A, rep))
+                for i in patches.members[c]:
+                    self.inv[i] = Ainv
+        else:
+            for i in range(len(patches.dofs)):
+                self.inv[i] = equilibrated_inverse(patches.extract(A, i))
+        if np.any(patches.p == 0):
+            raise ValueError("a DoF lies in no patch (S:L357)")
+
+    def patch_updates(self, r):
+        """y_P = A_P^{-1} R_P r for every patch, in lexicographic patch order (concatenated)."""
+        out = []
+        for c in self.P.classes:
+            mem = self.P.members[c]
+            if self.share:
+                Z = np.stack([self.P.dofs[i] for i in mem])
+                Y = r[Z] @ self.inv[mem[0]].T
+                for j, i in enumerate(mem):
+                    out.append((i, Y[j]))
+            else:
+                for i in mem:
+                    out.append((i, self.inv[i] @ r[self.P.dofs[i]]))
+        out.sort(key=lambda t: t[0])
+        return np.concatenate([y for _, y in out])
+
+    def sweep(self, b, d):
+        """One smoothing step (reading A17): d + omega * (sum_P E_P y_P) / p."""
+        r = b - self.A @ d
+        z = np.zeros_like(d)
+        np.add.at(z, self.P.flat_idx, self.patch_updates(r))
+        return d + self.omega * z / self.P.p
+
+    def sweep_literal(self, b, d):
+        """Literal Alg. 1 lines 3-9: z += E_P S_P(d), p++, d = z / p."""
+        r = b - self.A @ d
+        y = self.patch_updates(r)
+        z = np.zeros_like(d)
+        np.add.at(z, self.P.flat_idx, d[self.P.flat_idx] + self.omega * y)
+        return z / self.P.p
+
+    def smooth(self, b, d=None, steps=4):
+        """Alg. 1: d initialised with 0 (pre-smoothing) or continued (post-smoothing, reading A13)."""
+        d = np.zeros_like(b) if d is None else d.copy()
+        for _ in range(steps):
+            d = self.sweep(b, d)
+        return d

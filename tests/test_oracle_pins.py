@@ -1,0 +1,391 @@
+"""Pins of the oracle against what the paper and the mathematics fix.
+
+CPU only (-m "not gpu").  Each test names the pin and the passage it follows.  None of these re-types the
+oracle's own formula: they check printed paper values, closed forms, textbook special cases, invariants and
+brute force on tiny inputs.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+from numpy.polynomial import polynomial as Pn
+
+from oracle.basis import radau_right, gauss_lobatto_nodes01, lagrange_values
+from oracle.temporal import temporal_constants
+from oracle.mesh import Level, FIELD_V, FIELD_U, FIELD_P
+from oracle.assembly import SlabOperator
+from oracle.transfer import prolongation
+from oracle.vanka import Patches, VankaSmoother, equilibrated_inverse
+from oracle.mg import Hierarchy
+from oracle.gmres import fgmres
+from oracle.loads import (manufactured_eq53, manufactured_baseline, load_vectors, slab_rhs, end_state,
+                          interpolate_initial)
+from oracle.errors import march_errors
+from stgmg_inputs import config, dof_count, uniform_load
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+P0 = dict(rho=1.0, alpha=0.9, c0=0.01, lam=1.0, mu=1.0, K=[0.01, 0, 0, 0.01])
+
+
+def lame(E, nu):
+    return E * nu / ((1 + nu) * (1 - 2 * nu)), E / (2 * (1 + nu))
+
+
+# ---------------------------------------------------------------- P1 / P2: temporal constants -------
+def test_P1_closed_form_k0_k1():
+    """P1 (P:L122-128 Eq:GF): k=0 backward Euler, k=1 Radau IIA(2)."""
+    t, w, c, T = temporal_constants(0)
+    assert np.allclose(t, [1.0]) and np.allclose(w, [2.0]) and np.allclose(c, [1.0]) and np.allclose(T, [[1.0]])
+    t, w, c, T = temporal_constants(1)
+    assert np.allclose(t, [-1 / 3, 1], atol=1e-15)
+    assert np.allclose(w, [1.5, 0.5], atol=1e-15)
+    assert np.allclose(c, [1.5, -0.5], atol=1e-15)
+    assert np.allclose(T, [[9 / 8, 3 / 8], [-9 / 8, 5 / 8]], atol=1e-14)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_P1_radau_exactness(k):
+    """Eq:GF: exact on P_{2k}, last node t = +1; not exact on P_{2k+1}."""
+    t, w = radau_right(k)
+    assert t[-1] == 1.0
+    for deg in range(2 * k + 1):
+        exact = (1 - (-1) ** (deg + 1)) / (deg + 1)
+        assert abs(np.sum(w * t ** deg) - exact) < 1e-13
+    deg = 2 * k + 1
+    assert abs(np.sum(w * t ** deg) - (1 - (-1) ** (deg + 1)) / (deg + 1)) > 1e-6
+
+
+def _radau_iia_butcher(k):
+    """Textbook collocation Butcher matrix on [0,1]: c = (t+1)/2, A_ij = int_0^{c_i} l_j(s) ds."""
+    t, _ = radau_right(k)
+    c = 0.5 * (t + 1.0)
+    A = np.zeros((k + 1, k + 1))
+    for j in range(k + 1):
+        poly = np.array([1.0])
+        for m in range(k + 1):
+            if m != j:
+                poly = Pn.polymul(poly, np.array([-c[m], 1.0]) / (c[j] - c[m]))
+        integ = Pn.polyint(poly)
+        for i in range(k + 1):
+            A[i, j] = Pn.polyval(c[i], integ)
+    return A
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_P2_radau_iia_identity(k):
+    """P2: T = diag(w/2) A_RIIA^{-1}; row sums of T = chi(-1)."""
+    t, w, c, T = temporal_constants(k)
+    A = _radau_iia_butcher(k)
+    assert np.allclose(T, np.diag(w / 2) @ np.linalg.inv(A), atol=1e-12)
+    assert np.allclose(T.sum(axis=1), c, atol=1e-13)
+
+
+def _pade(k, z):
+    """Pade(k, k+1) approximant of e^z (textbook closed form; Radau IIA stability function)."""
+    num = sum(math.factorial(2 * k + 1 - j) * math.factorial(k) /
+              (math.factorial(2 * k + 1) * math.factorial(j) * math.factorial(k - j)) * z ** j for j in range(k + 1))
+    den = sum(math.factorial(2 * k + 1 - j) * math.factorial(k + 1) /
+              (math.factorial(2 * k + 1) * math.factorial(j) * math.factorial(k + 1 - j)) * (-z) ** j
+              for j in range(k + 2))
+    return num / den
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+@pytest.mark.parametrize("z", [-0.5, -3.0, -50.0, 2j])
+def test_P2_pade_amplification(k, z):
+    """dG(k) slab for y' = lambda y: (T - z diag(w)/2) Y = chi(-1) y0; end value = Pade(k,k+1)(z)."""
+    t, w, c, T = temporal_constants(k)
+    Y = np.linalg.solve(T.astype(complex) - z * np.diag(w) / 2, c.astype(complex))
+    assert abs(Y[-1] - _pade(k, z)) < 1e-12 * max(1.0, abs(_pade(k, z)))
+
+
+# ---------------------------------------------------------------- element / assembly invariants -----
+def test_element_invariants_2d():
+    """Mass sums to |Omega|; A_gamma, B_gamma symmetric; C(chi, 1) = 0 when G_D^u = dOmega
+    (divergence theorem); rigid translations in the kernel of the volume part of A."""
+    lev = Level(2, [3, 3], [0, 0], [1, 2], 2, 1)
+    op = SlabOperator(lev, P0, 0.01)
+    S = op.assemble_spatial()
+    assert abs(S["Mq"].sum() - 2.0) < 1e-13
+    assert abs(S["Mp"].sum() - 2.0) < 1e-13
+    for name in ("A", "B", "Mrho", "Mc"):
+        M = S[name].toarray()
+        assert np.abs(M - M.T).max() < 1e-9 * np.abs(M).max()
+    assert np.abs(S["C"].T @ np.ones(lev.np_)).max() < 1e-12
+    interior = SlabOperator(lev, P0, 0.01).forms.matrices((), ())
+    ones = np.ones(interior["A"].shape[0] // 2)
+    assert np.abs(interior["A"] @ np.concatenate([ones, 0 * ones])).max() < 1e-12
+    assert np.abs(interior["B"] @ np.ones(interior["B"].shape[0])).max() < 1e-12
+
+
+def test_element_rotation_kernel_3d():
+    """Infinitesimal rotations are strain-free: volume part of A annihilates (-y, x, 0) on a 3D cell."""
+    lev = Level(3, [1, 1, 1], [0, 0, 0], [1, 1, 1], 2, 0)
+    op = SlabOperator(lev, P0 | {"K": [0.01, 0, 0, 0, 0.01, 0, 0, 0, 0.01]}, 0.01)
+    A = op.forms.matrices((), ())["A"]
+    x = lev.node_coords(2, gauss_lobatto_nodes01(2))
+    rot = np.concatenate([-x[:, 1], x[:, 0], 0 * x[:, 0]])
+    assert np.abs(A @ rot).max() < 1e-12
+
+
+def test_P15_dof_counts():
+    """F8/P15: (k+1)(2R+S) without eliminated DoFs (Nitsche) for the BASELINE configs."""
+    assert [dof_count(config(i)) for i in range(5)] == [698, 141578, 7885839, 3367374, 26568846]
+    for i in range(5):
+        c = config(i)
+        lev = Level(c["dim"], c["cells"], c["lo"], c["hi"], c["r"], c["k"])
+        assert lev.N == dof_count(c)
+
+
+# ---------------------------------------------------------------- P4: Tab:3 --------------------------
+@pytest.mark.parametrize("level", [0, 1])
+def test_P4_table3_reproduction(level):
+    """P4: PAPER Tab:3 printed errors, Q5/Q4, k=2, Eq. 5.3, within 2 %."""
+    gold = json.load(open(os.path.join(GOLD, "tab3.json")))
+    lam, mu = lame(100.0, 0.35)
+    params = dict(rho=1.0, alpha=0.9, c0=0.01, lam=lam, mu=mu, K=[1, 0, 0, 1])
+    lev = Level(2, [4, 4], [0, 0], [1, 1], r=5, k=2)
+    res = march_errors(lev, params, manufactured_eq53(params), 0.0, 1.0, 50 * 2 ** level)
+    assert np.allclose(res["L2"], gold["L2"][str(level)], rtol=0.02, atol=0)
+    assert np.allclose(res["linf_tn"], gold["linf_tn"][str(level)], rtol=0.02, atol=0)
+
+
+# ---------------------------------------------------------------- P6: EOC of the BASELINE family ----
+def test_P6_eoc_baseline_family():
+    """P6: Q2/Q1 dG(1) with the config-0 manufactured solution, joint h/tau halving -> grad u and p
+    errors converge with order ~2 = min(r, k+1) (Eq:ApFES)."""
+    errs = []
+    for lvl in range(3):
+        n = 4 * 2 ** lvl
+        lev = Level(2, [n, n], [0, 0], [1, 1], 2, 1)
+        res = march_errors(lev, P0, manufactured_baseline(2, P0), 0.0, 0.2, 2 * 2 ** lvl)
+        errs.append(res["L2"])
+    errs = np.array(errs)
+    eoc = np.log2(errs[:-1] / errs[1:])
+    assert np.all(eoc[-1][[0, 2]] > 1.7) and np.all(eoc[-1] < 4.0)
+
+
+# ---------------------------------------------------------------- P7: energy ------------------------
+def test_P7_energy_monotone():
+    """P7 (Eq:ExUniDS_3 P:L300-306): zero loads -> E_n = A(u,u) + <rho v, v> + <c0 p, p> at t_n
+    is non-increasing."""
+    lev = Level(2, [4, 4], [0, 0], [1, 1], 2, 1)
+    op = SlabOperator(lev, P0, 0.05)
+    S = op.assemble_spatial()
+    lu = spla.splu(op.assemble().tocsc())
+    rng = np.random.default_rng(0)
+    U, V, P = rng.standard_normal(lev.R) * 1e-3, rng.standard_normal(lev.R), rng.standard_normal(lev.S)
+
+    def energy(U, V, P):
+        return U @ (S["A"] @ U) + V @ (S["Mrho"] @ V) + P @ (S["Mc"] @ P)
+
+    E_prev = energy(U, V, P)
+    for _ in range(10):
+        X = lu.solve(slab_rhs(lev, S, op.chi_m1, op.th, U, V, P, None, None))
+        U, V, P = end_state(lev, X)
+        E = energy(U, V, P)
+        assert E <= E_prev * (1 + 1e-12)
+        E_prev = E
+
+
+# ---------------------------------------------------------------- P8 / P9: transfer -------------------
+def test_P8_galerkin_identity_frozen_hF():
+    """P8: nested conforming spaces + exact quadrature => P^T A_l P = A_{l-1} when h_F is frozen."""
+    coarse = Level(2, [2, 2], [0, 0], [1, 1], 2, 1)
+    fine = Level(2, [4, 4], [0, 0], [1, 1], 2, 1)
+    hF = 0.25
+    Ac = SlabOperator(coarse, P0 | {"hF_fixed": hF}, 0.01).assemble().toarray()
+    Af = SlabOperator(fine, P0 | {"hF_fixed": hF}, 0.01).assemble()
+    P = prolongation(coarse, fine)
+    G = (P.T @ Af @ P).toarray()
+    assert np.abs(G - Ac).max() < 1e-12 * np.abs(Ac).max()
+
+
+def test_P8_galerkin_identity_level_hF_boundary_only():
+    """P8 with level h_F: the difference lives only in Nitsche penalty entries of boundary DoFs."""
+    coarse = Level(2, [2, 2], [0, 0], [1, 1], 2, 1)
+    fine = Level(2, [4, 4], [0, 0], [1, 1], 2, 1)
+    Ac = SlabOperator(coarse, P0, 0.01).assemble().toarray()
+    Af = SlabOperator(fine, P0, 0.01).assemble()
+    P = prolongation(coarse, fine)
+    Dm = (P.T @ Af @ P).toarray() - Ac
+    xq = coarse.node_coords(2, gauss_lobatto_nodes01(2))
+    on_bd = np.any((xq < 1e-12) | (xq > 1 - 1e-12), axis=1)
+    interior_nodes = np.nonzero(~on_bd)[0]
+    rows = np.concatenate([coarse.offset(m, f, c) + interior_nodes for m in range(2) for f in (0, 1) for c in range(2)])
+    assert np.abs(Dm[rows]).max() < 1e-12 * np.abs(Ac).max()
+    assert np.abs(Dm).max() > 1.0
+
+
+def test_P9_prolongation_reproduces_polynomials():
+    """P9: interpolation reproduces coarse Q_r / Q_{r-1} polynomials exactly at the fine nodes."""
+    for r in (2, 3):
+        coarse = Level(2, [2, 3], [0, 0], [1, 1], r, 0)
+        fine = Level(2, [4, 6], [0, 0], [1, 1], r, 0)
+        P = prolongation(coarse, fine)
+        f = lambda x: x[:, 0] ** r * x[:, 1] ** (r - 1) + 0.5 * x[:, 1] ** r
+        g = lambda x: x[:, 0] ** (r - 1) * x[:, 1] ** (r - 1) - x[:, 0]
+        xc = coarse.node_coords(r, gauss_lobatto_nodes01(r))
+        xf = fine.node_coords(r, gauss_lobatto_nodes01(r))
+        pc = coarse.node_coords(r - 1, gauss_lobatto_nodes01(r - 1))
+        pf = fine.node_coords(r - 1, gauss_lobatto_nodes01(r - 1))
+        vc = np.concatenate([f(xc), g(xc), f(xc), g(xc), g(pc)])
+        vf = np.concatenate([f(xf), g(xf), f(xf), g(xf), g(pf)])
+        assert np.abs(P @ vc - vf).max() < 1e-12
+
+
+# ---------------------------------------------------------------- P10-P12: Vanka ----------------------
+@pytest.fixture(scope="module")
+def cfg0():
+    c = config(0)
+    H = Hierarchy(2, c["cells"], c["lo"], c["hi"], c["r"], c["k"], c["levels"], P0, c["tau"])
+    return H
+
+
+def test_P10_vanka_fixed_point(cfg0):
+    """P10 (Eq:VankaOP0): b = A d => a sweep returns d."""
+    sm = cfg0.smoothers[1]
+    d = np.random.default_rng(3).standard_normal(cfg0.fine.N)
+    b = cfg0.A[1] @ d
+    assert np.abs(sm.sweep(b, d) - d).max() < 1e-12 * np.abs(d).max()
+
+
+def test_P11_multiplicities():
+    """P11: interior counts p_mu (2D Q2: 9/6/4 vertex/edge/cell; Q1 vertex 9; 3D 27/18/12/8, Q1 27)."""
+    lev = Level(2, [4, 4], [0, 0], [1, 1], 2, 0)
+    p = Patches(lev).p
+    q = lambda i, j: p[lev.offset(0, FIELD_U, 0) + i + j * lev.q_shape[0]]
+    assert (q(4, 4), q(5, 4), q(5, 5), q(4, 5)) == (9, 6, 4, 6)
+    assert p[lev.offset(0, FIELD_P) + 2 + 2 * lev.p_shape[0]] == 9
+    assert q(0, 0) == 4 and q(1, 0) == 4 and q(2, 0) == 6      # boundary: fewer patches
+    lev3 = Level(3, [4, 4, 4], [0, 0, 0], [1, 1, 1], 2, 0)
+    p3 = Patches(lev3).p
+    s = lev3.q_strides
+    qq = lambda i, j, k: p3[lev3.offset(0, FIELD_V, 1) + i * s[0] + j * s[1] + k * s[2]]
+    assert (qq(4, 4, 4), qq(5, 4, 4), qq(5, 5, 4), qq(5, 5, 5)) == (27, 18, 12, 8)
+    ps = lev3.p_strides
+    assert p3[lev3.offset(0, FIELD_P) + 2 * ps[0] + 2 * ps[1] + 2 * ps[2]] == 27
+
+
+def test_P11_literal_alg1_equals_averaged_form(cfg0):
+    """P11(iii), reading A17: literal (sum_P (d + w y_P))/p equals d + w sum y_P / p to rounding."""
+    sm = cfg0.smoothers[1]
+    rng = np.random.default_rng(4)
+    b, d = rng.standard_normal(cfg0.fine.N), rng.standard_normal(cfg0.fine.N)
+    s1, s2 = sm.sweep(b, d), sm.sweep_literal(b, d)
+    assert np.abs(s1 - s2).max() < 1e-13 * np.abs(s1).max()
+
+
+def test_P11_centre_patch_is_direct_solve():
+    """P11(iv): on the 2x2 mesh the centre patch holds every DoF, so A_P^{-1} R_P b = A^{-1} b."""
+    lev = Level(2, [2, 2], [0, 0], [1, 1], 2, 1)
+    A = SlabOperator(lev, P0, 0.01).assemble()
+    pa = Patches(lev)
+    centre = pa.verts.index((1, 1))
+    assert len(pa.dofs[centre]) == lev.N
+    b = np.random.default_rng(5).standard_normal(lev.N)
+    Ainv = equilibrated_inverse(pa.extract(A, centre))
+    y = np.empty(lev.N)
+    y[pa.dofs[centre]] = Ainv @ b[pa.dofs[centre]]
+    x = spla.spsolve(A.tocsc(), b)
+    assert np.abs(y - x).max() < 1e-9 * np.abs(x).max()
+
+
+@pytest.mark.parametrize("dim,cells", [(2, (6, 5)), (3, (4, 4, 5))])
+def test_P12_class_sharing_bitwise(dim, cells):
+    """P12 (App. A.4): A_P extracted per patch is identical within a per-axis class, up to the summation
+    order of the global assembly (scipy sums duplicate entries in its own order: differences <= 1e-15 rel)."""
+    lo, hi = [0.0] * dim, [1.0] * dim
+    lev = Level(dim, cells, lo, hi, 2, 1, bc_u=[0, 1, 0, 0, 1, 0][:2 * dim], bc_p=[1, 0, 0, 1, 0, 0][:2 * dim])
+    P3 = P0 | {"K": [0.01, 0, 0, 0, 0.01, 0, 0, 0, 0.01]} if dim == 3 else P0
+    A = SlabOperator(lev, P3, 0.01).assemble()
+    pa = Patches(lev)
+    nclass = 0
+    for c in pa.classes:
+        mem = pa.members[c]
+        ref = pa.extract(A, mem[0])
+        for i in mem[1:min(len(mem), 6)]:
+            assert np.abs(pa.extract(A, i) - ref).max() <= 1e-15 * np.abs(ref).max()
+        nclass += 1
+    assert nclass == np.prod([min(n, 4) + 1 for n in cells])
+
+
+def test_P12_shared_equals_unshared_smoother(cfg0):
+    """Class-shared inverses give the same sweep as one inverse per patch (configs 0-1 check, §8(c))."""
+    sm2 = VankaSmoother(cfg0.A[1], Patches(cfg0.fine), 0.7, share_classes=False)
+    rng = np.random.default_rng(6)
+    b = rng.standard_normal(cfg0.fine.N)
+    assert np.array_equal(cfg0.smoothers[1].sweep(b, 0 * b), sm2.sweep(b, 0 * b))
+
+
+# ---------------------------------------------------------------- P13: coercivity -------------------
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_P13_coercivity(n):
+    """P13 (Eq:CoercA P:L1018, Eq:CoercB P:L1046): lambda_min(sym A_gamma), lambda_min(sym B_gamma) > 0."""
+    lev = Level(2, [n, n], [0, 0], [1, 1], 2, 1)
+    S = SlabOperator(lev, P0, 0.01).assemble_spatial()
+    for name in ("A", "B"):
+        M = S[name].toarray()
+        assert np.linalg.eigvalsh(0.5 * (M + M.T)).min() > 0
+
+
+# ---------------------------------------------------------------- P3 / P14: solver ------------------
+def test_P3_fgmres_gmg_matches_direct_solve(cfg0):
+    """P3 (Lemma 3.1): FGMRES-GMG with rtol 1e-13 reaches the dense direct solution of config 0."""
+    A = cfg0.A[1]
+    b = np.random.default_rng(7).standard_normal(cfg0.fine.N)
+    xs = np.linalg.solve(A.toarray(), b)
+    x, info = fgmres(lambda v: A @ v, b, cfg0.vcycle, tol=1e-13, restart=30)
+    assert info["converged"]
+    assert np.linalg.norm(x - xs) <= 1e-9 * np.linalg.norm(xs)
+
+
+def test_P3_vcycle_single_level_is_direct():
+    """a V-cycle with one level is the coarse direct solve."""
+    H = Hierarchy(2, [2, 2], [0, 0], [1, 1], 2, 1, 1, P0, 0.01)
+    b = np.random.default_rng(8).standard_normal(H.fine.N)
+    x = np.linalg.solve(H.A[0].toarray(), b)
+    assert np.abs(H.vcycle(b) - x).max() < 1e-10 * np.abs(x).max()
+
+
+def test_P14_gmres_minimal_residual_bruteforce():
+    """P14: after j steps the FGMRES iterate minimises ||b - A x|| over span{Z_j}; with a fixed linear
+    preconditioner M that is M K_j(AM, b): compare with dense least squares."""
+    rng = np.random.default_rng(9)
+    n = 12
+    A = rng.standard_normal((n, n)) + 6 * np.eye(n)
+    M = np.eye(n) + 0.1 * rng.standard_normal((n, n))
+    b = rng.standard_normal(n)
+    for j in (1, 2, 3, 5):
+        x, info = fgmres(lambda v: A @ v, b, lambda v: M @ v, tol=1e-300, restart=j, maxit=j)
+        K = [b]
+        for _ in range(j - 1):
+            K.append(A @ (M @ K[-1]))
+        Zb = M @ np.array(K).T
+        y = np.linalg.lstsq(A @ Zb, b, rcond=None)[0]
+        assert abs(np.linalg.norm(b - A @ x) - np.linalg.norm(b - A @ Zb @ y)) < 1e-10
+
+
+def test_P14_exact_preconditioner_one_iteration():
+    """FGMRES with M = A^{-1} converges in one iteration."""
+    rng = np.random.default_rng(10)
+    A = rng.standard_normal((20, 20)) + 8 * np.eye(20)
+    Ai = np.linalg.inv(A)
+    b = rng.standard_normal(20)
+    x, info = fgmres(lambda v: A @ v, b, lambda v: Ai @ v, tol=1e-10)
+    assert info["iterations"] == 1 and info["converged"]
+
+
+def test_P16_grid_robustness_cfg0_cfg1():
+    """P16 (plausibility): iteration counts of config 0 (2 levels) and a 16x16 / 4-level version
+    of the same problem stay within +-50 %; parity of counts is otherwise unpinned."""
+    its = []
+    for cells, lv in (((4, 4), 2), ((16, 16), 4)):
+        H = Hierarchy(2, cells, [0, 0], [1, 1], 2, 1, lv, P0, 0.01)
+        b = uniform_load(H.fine.N, 1)
+        _, info = fgmres(lambda v: H.A[-1] @ v, b, H.vcycle, tol=1e-8, restart=30)
+        its.append(info["iterations"])
+    assert max(its) <= 1.5 * min(its) + 1
