@@ -1,0 +1,146 @@
+/* stgmg.h — C ABI of the B200-native space-time GMRES–GMG slab solver (arXiv:2303.06742 hot path).
+ *
+ * One call of stgmg_solve solves the algebraic I_n-problem  A_n X_n = F_n  (Problem 4.1, Eq:ALS_In,
+ * PAPER.md P:L384-390) of the numerically integrated slab problem (Problem 3.1, Eq:DPQ_A0):
+ * flexible GMRES(m) right-preconditioned by one geometric-multigrid V-cycle
+ * whose smoother is the additive patch-wise Vanka Algorithm 1 (Def:VankaOP P:L469-485,
+ * alg:smoother P:L488-524), with interpolation / transpose grid transfer and a direct coarse solve
+ * (P:L438).  Spaces: Taylor–Hood Q_r^d / Q_{r-1} (continuous pressure, P:L148 Def:VhQh) with Nitsche
+ * boundary terms (Def:ACB, Def:ab); time: dG(k) with a Lagrange basis at the k+1 right
+ * Gauss–Radau nodes (Eq:GF P:L122-128, Eq:TimeExp P:L356-362).  Everything is IEEE binary64.
+ *
+ * Vector layout (every vector argument; Eq:DefXn): for m = 0..k (Radau node), blocks
+ *   V (d components), U (d components), P, each component a lexicographic node array (x fastest);
+ *   Q_r nodes per axis r*n_a+1 (n_q in total), Q_{r-1} nodes per axis (r-1)*n_a+1 (n_p in total);
+ *   offsets V_c: m*(2R+S) + c*n_q,  U_c: m*(2R+S) + R + c*n_q,  P: m*(2R+S) + 2R,  R = d*n_q, S = n_p,
+ *   N_l = (k+1)(2R+S).  Row slots of A_n are aligned with the column slots: the V slot holds the rho-scaled
+ *   u-equation (test phi), the U slot the v-equation (test chi), the P slot the p-equation (test psi)
+ *   (SURVEY §8(c) reading A5).
+ *
+ * Return codes: 0 = OK, >0 = soft result, <0 = error (message via stgmg_last_error()).
+ * Ownership: every vector pointer is caller-owned DEVICE memory (e.g. torch.Tensor.data_ptr()) of length
+ * stgmg_local_size(level), except the *_host entry points, which take caller-owned HOST memory.  The
+ * library owns every internal buffer (inverses, Krylov basis, level vectors); all of them are allocated in
+ * stgmg_setup and freed in stgmg_destroy; nothing is allocated during a solve.  All device work is
+ * enqueued on params.stream (0 = the legacy default stream); stgmg_solve / stgmg_solve_host return after a
+ * stream synchronisation with the stats filled.  A handle is not thread-safe: one handle per stream/thread.
+ */
+#ifndef STGMG_H
+#define STGMG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct stgmg_handle stgmg_handle; /* opaque, owned by the library */
+
+enum {
+  STGMG_OK = 0,
+  STGMG_NOT_CONVERGED = 1, /* maxit Arnoldi steps reached; stats filled, x = last iterate */
+  STGMG_EINVAL = -1,       /* invalid argument: r<2, k<0, cells not divisible by 2^(levels-1), rho/c0/tau<=0, ... */
+  STGMG_ENOMEM = -2,       /* device allocation failed */
+  STGMG_ECUDA = -3,        /* CUDA runtime error; message carries cudaGetErrorString */
+  STGMG_ENCCL = -4,        /* reserved for the multi-GPU path */
+  STGMG_ESINGULAR = -5,    /* zero pivot in a patch-class or coarse inverse; message names level and class */
+  STGMG_ECOVER = -6,       /* a DoF lies in no patch (p_mu == 0) */
+  STGMG_ENOTSUP = -7       /* (d, r, k) combination not compiled into this library */
+};
+enum { STGMG_BC_DIRICHLET = 0, STGMG_BC_NEUMANN = 1 };
+enum { STGMG_HF_MEASURE = 0 /* h_F = |K|_d, P:L205 (default) */, STGMG_HF_EDGE = 1 /* h_F = h normal to F */ };
+enum { STGMG_TOL_REL = 0 /* ||r|| <= tol ||b|| (BASELINE) */, STGMG_TOL_ABS = 1 /* ||r|| <= tol */ };
+enum { STGMG_SMOOTH_ADDITIVE = 0 /* Alg. 1 (only variant implemented) */ };
+
+/* Structured box, fine level (nested quad/hex levels, h_l = h_{l-1}/2). */
+typedef struct {
+  int dim;          /* 2 or 3 */
+  int cells[3];     /* fine cells per axis; each divisible by 2^(levels-1); cells[2] ignored for dim 2 */
+  double lo[3];     /* box lower corner */
+  double hi[3];     /* box upper corner */
+  int bc_u[6];      /* per face x-,x+,y-,y+,z-,z+: STGMG_BC_DIRICHLET (Nitsche) or _NEUMANN */
+  int bc_p[6];
+} stgmg_mesh;
+
+typedef struct {
+  int r; /* degree of u, v (Q_r); pressure Q_{r-1}; r >= 2 */
+  int k; /* dG(k) in time, k+1 Radau nodes; k >= 0 */
+} stgmg_order;
+
+typedef struct {
+  double rho, alpha, c0, lambda, mu; /* P:L52; isotropic C from (lambda, mu); all > 0 except lambda >= 0 */
+  double K[9];                       /* permeability / conductivity, row-major d x d (upper-left block used) */
+  double tau;                        /* slab length tau_n (uniform) */
+  double gamma_a, gamma_b;           /* Nitsche penalties; < 0 -> 5e4 r(r+1), r(r-1)/2 */
+  int hF_mode;                       /* STGMG_HF_MEASURE (default) | STGMG_HF_EDGE */
+  double omega;                      /* Vanka under-relaxation, 0.7; <= 0 -> 0.7 */
+  int jmax;                          /* smoothing steps per level, 4; <= 0 -> 4 */
+  int smoother;                      /* STGMG_SMOOTH_ADDITIVE */
+  void* nccl_comm;                   /* reserved (multi-GPU); must be NULL in this build */
+  int rank, nranks;                  /* 0, 1 */
+  void* stream;                      /* cudaStream_t for all work; NULL = default stream */
+} stgmg_params;
+
+typedef struct {
+  int iterations;         /* total Arnoldi steps (= V-cycles applied) */
+  int restarts;           /* completed restart cycles */
+  double rel_residual;    /* true ||b - A x|| / ||b|| at return */
+  double abs_residual;    /* true ||b - A x|| at return */
+  double seconds;         /* device time of the solve (CUDA events on params.stream) */
+  double level_seconds[16];/* reserved */
+} stgmg_stats;
+
+/* Build the level hierarchy, the matrix-free operators, the patch-class inverses (equilibrated LU /
+ * Gauss–Jordan on the device) and the coarse inverse; capture the V-cycle as a CUDA graph.
+ * levels counts the coarse level (levels = 1: direct solve only).  *out receives the handle.
+ * Errors: EINVAL (parameters), ENOMEM, ECUDA, ESINGULAR, ECOVER, ENOTSUP. */
+int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, const stgmg_params* params,
+                stgmg_handle** out);
+
+/* Number of slab DoFs N_l of a level (0 = coarse .. levels-1 = fine). */
+int stgmg_local_size(const stgmg_handle* h, int level, int64_t* n_owned);
+
+/* y = A_l x on level l (matrix-free, Problem 3.1 rediscretised on T_l; reading A14).  x, y: device. */
+int stgmg_apply_operator(stgmg_handle* h, int level, const double* x, double* y);
+
+/* r = b - A_l x on level l.  b, x, r: device, r may not alias x. */
+int stgmg_residual(stgmg_handle* h, int level, const double* b, const double* x, double* r);
+
+/* One smoothing sweep of Algorithm 1 on level l >= 1: d <- d + omega (sum_P E_P A_P^-1 R_P
+ * (b - A_l d)) / p.  d is updated in place.  Exposed for kernel-level parity tests. */
+int stgmg_smooth_sweep(stgmg_handle* h, int level, const double* b, double* d);
+
+/* x = V-cycle(b) on the fine level: the preconditioner application M^{-1} b. */
+int stgmg_vcycle(stgmg_handle* h, const double* b, double* x);
+
+/* Restriction b_c = P_l^T r_f (level l -> l-1) and prolongation-add d_f += P_l d_c. */
+int stgmg_restrict(stgmg_handle* h, int level, const double* r_fine, double* b_coarse);
+int stgmg_prolong_add(stgmg_handle* h, int level, const double* d_coarse, double* d_fine);
+
+/* FGMRES(restart) with x as initial guess (x = 0 for the paper's setting).  tol_mode: STGMG_TOL_*.
+ * maxit counts Arnoldi steps (reading A35).  Returns OK, NOT_CONVERGED or an error; stats may be NULL. */
+int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int tol_mode, int restart, int maxit,
+                stgmg_stats* stats);
+
+/* Same as stgmg_solve with HOST buffers: copies rhs host->device and x both ways inside the call. */
+int stgmg_solve_host(stgmg_handle* h, const double* rhs_host, double* x_host, double tol, int tol_mode,
+                     int restart, int maxit, stgmg_stats* stats);
+
+/* Slab RHS: rhs = load + J X_prev, where X_prev is the previous slab's full vector (its last
+ * Radau block is the state at t_{n-1}) and J puts chi_b(-1) M_rho U, chi_b(-1) M_rho V,
+ * chi_b(-1) M_c P into the V, U, P slots of node b.  load: the theta_b-scaled load part (may be NULL). */
+int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, double* rhs);
+
+int stgmg_destroy(stgmg_handle* h);
+
+/* Thread-local message of the last error. */
+const char* stgmg_last_error(void);
+
+/* Diagnostics: number of patch classes on level l, their sizes C_P and the number of kernels launched by
+ * the last stgmg_solve (for the bench's gpu_launches field). */
+int stgmg_info(const stgmg_handle* h, int level, int* n_classes, int* max_patch_dofs, int64_t* n_patches);
+int64_t stgmg_last_launch_count(const stgmg_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STGMG_H */

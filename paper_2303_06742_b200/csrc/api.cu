@@ -1,0 +1,902 @@
+// C ABI (include/stgmg.h) and host orchestration of the B200 space-time GMRES–GMG slab solver.
+//   setup   : level geometry, reference tables (Eq:GF P:L122-128, Def:VhQh P:L148), temporal constants
+//             (P:L412-430 read per SURVEY App. A.1), patch classes (Eq:DefPlm, App. A.4), class
+//             inverses on the device, coarse inverse, transfer tables, CUDA graph
+//             of the V-cycle.
+//   vcycle  : P:L435-440 with Algorithm 1 on l = L..1 and the coarse direct solve on T_0.
+//   solve   : flexible GMRES(m), right preconditioned (readings A2-A4, A35).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+
+#include "../../include/stgmg.h"
+#include "stgmg_internal.cuh"
+
+namespace stgmg {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+cudaError_t launch_mgs_dot(double* w, const double* vprev, const double* hprev, const double* vnext, long long n,
+                           double* partials, unsigned* counter, double* out, int do_sqrt, cudaStream_t s);
+cudaError_t launch_scale(double* y, const double* x, const double* sc, int invert, long long n, cudaStream_t s);
+cudaError_t launch_givens(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, cudaStream_t s);
+cudaError_t launch_backsub(const double* H, int ldh, const double* gv, double* y, int jn, cudaStream_t s);
+cudaError_t launch_update_x(double* x, const double* Z, const double* y, int jn, long long n, cudaStream_t s);
+cudaError_t launch_set_scalar(double* dst, const double* src, cudaStream_t s);
+cudaError_t launch_identity(double* X, long long n, cudaStream_t s);
+
+// ------------------------------------------------------------------------------ host numerics (1D tables) ----
+static void legendre(int n, double x, double& p, double& dp) {
+  double p0 = 1.0, p1 = x;
+  if (n == 0) { p = 1.0; dp = 0.0; return; }
+  for (int k = 2; k <= n; ++k) {
+    const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+    p0 = p1;
+    p1 = p2;
+  }
+  p = p1;
+  dp = (std::fabs(x) < 1.0) ? n * (x * p1 - p0) / (x * x - 1.0) : 0.0;
+}
+
+// all roots of f in (-1, 1) by sign scan + bisection (n <= 8 roots; robust, to full precision)
+static std::vector<double> roots_in(const std::function<double(double)>& f) {
+  std::vector<double> out;
+  const int M = 20000;
+  double xa = -1.0 + 1e-14, fa = f(xa);
+  for (int i = 1; i <= M; ++i) {
+    const double xb = -1.0 + 2.0 * i / M - (i == M ? 1e-14 : 0.0);
+    const double fb = f(xb);
+    if (fa == 0.0) out.push_back(xa);
+    else if (fa * fb < 0.0) {
+      double lo = xa, hi = xb, flo = fa;
+      for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        const double fm = f(mid);
+        if (fm == 0.0 || hi - lo < 1e-17) { lo = hi = mid; break; }
+        if ((fm < 0) == (flo < 0)) { lo = mid; flo = fm; } else hi = mid;
+      }
+      out.push_back(0.5 * (lo + hi));
+    }
+    xa = xb;
+    fa = fb;
+  }
+  return out;
+}
+
+static void gauss01(int n, std::vector<double>& x, std::vector<double>& w) {
+  auto r = roots_in([n](double t) { double p, dp; legendre(n, t, p, dp); return p; });
+  x.clear(); w.clear();
+  for (double t : r) {
+    // Newton polish
+    for (int it = 0; it < 3; ++it) { double p, dp; legendre(n, t, p, dp); t -= p / dp; }
+    double p, dp;
+    legendre(n, t, p, dp);
+    x.push_back(0.5 * (t + 1.0));
+    w.push_back(0.5 * 2.0 / ((1.0 - t * t) * dp * dp));
+  }
+}
+
+static std::vector<double> gll01(int r) {   // Gauss–Lobatto nodes on [0,1] (reading A9)
+  std::vector<double> x{0.0};
+  if (r >= 2) {
+    auto rr = roots_in([r](double t) { double p, dp; legendre(r, t, p, dp); return dp; });
+    for (double t : rr) x.push_back(0.5 * (t + 1.0));
+  }
+  x.push_back(1.0);
+  return x;
+}
+
+static double lag(const std::vector<double>& nd, int j, double x) {
+  double v = 1.0;
+  for (size_t m = 0; m < nd.size(); ++m)
+    if ((int)m != j) v *= (x - nd[m]) / (nd[j] - nd[m]);
+  return v;
+}
+
+static double dlag(const std::vector<double>& nd, int j, double x) {
+  double s = 0.0;
+  for (size_t m = 0; m < nd.size(); ++m) {
+    if ((int)m == j) continue;
+    double t = 1.0 / (nd[j] - nd[m]);
+    for (size_t l = 0; l < nd.size(); ++l)
+      if ((int)l != j && l != m) t *= (x - nd[l]) / (nd[j] - nd[l]);
+    s += t;
+  }
+  return s;
+}
+
+// right Gauss–Radau on [-1,1]: nodes = roots of P_{k+1} - P_k (includes +1); weights (1+t)/((k+1)^2 P_k(t)^2),
+// 2/(k+1)^2 at t = 1 (Eq:GF).
+static void radau(int k, std::vector<double>& t, std::vector<double>& w) {
+  t.clear(); w.clear();
+  if (k > 0) {
+    auto rr = roots_in([k](double x) { double a, da, b, db; legendre(k + 1, x, a, da); legendre(k, x, b, db); return a - b; });
+    for (double x : rr) {
+      double pk, dpk;
+      legendre(k, x, pk, dpk);
+      t.push_back(x);
+      w.push_back((1.0 + x) / ((k + 1.0) * (k + 1.0) * pk * pk));
+    }
+  }
+  t.push_back(1.0);
+  w.push_back(2.0 / ((k + 1.0) * (k + 1.0)));
+}
+
+static OpConsts make_consts(int d, int r, int k, const stgmg_params& p) {
+  OpConsts c;
+  std::memset(&c, 0, sizeof(c));
+  std::vector<double> xg, wg;
+  gauss01(r + 1, xg, wg);
+  const auto nq = gll01(r), np = gll01(r - 1);
+  for (int g = 0; g <= r; ++g) {
+    c.wg[g] = wg[g];
+    for (int j = 0; j <= r; ++j) {
+      c.B[g][j] = lag(nq, j, xg[g]);
+      c.Dm[g][j] = dlag(nq, j, xg[g]);
+    }
+    for (int j = 0; j < r; ++j) {
+      c.Bp[g][j] = lag(np, j, xg[g]);
+      c.Dp[g][j] = dlag(np, j, xg[g]);
+    }
+  }
+  for (int s = 0; s < 2; ++s) {
+    for (int j = 0; j <= r; ++j) {
+      c.E[s][j] = lag(nq, j, (double)s);
+      c.dE[s][j] = dlag(nq, j, (double)s);
+    }
+    for (int j = 0; j < r; ++j) {
+      c.Ep[s][j] = lag(np, j, (double)s);
+      c.dEp[s][j] = dlag(np, j, (double)s);
+    }
+  }
+  std::vector<double> t, w;
+  radau(k, t, w);
+  for (int b = 0; b <= k; ++b) {
+    c.theta[b] = 0.5 * p.tau * w[b];
+    c.chim1[b] = lag(t, b, -1.0);
+  }
+  for (int b = 0; b <= k; ++b)
+    for (int a = 0; a <= k; ++a) c.T[b][a] = w[b] * dlag(t, a, t[b]) + c.chim1[a] * c.chim1[b];
+  c.rho = p.rho; c.alpha = p.alpha; c.c0 = p.c0; c.lam = p.lambda; c.mu = p.mu;
+  c.gamma_a = p.gamma_a < 0 ? 5.0e4 * r * (r + 1) : p.gamma_a;
+  c.gamma_b = p.gamma_b < 0 ? 0.5 * r * (r - 1) : p.gamma_b;
+  for (int i = 0; i < 9; ++i) c.K[i] = 0.0;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) c.K[i * 3 + j] = p.K[i * 3 + j];
+  return c;
+}
+
+static LevelGeom make_geom(int d, const int n[3], const double h[3], int r, int k1, const int bcu[6], const int bcp[6],
+                           int hF_mode) {
+  LevelGeom g;
+  std::memset(&g, 0, sizeof(g));
+  g.d = d;
+  g.vol = 1.0;
+  g.nq = 1; g.np = 1;
+  for (int a = 0; a < 3; ++a) {
+    g.n[a] = a < d ? n[a] : 1;
+    g.h[a] = a < d ? h[a] : 1.0;
+    g.qn[a] = a < d ? r * n[a] + 1 : 1;
+    g.pn[a] = a < d ? (r - 1) * n[a] + 1 : 1;
+  }
+  for (int a = 0; a < d; ++a) {
+    g.vol *= h[a];
+    g.qs[a] = g.nq; g.ps[a] = g.np;
+    g.nq *= g.qn[a]; g.np *= g.pn[a];
+  }
+  g.R = (long long)d * g.nq;
+  g.S = g.np;
+  g.block = 2 * g.R + g.S;
+  g.N = (long long)k1 * g.block;
+  for (int f = 0; f < 6; ++f) {
+    g.bcu[f] = bcu[f];
+    g.bcp[f] = bcp[f];
+    g.hF[f] = hF_mode == STGMG_HF_EDGE ? g.h[f / 2] : g.vol;   // h_F = |K|_d on boundary faces
+  }
+  return g;
+}
+
+// 1D prolongation tables for one axis (n_coarse cells, degree deg): CSR by fine rows and by coarse rows.
+struct Interp1DHost {
+  std::vector<int> rp_f, ci_f, rp_c, ci_c;
+  std::vector<double> v_f, v_c;
+};
+
+static Interp1DHost make_interp(int nc, int deg) {
+  const auto nodes = gll01(deg);
+  const int nf_nodes = deg * 2 * nc + 1, nc_nodes = deg * nc + 1;
+  std::vector<std::vector<std::pair<int, double>>> rows(nf_nodes);
+  for (int f = 0; f < nf_nodes; ++f) {
+    const int cf = std::min(f / deg, 2 * nc - 1);   // fine cell holding fine node f
+    const int i = f - deg * cf;
+    const int cc = cf / 2;
+    const double xhat = 0.5 * ((cf % 2) + nodes[i]);
+    for (int j = 0; j <= deg; ++j) {
+      const double v = lag(nodes, j, xhat);
+      if (v != 0.0) rows[f].push_back({deg * cc + j, v});
+    }
+  }
+  Interp1DHost o;
+  o.rp_f.push_back(0);
+  std::vector<std::vector<std::pair<int, double>>> cols(nc_nodes);
+  for (int f = 0; f < nf_nodes; ++f) {
+    for (auto& e : rows[f]) {
+      o.ci_f.push_back(e.first);
+      o.v_f.push_back(e.second);
+      cols[e.first].push_back({f, e.second});
+    }
+    o.rp_f.push_back((int)o.ci_f.size());
+  }
+  o.rp_c.push_back(0);
+  for (int c = 0; c < nc_nodes; ++c) {
+    for (auto& e : cols[c]) {
+      o.ci_c.push_back(e.first);
+      o.v_c.push_back(e.second);
+    }
+    o.rp_c.push_back((int)o.ci_c.size());
+  }
+  return o;
+}
+
+}  // namespace stgmg
+
+using namespace stgmg;
+
+struct LevelData {
+  LevelGeom g;
+  double *b = nullptr, *d = nullptr, *r = nullptr, *Y = nullptr;
+  int ldy = 0, lda = 0, maxcp = 0, ntiles = 0;
+  long long npatch = 0;
+  std::vector<PatchClass> cls;
+  PatchClass* cls_dev = nullptr;
+  TileDesc* tiles_dev = nullptr;
+  int* relidx_dev = nullptr;
+  double* inv_dev = nullptr;
+  TransferTables tt;
+};
+
+struct stgmg_handle {
+  int d = 2, r = 2, k = 1, k1 = 2, L = 1;
+  stgmg_params prm;
+  OpConsts c;
+  std::vector<LevelData> lev;
+  double* A0inv = nullptr;
+  int n0 = 0;
+  cudaStream_t s = nullptr;
+  bool own_stream = false;
+  // Krylov workspace
+  int m_alloc = 0;
+  double *V = nullptr, *Z = nullptr, *w = nullptr, *rv = nullptr, *H = nullptr, *cs = nullptr, *sn = nullptr,
+         *gv = nullptr, *yv = nullptr, *scal = nullptr, *partials = nullptr;
+  unsigned* counter = nullptr;
+  double* pinned = nullptr;
+  double *stage_rhs = nullptr, *stage_x = nullptr;
+  cudaGraphExec_t vgraph = nullptr;
+  int vgraph_launches = 0;
+  long long launches = 0;
+  std::vector<void*> allocs;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+template <typename T>
+static int dalloc(stgmg_handle* h, T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return STGMG_ENOMEM;
+  }
+  h->allocs.push_back((void*)*p);
+  return 0;
+}
+
+template <typename T>
+static int upload(stgmg_handle* h, T** p, const std::vector<T>& v) {
+  int rc = dalloc(h, p, v.size());
+  if (rc) return rc;
+  if (!v.empty()) STGMG_CUDA(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+#define CK(x)                \
+  do {                       \
+    int _rc = (x);           \
+    if (_rc) return _rc;     \
+  } while (0)
+#define CKE(x)                                                                      \
+  do {                                                                              \
+    cudaError_t _e = (x);                                                           \
+    if (_e != cudaSuccess) {                                                        \
+      set_error(std::string(#x) + ": " + cudaGetErrorString(_e));                   \
+      return STGMG_ECUDA;                                                           \
+    }                                                                               \
+  } while (0)
+
+// ------------------------------------------------------------------------------------- operator wrappers ----
+static int op_apply(stgmg_handle* h, const LevelGeom& g, const double* x, double* y, double sign, int batch = 1,
+                    long long stride = 0) {
+  int nl = 0;
+  cudaError_t e = launch_op_apply(h->d, h->r, h->k1, g, h->c, x, y, sign, batch, stride, h->s, &nl);
+  h->launches += nl;
+  if (e == cudaErrorNotSupported) {
+    set_error("(d, r, k) combination not compiled");
+    return STGMG_ENOTSUP;
+  }
+  CKE(e);
+  return 0;
+}
+
+static int residual(stgmg_handle* h, int l, const double* b, const double* x, double* r) {
+  const LevelGeom& g = h->lev[l].g;
+  CKE(cudaMemcpyAsync(r, b, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, h->s));
+  return op_apply(h, g, x, r, -1.0);
+}
+
+static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
+  LevelData& L = h->lev[l];
+  const double* rin = b;
+  if (!zero_start) {
+    CK(residual(h, l, b, d, L.r));
+    rin = L.r;
+  }
+  CKE(launch_patch_gemm(L.g, h->r, h->k1, L.cls_dev, L.tiles_dev, L.ntiles, L.relidx_dev, L.inv_dev, L.lda, rin, L.Y,
+                        L.ldy, h->s));
+  CKE(launch_vanka_average(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero_start ? 1 : 0, d, h->s));
+  h->launches += 2;
+  return 0;
+}
+
+static int enqueue_vcycle(stgmg_handle* h) {
+  const int L = h->L;
+  for (int l = L - 1; l >= 1; --l) {
+    LevelData& Lv = h->lev[l];
+    for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, l, Lv.b, Lv.d, j == 0));
+    CK(residual(h, l, Lv.b, Lv.d, Lv.r));
+    CKE(launch_restrict(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, Lv.r, h->lev[l - 1].b, h->s));
+    h->launches += 1;
+  }
+  CKE(launch_gemv(h->A0inv, h->n0, h->n0, h->lev[0].b, h->lev[0].d, h->s));
+  h->launches += 1;
+  for (int l = 1; l < L; ++l) {
+    LevelData& Lv = h->lev[l];
+    CKE(launch_prolong_add(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, h->lev[l - 1].d, Lv.d, h->s));
+    h->launches += 1;
+    for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, l, Lv.b, Lv.d, false));
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------------ setup pieces ----
+static int build_patches(stgmg_handle* h, int l) {
+  LevelData& Lv = h->lev[l];
+  const LevelGeom& g = Lv.g;
+  const int d = h->d, r = h->r, k1 = h->k1;
+  // per-axis classes: (vlo, cnt, mini vertex, cells)
+  struct AxCls { int vlo, cnt, vmini, cells; };
+  std::vector<AxCls> ax[3];
+  int nmini[3] = {1, 1, 1};
+  for (int a = 0; a < d; ++a) {
+    const int n = g.n[a];
+    nmini[a] = std::min(n, 4);
+    if (n < 4) {
+      for (int v = 0; v <= n; ++v) ax[a].push_back({v, 1, v, (v > 0 ? 1 : 0) + (v < n ? 1 : 0)});
+    } else {
+      ax[a].push_back({0, 1, 0, 1});
+      ax[a].push_back({1, 1, 1, 2});
+      ax[a].push_back({2, n - 3, 2, 2});
+      ax[a].push_back({n - 1, 1, 3, 2});
+      ax[a].push_back({n, 1, 4, 1});
+    }
+  }
+  if (d < 3) ax[2].push_back({0, 1, 0, 1});
+  if (d < 2) ax[1].push_back({0, 1, 0, 1});
+  // mini level: same h, same boundary conditions, min(n,4) cells per axis
+  LevelGeom mini = make_geom(d, nmini, g.h, r, k1, g.bcu, g.bcp, h->prm.hF_mode);
+  std::vector<int> relidx, minidofs, cps;
+  std::vector<long long> offs;
+  Lv.cls.clear();
+  Lv.maxcp = 0;
+  Lv.npatch = 1;
+  for (int a = 0; a < d; ++a) Lv.npatch *= (g.n[a] + 1);
+  for (auto& cz : ax[2])
+    for (auto& cy : ax[1])
+      for (auto& cx : ax[0]) {
+        const AxCls* A3[3] = {&cx, &cy, &cz};
+        PatchClass pc;
+        std::memset(&pc, 0, sizeof(pc));
+        pc.ncols = 1;
+        long long nQ = 1, nP = 1;
+        int qbox[3] = {1, 1, 1}, pbox[3] = {1, 1, 1};
+        for (int a = 0; a < 3; ++a) {
+          pc.vlo[a] = A3[a]->vlo;
+          pc.cnt[a] = A3[a]->cnt;
+          pc.cells[a] = A3[a]->cells;
+          pc.ncols *= pc.cnt[a];
+          if (a < d) {
+            qbox[a] = r * pc.cells[a] + 1;
+            pbox[a] = (r - 1) * pc.cells[a] + 1;
+            nQ *= qbox[a];
+            nP *= pbox[a];
+          }
+        }
+        pc.cp = (int)(k1 * (2 * d * nQ + nP));
+        pc.rel_off = (long long)relidx.size();
+        // mini-level base of the representative patch
+        long long mbq = 0, mbp = 0;
+        for (int a = 0; a < d; ++a) {
+          const int v = A3[a]->vmini;
+          const int c0 = v > 0 ? v - 1 : 0;
+          mbq += (long long)(r * c0) * mini.qs[a];
+          mbp += (long long)((r - 1) * c0) * mini.ps[a];
+        }
+        offs.push_back((long long)minidofs.size());
+        for (int m = 0; m < k1; ++m) {
+          for (int slot = 0; slot <= 2 * d; ++slot) {
+            const bool pres = slot == 2 * d;
+            const int* box = pres ? pbox : qbox;
+            const long long tot = pres ? nP : nQ;
+            for (long long e = 0; e < tot; ++e) {
+              long long rem = e, rel = 0, mrel = 0;
+              for (int a = 0; a < d; ++a) {
+                const int la = (int)(rem % box[a]);
+                rem /= box[a];
+                rel += (long long)la * (pres ? g.ps[a] : g.qs[a]);
+                mrel += (long long)la * (pres ? mini.ps[a] : mini.qs[a]);
+              }
+              const long long off = (long long)m * g.block + (pres ? 2 * g.R : (long long)slot * g.nq);
+              const long long moff = (long long)m * mini.block + (pres ? 2 * mini.R : (long long)slot * mini.nq);
+              relidx.push_back((int)(2 * (off + rel) + (pres ? 1 : 0)));
+              minidofs.push_back((int)(moff + mrel + (pres ? mbp : mbq)));
+            }
+          }
+        }
+        cps.push_back(pc.cp);
+        Lv.maxcp = std::max(Lv.maxcp, pc.cp);
+        Lv.cls.push_back(pc);
+      }
+  const int ncls = (int)Lv.cls.size();
+  Lv.lda = (Lv.maxcp + 15) / 16 * 16;
+  Lv.ldy = Lv.maxcp;
+  for (int c = 0; c < ncls; ++c) Lv.cls[c].inv_off = (long long)c * Lv.lda * Lv.lda;
+  // tiles
+  std::vector<TileDesc> tiles;
+  for (int c = 0; c < ncls; ++c)
+    for (int m0 = 0; m0 < Lv.cls[c].cp; m0 += 64)
+      for (int n0 = 0; n0 < Lv.cls[c].ncols; n0 += 32) tiles.push_back({c, m0, n0, 0});
+  Lv.ntiles = (int)tiles.size();
+  CK(upload(h, &Lv.cls_dev, Lv.cls));
+  CK(upload(h, &Lv.tiles_dev, tiles));
+  CK(upload(h, &Lv.relidx_dev, relidx));
+  CK(dalloc(h, &Lv.Y, (size_t)Lv.npatch * Lv.ldy));
+  CK(dalloc(h, &Lv.inv_dev, (size_t)ncls * Lv.lda * Lv.lda));
+  // dense mini-level operator: column j = A_mini e_j
+  const long long Nm = mini.N;
+  double *X = nullptr, *Ym = nullptr;
+  CKE(cudaMalloc(&X, sizeof(double) * Nm * Nm));
+  CKE(cudaMalloc(&Ym, sizeof(double) * Nm * Nm));
+  CKE(cudaMemsetAsync(X, 0, sizeof(double) * Nm * Nm, h->s));
+  CKE(cudaMemsetAsync(Ym, 0, sizeof(double) * Nm * Nm, h->s));
+  CKE(launch_identity(X, Nm, h->s));
+  int rc = op_apply(h, mini, X, Ym, 1.0, (int)Nm, Nm);
+  if (rc) return rc;
+  int* cps_dev = nullptr;
+  long long* offs_dev = nullptr;
+  int* mdofs_dev = nullptr;
+  CK(upload(h, &cps_dev, cps));
+  CK(upload(h, &offs_dev, offs));
+  CK(upload(h, &mdofs_dev, minidofs));
+  CKE(launch_extract_patch(mini, r, k1, Ym, Nm, nullptr, ncls, cps_dev, offs_dev, mdofs_dev, Lv.inv_dev, Lv.lda, h->s));
+  int *perm = nullptr, *status = nullptr;
+  double *colk = nullptr, *scale = nullptr;
+  CK(dalloc(h, &perm, (size_t)ncls * Lv.lda));
+  CK(dalloc(h, &status, (size_t)ncls));
+  CK(dalloc(h, &colk, (size_t)ncls * Lv.lda));
+  CK(dalloc(h, &scale, (size_t)ncls * Lv.lda));
+  CKE(cudaMemsetAsync(status, 0, sizeof(int) * ncls, h->s));
+  if (gauss_jordan_inverse(Lv.inv_dev, ncls, Lv.maxcp, cps_dev, Lv.lda, perm, colk, scale, status, h->s)) {
+    set_error("gauss_jordan_inverse launch failed");
+    return STGMG_ECUDA;
+  }
+  std::vector<int> st(ncls);
+  CKE(cudaMemcpyAsync(st.data(), status, sizeof(int) * ncls, cudaMemcpyDeviceToHost, h->s));
+  CKE(cudaStreamSynchronize(h->s));
+  CKE(cudaFree(X));
+  CKE(cudaFree(Ym));
+  for (int c = 0; c < ncls; ++c)
+    if (st[c] != 0) {
+      set_error("singular patch matrix: level " + std::to_string(l) + " class " + std::to_string(c) +
+                " (pivot step " + std::to_string(st[c]) + ")");
+      return STGMG_ESINGULAR;
+    }
+  return 0;
+}
+
+static int build_coarse(stgmg_handle* h) {
+  const LevelGeom& g = h->lev[0].g;
+  const long long N = g.N;
+  h->n0 = (int)N;
+  double *X = nullptr, *Ym = nullptr;
+  CKE(cudaMalloc(&X, sizeof(double) * N * N));
+  CKE(cudaMalloc(&Ym, sizeof(double) * N * N));
+  CKE(cudaMemsetAsync(X, 0, sizeof(double) * N * N, h->s));
+  CKE(cudaMemsetAsync(Ym, 0, sizeof(double) * N * N, h->s));
+  CKE(launch_identity(X, N, h->s));
+  CK(op_apply(h, g, X, Ym, 1.0, (int)N, N));
+  std::vector<int> dofs(N);
+  for (long long i = 0; i < N; ++i) dofs[i] = (int)i;
+  std::vector<int> cps{(int)N};
+  std::vector<long long> offs{0};
+  int *cps_dev, *dofs_dev, *perm, *status;
+  long long* offs_dev;
+  double *colk, *scale;
+  CK(upload(h, &cps_dev, cps));
+  CK(upload(h, &offs_dev, offs));
+  CK(upload(h, &dofs_dev, dofs));
+  CK(dalloc(h, &h->A0inv, (size_t)N * N));
+  CKE(launch_extract_patch(g, h->r, h->k1, Ym, N, nullptr, 1, cps_dev, offs_dev, dofs_dev, h->A0inv, (int)N, h->s));
+  CK(dalloc(h, &perm, (size_t)N));
+  CK(dalloc(h, &status, 1));
+  CK(dalloc(h, &colk, (size_t)N));
+  CK(dalloc(h, &scale, (size_t)N));
+  CKE(cudaMemsetAsync(status, 0, sizeof(int), h->s));
+  if (gauss_jordan_inverse(h->A0inv, 1, (int)N, cps_dev, (int)N, perm, colk, scale, status, h->s)) {
+    set_error("coarse gauss_jordan_inverse launch failed");
+    return STGMG_ECUDA;
+  }
+  int st = 0;
+  CKE(cudaMemcpyAsync(&st, status, sizeof(int), cudaMemcpyDeviceToHost, h->s));
+  CKE(cudaStreamSynchronize(h->s));
+  CKE(cudaFree(X));
+  CKE(cudaFree(Ym));
+  if (st != 0) {
+    set_error("singular coarse matrix (pivot step " + std::to_string(st) + ")");
+    return STGMG_ESINGULAR;
+  }
+  return 0;
+}
+
+static int build_transfer(stgmg_handle* h, int l) {
+  LevelData& F = h->lev[l];
+  const LevelGeom& cg = h->lev[l - 1].g;
+  for (int a = 0; a < 3; ++a) {
+    for (int pres = 0; pres < 2; ++pres) {
+      Interp1D& T = pres ? F.tt.p[a] : F.tt.q[a];
+      if (a >= h->d) {
+        T = Interp1D{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        continue;
+      }
+      Interp1DHost ih = make_interp(cg.n[a], pres ? h->r - 1 : h->r);
+      int *rpf, *cif, *rpc, *cic;
+      double *vf, *vc;
+      CK(upload(h, &rpf, ih.rp_f));
+      CK(upload(h, &cif, ih.ci_f));
+      CK(upload(h, &vf, ih.v_f));
+      CK(upload(h, &rpc, ih.rp_c));
+      CK(upload(h, &cic, ih.ci_c));
+      CK(upload(h, &vc, ih.v_c));
+      T = Interp1D{rpf, cif, vf, rpc, cic, vc};
+    }
+  }
+  return 0;
+}
+
+static int capture_vcycle(stgmg_handle* h) {
+  cudaGraph_t graph;
+  const long long before = h->launches;
+  CKE(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_vcycle(h);
+  cudaError_t e = cudaStreamEndCapture(h->s, &graph);
+  if (rc) return rc;
+  CKE(e);
+  CKE(cudaGraphInstantiate(&h->vgraph, graph, 0));
+  CKE(cudaGraphDestroy(graph));
+  h->vgraph_launches = (int)(h->launches - before);
+  h->launches = before;
+  return 0;
+}
+
+static int ensure_krylov(stgmg_handle* h, int m) {
+  if (m <= h->m_alloc) return 0;
+  const long long N = h->lev[h->L - 1].g.N;
+  CK(dalloc(h, &h->V, (size_t)(m + 1) * N));
+  CK(dalloc(h, &h->Z, (size_t)m * N));
+  CK(dalloc(h, &h->H, (size_t)(m + 1) * m));
+  CK(dalloc(h, &h->cs, (size_t)m));
+  CK(dalloc(h, &h->sn, (size_t)m));
+  CK(dalloc(h, &h->gv, (size_t)m + 1));
+  CK(dalloc(h, &h->yv, (size_t)m));
+  h->m_alloc = m;
+  return 0;
+}
+
+// ----------------------------------------------------------------------------------------------- C ABI ----
+extern "C" {
+
+const char* stgmg_last_error(void) { return g_last_error.c_str(); }
+
+int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, const stgmg_params* params,
+                stgmg_handle** out) {
+  if (!mesh || !order || !params || !out) { set_error("null argument"); return STGMG_EINVAL; }
+  const int d = mesh->dim, r = order->r, k = order->k;
+  if ((d != 2 && d != 3) || r < 2 || r > 3 || k < 0 || k > 3 || levels < 1 || levels > 16) {
+    set_error("invalid dim / order / levels (d in {2,3}, 2 <= r <= 3, 0 <= k <= 3)");
+    return STGMG_EINVAL;
+  }
+  if (!(params->rho > 0) || !(params->c0 > 0) || !(params->tau > 0) || !(params->mu > 0) || params->lambda < 0 ||
+      !(params->alpha > 0)) {
+    set_error("rho, c0, tau, mu, alpha must be > 0 and lambda >= 0 (P:L52)");
+    return STGMG_EINVAL;
+  }
+  // K symmetric positive definite (Eq:PosDefK): Cholesky of the d x d block
+  {
+    double Kd[3][3];
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) Kd[i][j] = params->K[i * 3 + j];
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j)
+        if (Kd[i][j] != Kd[j][i]) { set_error("K not symmetric"); return STGMG_EINVAL; }
+    for (int j = 0; j < d; ++j) {
+      double s = Kd[j][j];
+      for (int l = 0; l < j; ++l) s -= Kd[j][l] * Kd[j][l];
+      if (!(s > 0)) { set_error("K not positive definite (Eq:PosDefK)"); return STGMG_EINVAL; }
+      Kd[j][j] = std::sqrt(s);
+      for (int i = j + 1; i < d; ++i) {
+        double t = Kd[i][j];
+        for (int l = 0; l < j; ++l) t -= Kd[i][l] * Kd[j][l];
+        Kd[i][j] = t / Kd[j][j];
+      }
+    }
+  }
+  for (int a = 0; a < d; ++a)
+    if (mesh->cells[a] < 1 || mesh->cells[a] % (1 << (levels - 1)) != 0 || !(mesh->hi[a] > mesh->lo[a])) {
+      set_error("cells must be divisible by 2^(levels-1) and the box non-degenerate");
+      return STGMG_EINVAL;
+    }
+  if (params->nccl_comm != nullptr || params->nranks > 1) {
+    set_error("multi-GPU path not built in this round");
+    return STGMG_EINVAL;
+  }
+  auto h = std::make_unique<stgmg_handle>();
+  h->d = d; h->r = r; h->k = k; h->k1 = k + 1; h->L = levels;
+  h->prm = *params;
+  if (h->prm.omega <= 0) h->prm.omega = 0.7;
+  if (h->prm.jmax <= 0) h->prm.jmax = 4;
+  if (params->stream) {
+    h->s = (cudaStream_t)params->stream;
+  } else {
+    CKE(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  h->c = make_consts(d, r, k, h->prm);
+  h->lev.resize(levels);
+  for (int l = 0; l < levels; ++l) {
+    int n[3] = {1, 1, 1};
+    double hh[3] = {1, 1, 1};
+    for (int a = 0; a < d; ++a) {
+      n[a] = mesh->cells[a] >> (levels - 1 - l);
+      hh[a] = (mesh->hi[a] - mesh->lo[a]) / n[a];
+    }
+    h->lev[l].g = make_geom(d, n, hh, r, h->k1, mesh->bc_u, mesh->bc_p, h->prm.hF_mode);
+    const long long N = h->lev[l].g.N;
+    CK(dalloc(h.get(), &h->lev[l].b, (size_t)N));
+    CK(dalloc(h.get(), &h->lev[l].d, (size_t)N));
+    CK(dalloc(h.get(), &h->lev[l].r, (size_t)N));
+  }
+  CK(build_coarse(h.get()));
+  for (int l = 1; l < levels; ++l) {
+    CK(build_patches(h.get(), l));
+    CK(build_transfer(h.get(), l));
+  }
+  const long long Nf = h->lev[levels - 1].g.N;
+  CK(dalloc(h.get(), &h->w, (size_t)Nf));
+  CK(dalloc(h.get(), &h->rv, (size_t)Nf));
+  CK(dalloc(h.get(), &h->stage_rhs, (size_t)Nf));
+  CK(dalloc(h.get(), &h->stage_x, (size_t)Nf));
+  CK(dalloc(h.get(), &h->scal, 16));
+  CK(dalloc(h.get(), &h->partials, 2048));
+  CK(dalloc(h.get(), &h->counter, 4));
+  CKE(cudaMemset(h->counter, 0, 4 * sizeof(unsigned)));
+  CKE(cudaMallocHost(&h->pinned, 16 * sizeof(double)));
+  CKE(cudaEventCreate(&h->e0));
+  CKE(cudaEventCreate(&h->e1));
+  CK(capture_vcycle(h.get()));
+  CKE(cudaStreamSynchronize(h->s));
+  *out = h.release();
+  return 0;
+}
+
+int stgmg_destroy(stgmg_handle* h) {
+  if (!h) return 0;
+  cudaStreamSynchronize(h->s);
+  if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  if (h->e0) cudaEventDestroy(h->e0);
+  if (h->e1) cudaEventDestroy(h->e1);
+  if (h->own_stream) cudaStreamDestroy(h->s);
+  delete h;
+  return 0;
+}
+
+int stgmg_local_size(const stgmg_handle* h, int level, int64_t* n_owned) {
+  if (!h || !n_owned || level < 0 || level >= h->L) { set_error("bad level"); return STGMG_EINVAL; }
+  *n_owned = h->lev[level].g.N;
+  return 0;
+}
+
+int stgmg_info(const stgmg_handle* h, int level, int* n_classes, int* max_patch_dofs, int64_t* n_patches) {
+  if (!h || level < 0 || level >= h->L) { set_error("bad level"); return STGMG_EINVAL; }
+  if (n_classes) *n_classes = (int)h->lev[level].cls.size();
+  if (max_patch_dofs) *max_patch_dofs = h->lev[level].maxcp;
+  if (n_patches) *n_patches = h->lev[level].npatch;
+  return 0;
+}
+
+int64_t stgmg_last_launch_count(const stgmg_handle* h) { return h ? h->launches : 0; }
+
+static int sync_if_own(stgmg_handle* h) {
+  if (h->own_stream) CKE(cudaStreamSynchronize(h->s));
+  CKE(cudaGetLastError());
+  return 0;
+}
+
+int stgmg_apply_operator(stgmg_handle* h, int level, const double* x, double* y) {
+  if (!h || level < 0 || level >= h->L || !x || !y) { set_error("bad argument"); return STGMG_EINVAL; }
+  const LevelGeom& g = h->lev[level].g;
+  h->launches = 0;
+  CKE(cudaMemsetAsync(y, 0, sizeof(double) * g.N, h->s));
+  CK(op_apply(h, g, x, y, 1.0));
+  return sync_if_own(h);
+}
+
+int stgmg_residual(stgmg_handle* h, int level, const double* b, const double* x, double* r) {
+  if (!h || level < 0 || level >= h->L || !x || !b || !r) { set_error("bad argument"); return STGMG_EINVAL; }
+  h->launches = 0;
+  CK(residual(h, level, b, x, r));
+  return sync_if_own(h);
+}
+
+int stgmg_smooth_sweep(stgmg_handle* h, int level, const double* b, double* d) {
+  if (!h || level < 1 || level >= h->L || !b || !d) { set_error("bad argument"); return STGMG_EINVAL; }
+  h->launches = 0;
+  CK(sweep(h, level, b, d, false));
+  return sync_if_own(h);
+}
+
+int stgmg_restrict(stgmg_handle* h, int level, const double* rf, double* bc) {
+  if (!h || level < 1 || level >= h->L) { set_error("bad level"); return STGMG_EINVAL; }
+  CKE(launch_restrict(h->lev[level].g, h->lev[level - 1].g, h->k1, h->lev[level].tt, rf, bc, h->s));
+  return sync_if_own(h);
+}
+
+int stgmg_prolong_add(stgmg_handle* h, int level, const double* dc, double* df) {
+  if (!h || level < 1 || level >= h->L) { set_error("bad level"); return STGMG_EINVAL; }
+  CKE(launch_prolong_add(h->lev[level].g, h->lev[level - 1].g, h->k1, h->lev[level].tt, dc, df, h->s));
+  return sync_if_own(h);
+}
+
+static int vcycle_dev(stgmg_handle* h, const double* b, double* x) {
+  LevelData& F = h->lev[h->L - 1];
+  const size_t bytes = sizeof(double) * F.g.N;
+  CKE(cudaMemcpyAsync(F.b, b, bytes, cudaMemcpyDeviceToDevice, h->s));
+  CKE(cudaGraphLaunch(h->vgraph, h->s));
+  CKE(cudaMemcpyAsync(x, F.d, bytes, cudaMemcpyDeviceToDevice, h->s));
+  h->launches += h->vgraph_launches;
+  return 0;
+}
+
+int stgmg_vcycle(stgmg_handle* h, const double* b, double* x) {
+  if (!h || !b || !x) { set_error("bad argument"); return STGMG_EINVAL; }
+  h->launches = 0;
+  CK(vcycle_dev(h, b, x));
+  return sync_if_own(h);
+}
+
+int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, double* rhs) {
+  if (!h || !x_prev || !rhs) { set_error("bad argument"); return STGMG_EINVAL; }
+  const LevelGeom& g = h->lev[h->L - 1].g;
+  int nl = 0;
+  cudaError_t e = launch_slab_rhs(g, h->k1, h->c, h->r, load, x_prev, rhs, h->s, &nl);
+  CKE(e);
+  return sync_if_own(h);
+}
+
+int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int tol_mode, int restart, int maxit,
+                stgmg_stats* stats) {
+  if (!h || !rhs || !x || restart < 1 || maxit < 1 || !(tol > 0)) { set_error("bad argument"); return STGMG_EINVAL; }
+  CK(ensure_krylov(h, restart));
+  const LevelGeom& g = h->lev[h->L - 1].g;
+  const long long N = g.N;
+  const int m = restart, ldh = m + 1;
+  h->launches = 0;
+  double* scal = h->scal;     // [0] |g_{j+1}|, [1] h_{j+1,j}, [2] beta, [3] ||b||
+  double* hp = h->pinned;
+  CKE(cudaEventRecord(h->e0, h->s));
+  CKE(launch_mgs_dot(const_cast<double*>(rhs), nullptr, nullptr, nullptr, N, h->partials, h->counter, scal + 3, 1, h->s));
+  CK(residual(h, h->L - 1, rhs, x, h->rv));
+  CKE(launch_mgs_dot(h->rv, nullptr, nullptr, nullptr, N, h->partials, h->counter, scal + 2, 1, h->s));
+  h->launches += 2;
+  CKE(cudaMemcpyAsync(hp, scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
+  CKE(cudaStreamSynchronize(h->s));
+  const double bnorm = hp[3];
+  double beta = hp[2];
+  const double target = tol_mode == STGMG_TOL_ABS ? tol : tol * bnorm;
+  int its = 0, restarts = 0;
+  bool converged = beta <= target;
+  while (!converged && its < maxit) {
+    CKE(launch_scale(h->V, h->rv, scal + 2, 1, N, h->s));                 // v_0 = r / beta
+    CKE(cudaMemsetAsync(h->gv, 0, sizeof(double) * (m + 1), h->s));
+    CKE(launch_set_scalar(h->gv, scal + 2, h->s));                        // g_0 = beta
+    CKE(cudaMemsetAsync(h->H, 0, sizeof(double) * ldh * m, h->s));
+    h->launches += 2;
+    int jdone = 0;
+    for (int j = 0; j < m; ++j) {
+      double* vj = h->V + (long long)j * N;
+      double* zj = h->Z + (long long)j * N;
+      CK(vcycle_dev(h, vj, zj));                                          // z_j = M^{-1} v_j
+      CKE(cudaMemsetAsync(h->w, 0, sizeof(double) * N, h->s));
+      CK(op_apply(h, g, zj, h->w, 1.0));                                  // w = A z_j
+      double* hcol = h->H + (long long)j * ldh;
+      for (int i = 0; i <= j; ++i)                                        // modified Gram–Schmidt
+        CKE(launch_mgs_dot(h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
+                           h->V + (long long)i * N, N, h->partials, h->counter, hcol + i, 0, h->s));
+      CKE(launch_mgs_dot(h->w, h->V + (long long)j * N, hcol + j, nullptr, N, h->partials, h->counter, hcol + j + 1, 1,
+                         h->s));
+      CKE(launch_givens(h->H, ldh, h->cs, h->sn, h->gv, j, scal, h->s));
+      CKE(launch_scale(h->V + (long long)(j + 1) * N, h->w, scal + 1, 1, N, h->s));   // v_{j+1} = w / h_{j+1,j}
+      h->launches += j + 4;
+      CKE(cudaMemcpyAsync(hp, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
+      CKE(cudaStreamSynchronize(h->s));
+      ++its;
+      jdone = j + 1;
+      if (hp[0] <= target || hp[1] <= 1e-14 * beta || its >= maxit) break;
+    }
+    CKE(launch_backsub(h->H, ldh, h->gv, h->yv, jdone, h->s));
+    CKE(launch_update_x(x, h->Z, h->yv, jdone, N, h->s));
+    CK(residual(h, h->L - 1, rhs, x, h->rv));
+    CKE(launch_mgs_dot(h->rv, nullptr, nullptr, nullptr, N, h->partials, h->counter, scal + 2, 1, h->s));
+    h->launches += 3;
+    CKE(cudaMemcpyAsync(hp + 2, scal + 2, sizeof(double), cudaMemcpyDeviceToHost, h->s));
+    CKE(cudaStreamSynchronize(h->s));
+    beta = hp[2];
+    if (beta <= target) { converged = true; break; }
+    if (its >= maxit) break;
+    ++restarts;
+  }
+  CKE(cudaEventRecord(h->e1, h->s));
+  CKE(cudaEventSynchronize(h->e1));
+  float ms = 0.f;
+  CKE(cudaEventElapsedTime(&ms, h->e0, h->e1));
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->iterations = its;
+    stats->restarts = restarts;
+    stats->abs_residual = beta;
+    stats->rel_residual = bnorm > 0 ? beta / bnorm : 0.0;
+    stats->seconds = ms * 1e-3;
+  }
+  return converged ? STGMG_OK : STGMG_NOT_CONVERGED;
+}
+
+int stgmg_solve_host(stgmg_handle* h, const double* rhs_host, double* x_host, double tol, int tol_mode, int restart,
+                     int maxit, stgmg_stats* stats) {
+  if (!h || !rhs_host || !x_host) { set_error("bad argument"); return STGMG_EINVAL; }
+  LevelData& F = h->lev[h->L - 1];
+  const size_t bytes = sizeof(double) * F.g.N;
+  CK(ensure_krylov(h, restart));
+  double* stage_rhs = h->stage_rhs;   // allocated in stgmg_setup
+  double* stage_x = h->stage_x;
+  CKE(cudaMemcpyAsync(stage_rhs, rhs_host, bytes, cudaMemcpyHostToDevice, h->s));
+  CKE(cudaMemcpyAsync(stage_x, x_host, bytes, cudaMemcpyHostToDevice, h->s));
+  int rc = stgmg_solve(h, stage_rhs, stage_x, tol, tol_mode, restart, maxit, stats);
+  if (rc < 0) return rc;
+  CKE(cudaMemcpyAsync(x_host, stage_x, bytes, cudaMemcpyDeviceToHost, h->s));
+  CKE(cudaStreamSynchronize(h->s));
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// K7 — FGMRES(m) vector kernels (sm_100a, fp64): P:L354, P:L433-435 (flexible GMRES, right preconditioned),
+// modified Gram–Schmidt with the update of step i-1 fused into the dot of step i, deterministic two-level
+// reductions (fixed grid, fixed-order last-block combine), Givens rotations and back substitution on device
+// (readings A2-A4, A35).
+#include "stgmg_internal.cuh"
+
+namespace stgmg {
+
+constexpr int RED_BLOCKS = 1184;   // 8 x 148 SMs
+constexpr int RED_THREADS = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+  __syncthreads();
+  return s;   // valid in thread 0
+}
+
+// w <- w - (*hprev) vprev (if vprev), then out = <w, vnext> (vnext == nullptr: <w, w>; do_sqrt: sqrt).
+__global__ void __launch_bounds__(RED_THREADS) mgs_dot_kernel(double* __restrict__ w, const double* __restrict__ vprev,
+                                                              const double* __restrict__ hprev,
+                                                              const double* __restrict__ vnext, long long n,
+                                                              double* __restrict__ partials, unsigned* counter,
+                                                              double* __restrict__ out, int do_sqrt) {
+  __shared__ double sh[32];
+  __shared__ bool last;
+  const double coef = vprev ? *hprev : 0.0;
+  double s = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double wi = w[i];
+    if (vprev) {
+      wi = fma(-coef, vprev[i], wi);
+      w[i] = wi;
+    }
+    const double vi = vnext ? vnext[i] : wi;
+    s = fma(wi, vi, s);
+  }
+  const double bsum = block_sum(s, sh);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = bsum;
+    __threadfence();
+    const unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double p = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) p += ((volatile double*)partials)[i];
+    const double tot = block_sum(p, sh);
+    if (threadIdx.x == 0) {
+      *out = do_sqrt ? sqrt(tot) : tot;
+      *counter = 0u;
+    }
+  }
+}
+
+cudaError_t launch_mgs_dot(double* w, const double* vprev, const double* hprev, const double* vnext, long long n,
+                           double* partials, unsigned* counter, double* out, int do_sqrt, cudaStream_t s) {
+  mgs_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(w, vprev, hprev, vnext, n, partials, counter, out, do_sqrt);
+  return cudaGetLastError();
+}
+
+// y = x * (*sc) (invert: y = x / *sc)
+__global__ void scale_kernel(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ sc,
+                             int invert, long long n) {
+  const double f = invert ? 1.0 / *sc : *sc;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = x[i] * f;
+}
+
+cudaError_t launch_scale(double* y, const double* x, const double* sc, int invert, long long n, cudaStream_t s) {
+  scale_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(y, x, sc, invert, n);
+  return cudaGetLastError();
+}
+
+// Givens step for Arnoldi column j of H (column-major, ldh = m+1).  scal[0] = |g_{j+1}|, scal[1] = h_{j+1,j}.
+__global__ void givens_kernel(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double* h = H + (long long)j * ldh;
+  const double hn = h[j + 1];
+  for (int i = 0; i < j; ++i) {
+    const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double rho = hypot(h[j], hn);
+  cs[j] = h[j] / rho;
+  sn[j] = hn / rho;
+  h[j] = rho;
+  h[j + 1] = 0.0;
+  gv[j + 1] = -sn[j] * gv[j];
+  gv[j] = cs[j] * gv[j];
+  scal[0] = fabs(gv[j + 1]);
+  scal[1] = hn;
+}
+
+cudaError_t launch_givens(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, cudaStream_t s) {
+  givens_kernel<<<1, 32, 0, s>>>(H, ldh, cs, sn, gv, j, scal);
+  return cudaGetLastError();
+}
+
+// Back substitution H(0:jn,0:jn) y = g(0:jn).
+__global__ void backsub_kernel(const double* H, int ldh, const double* gv, double* y, int jn) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = jn - 1; i >= 0; --i) {
+    double s = gv[i];
+    for (int l = i + 1; l < jn; ++l) s -= H[(long long)l * ldh + i] * y[l];
+    y[i] = s / H[(long long)i * ldh + i];
+  }
+}
+
+cudaError_t launch_backsub(const double* H, int ldh, const double* gv, double* y, int jn, cudaStream_t s) {
+  backsub_kernel<<<1, 32, 0, s>>>(H, ldh, gv, y, jn);
+  return cudaGetLastError();
+}
+
+// x += sum_j y_j Z_j
+__global__ void update_x_kernel(double* __restrict__ x, const double* __restrict__ Z, const double* __restrict__ y,
+                                int jn, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = x[i];
+    for (int j = 0; j < jn; ++j) s = fma(y[j], Z[(long long)j * n + i], s);
+    x[i] = s;
+  }
+}
+
+cudaError_t launch_update_x(double* x, const double* Z, const double* y, int jn, long long n, cudaStream_t s) {
+  update_x_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, Z, y, jn, n);
+  return cudaGetLastError();
+}
+
+__global__ void set_scalar_kernel(double* dst, const double* src) {
+  if (threadIdx.x == 0) *dst = *src;
+}
+
+cudaError_t launch_set_scalar(double* dst, const double* src, cudaStream_t s) {
+  set_scalar_kernel<<<1, 32, 0, s>>>(dst, src);
+  return cudaGetLastError();
+}
+
+__global__ void identity_kernel(double* X, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) X[i * n + i] = 1.0;
+}
+
+cudaError_t launch_identity(double* X, long long n, cudaStream_t s) {
+  identity_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(X, n);
+  return cudaGetLastError();
+}
+
+}  // namespace stgmg

@@ -1,0 +1,105 @@
+// Internal declarations of the B200 space-time GMRES–GMG library (sm_100a, fp64).
+// Public ABI: include/stgmg.h.  Paper references: P:Ln = line n of PAPER.md (arXiv:2303.06742).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace stgmg {
+
+constexpr int kMaxR1 = 4;   // max nodes per axis of a Q_r cell (r <= 3)
+constexpr int kMaxK1 = 4;   // max Radau nodes (k <= 3)
+
+// Reference-element and problem constants passed by value to the operator kernels.
+// 1D tables live on the reference interval [0,1]; derivatives are d/dx_hat (scaled by 1/h in the kernels).
+struct OpConsts {
+  double B[kMaxR1][kMaxR1];    // B[g][j]  = l_j(x_g)   Q_r Lagrange (GLL nodes) at Gauss points
+  double Dm[kMaxR1][kMaxR1];   // Dm[g][j] = l_j'(x_g)
+  double Bp[kMaxR1][kMaxR1];   // Q_{r-1}
+  double Dp[kMaxR1][kMaxR1];
+  double E[2][kMaxR1];         // l_j(0), l_j(1)
+  double dE[2][kMaxR1];        // l_j'(0), l_j'(1)
+  double Ep[2][kMaxR1];
+  double dEp[2][kMaxR1];
+  double wg[kMaxR1];           // Gauss weights on [0,1]
+  double T[kMaxK1][kMaxK1];    // T[b][a] = w_b chi_a'(t_b) + chi_a(-1) chi_b(-1)
+  double theta[kMaxK1];        // (tau/2) w_b
+  double chim1[kMaxK1];        // chi_b(-1)
+  double rho, alpha, c0, lam, mu, gamma_a, gamma_b;
+  double K[9];                 // row-major d x d (stride 3)
+};
+
+// Geometry of one structured level (box split into n[a] cells per axis).
+struct LevelGeom {
+  int d;
+  int n[3];
+  double h[3];
+  double vol;                  // |K|_d
+  int qn[3], pn[3];            // Q_r / Q_{r-1} nodes per axis
+  long long qs[3], ps[3];      // lexicographic strides
+  long long nq, np, R, S, block, N;
+  int bcu[6], bcp[6];          // 0 = Dirichlet (Nitsche), 1 = Neumann
+  double hF[6];                // penalty length per boundary face on this level
+};
+
+// One patch class on a level.  Patches of a class: vertices v with per-axis index in
+// [vlo[a], vlo[a] + cnt[a]).  Patch-local layout (m, f, c, node lex in the patch box) (reading A12).
+struct PatchClass {
+  int cp;                      // C_P
+  int ncols;                   // number of patches in the class
+  int vlo[3], cnt[3];
+  int cells[3];                // cells of the patch per axis (1 or 2)
+  long long rel_off;           // offset of this class's relidx table (cp entries)
+  long long inv_off;           // offset of the class inverse (lda x lda)
+};
+
+struct TileDesc {              // one CTA tile of the grouped patch GEMM
+  int cls, m0, n0, pad;
+};
+
+#define STGMG_CUDA(call)                                                                   \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      ::stgmg::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));              \
+      return -3;                                                                           \
+    }                                                                                      \
+  } while (0)
+
+void set_error(const std::string& msg);
+
+// ---- kernels launchers (each returns cudaError_t of the launch) ----
+// K1: y (+)= sign * A_l x over the cells of one colour (or all colours); batch vectors with stride.
+cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpConsts& c, const double* x,
+                            double* y, double sign, int batch, long long stride, cudaStream_t s, int* nlaunch);
+// K2: Y[patch][mu_hat] = Ainv_class * R_P r for all patches (grouped DMMA GEMM).
+cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int k1, const PatchClass* cls_dev, const TileDesc* tiles,
+                              int ntiles, const int* relidx, const double* inv, int lda, const double* rvec,
+                              double* Y, int ldy, cudaStream_t s);
+// K3: d <- (zero ? 0 : d) + omega * (sum_P Y_P[mu_hat]) / p_mu   (pull form, lexicographic patch order).
+cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
+                                 int zero_init, double* dvec, cudaStream_t s);
+// K4 (setup): gather A_P of each class from the dense mini-level matrix; equilibrated Gauss–Jordan inverse.
+cudaError_t launch_extract_patch(const LevelGeom& mini, int r, int k1, const double* Adense, long long ldA,
+                                 const int* vrep, int nclass, const int* cps, const long long* rel_offs,
+                                 const int* relidx_mini, double* inv, int lda, cudaStream_t s);
+int gauss_jordan_inverse(double* mats, int nmat, int n_max, const int* n_each, int lda, int* perm, double* colk,
+                         double* scale, int* status, cudaStream_t s);
+// K5: restriction / prolongation with per-axis sparse 1D interpolation tables.
+struct Interp1D {              // CSR tables of the 1D prolongation for one axis and degree (device)
+  const int* rp_f; const int* ci_f; const double* v_f;   // rows = fine nodes
+  const int* rp_c; const int* ci_c; const double* v_c;   // rows = coarse nodes (transpose)
+};
+struct TransferTables { Interp1D q[3], p[3]; };
+cudaError_t launch_restrict(const LevelGeom& fine, const LevelGeom& coarse, int k1, const TransferTables& t,
+                            const double* rf, double* bc, cudaStream_t s);
+cudaError_t launch_prolong_add(const LevelGeom& fine, const LevelGeom& coarse, int k1, const TransferTables& t,
+                               const double* dc, double* df, cudaStream_t s);
+// K6: y = A x dense (coarse solve, row-major lda).
+cudaError_t launch_gemv(const double* A, int n, int lda, const double* x, double* y, cudaStream_t s);
+// K8: slab RHS.
+cudaError_t launch_slab_rhs(const LevelGeom& g, int k1, const OpConsts& c, int r, const double* load,
+                            const double* xprev, double* rhs, cudaStream_t s, int* nlaunch);
+
+}  // namespace stgmg

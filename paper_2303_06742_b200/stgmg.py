@@ -1,0 +1,231 @@
+"""Thin ctypes binding of the C ABI in include/stgmg.h (argument marshalling only).
+
+Every step of the hot path runs in the CUDA kernels of libstgmg.so; this module only converts Python /
+torch arguments to the plain pointers and structs of the ABI.  It never falls back to a CPU path: if the
+library or a CUDA device is missing, it raises.
+"""
+import ctypes
+import os
+
+from .build import LIB, build, needs_build
+
+STGMG_OK, STGMG_NOT_CONVERGED = 0, 1
+TOL_REL, TOL_ABS = 0, 1
+BC_DIRICHLET, BC_NEUMANN = 0, 1
+HF_MEASURE, HF_EDGE = 0, 1
+
+
+class Mesh(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("cells", ctypes.c_int * 3), ("lo", ctypes.c_double * 3),
+                ("hi", ctypes.c_double * 3), ("bc_u", ctypes.c_int * 6), ("bc_p", ctypes.c_int * 6)]
+
+
+class Order(ctypes.Structure):
+    _fields_ = [("r", ctypes.c_int), ("k", ctypes.c_int)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("rho", ctypes.c_double), ("alpha", ctypes.c_double), ("c0", ctypes.c_double),
+                ("lambda_", ctypes.c_double), ("mu", ctypes.c_double), ("K", ctypes.c_double * 9),
+                ("tau", ctypes.c_double), ("gamma_a", ctypes.c_double), ("gamma_b", ctypes.c_double),
+                ("hF_mode", ctypes.c_int), ("omega", ctypes.c_double), ("jmax", ctypes.c_int),
+                ("smoother", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("rank", ctypes.c_int),
+                ("nranks", ctypes.c_int), ("stream", ctypes.c_void_p)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("restarts", ctypes.c_int), ("rel_residual", ctypes.c_double),
+                ("abs_residual", ctypes.c_double), ("seconds", ctypes.c_double),
+                ("level_seconds", ctypes.c_double * 16)]
+
+    def as_dict(self):
+        return dict(iterations=self.iterations, restarts=self.restarts, rel_residual=self.rel_residual,
+                    abs_residual=self.abs_residual, seconds=self.seconds)
+
+
+# name -> (restype, argtypes) — every symbol declared in include/stgmg.h
+_P = ctypes.c_void_p
+SIGNATURES = {
+    "stgmg_setup": (ctypes.c_int, [ctypes.POINTER(Mesh), ctypes.c_int, ctypes.POINTER(Order), ctypes.POINTER(Params),
+                                   ctypes.POINTER(_P)]),
+    "stgmg_local_size": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]),
+    "stgmg_apply_operator": (ctypes.c_int, [_P, ctypes.c_int, _P, _P]),
+    "stgmg_residual": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P]),
+    "stgmg_smooth_sweep": (ctypes.c_int, [_P, ctypes.c_int, _P, _P]),
+    "stgmg_vcycle": (ctypes.c_int, [_P, _P, _P]),
+    "stgmg_restrict": (ctypes.c_int, [_P, ctypes.c_int, _P, _P]),
+    "stgmg_prolong_add": (ctypes.c_int, [_P, ctypes.c_int, _P, _P]),
+    "stgmg_solve": (ctypes.c_int, [_P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                   ctypes.POINTER(Stats)]),
+    "stgmg_solve_host": (ctypes.c_int, [_P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(Stats)]),
+    "stgmg_slab_rhs": (ctypes.c_int, [_P, _P, _P, _P]),
+    "stgmg_destroy": (ctypes.c_int, [_P]),
+    "stgmg_last_error": (ctypes.c_char_p, []),
+    "stgmg_info": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                  ctypes.POINTER(ctypes.c_int64)]),
+    "stgmg_last_launch_count": (ctypes.c_int64, [_P]),
+}
+
+_lib = None
+
+
+def load_library(path=None, rebuild=False):
+    """Load libstgmg.so (building it in-tree first if it is missing or stale)."""
+    global _lib
+    if _lib is not None and not rebuild:
+        return _lib
+    path = path or LIB
+    if rebuild or needs_build():
+        build()
+    if not os.path.exists(path):
+        raise RuntimeError("libstgmg.so not found at %s (build with paper_2303_06742_b200.build)" % path)
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class StgmgError(RuntimeError):
+    pass
+
+
+def _check(rc, what):
+    if rc < 0:
+        raise StgmgError("%s failed (%d): %s" % (what, rc, _lib.stgmg_last_error().decode()))
+    return rc
+
+
+def _ptr(t):
+    """Device pointer of a CUDA float64 torch tensor (contiguous)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise TypeError("expected a contiguous CUDA float64 tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Solver:
+    """One slab system A_n X_n = F_n of a structured configuration (see stgmg_inputs.CONFIGS)."""
+
+    def __init__(self, cfg, stream=None, tau=None, omega=0.7, jmax=4, hF_mode=HF_MEASURE, levels=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise StgmgError("no CUDA device: the stgmg product path has no CPU fallback")
+        self.lib = load_library()
+        self.cfg = cfg
+        d = cfg["dim"]
+        m = Mesh()
+        m.dim = d
+        for a in range(3):
+            m.cells[a] = int(cfg["cells"][a]) if a < d else 1
+            m.lo[a] = float(cfg["lo"][a])
+            m.hi[a] = float(cfg["hi"][a])
+        for f in range(6):
+            m.bc_u[f] = int(cfg["bc_u"][f])
+            m.bc_p[f] = int(cfg["bc_p"][f])
+        o = Order(int(cfg["r"]), int(cfg["k"]))
+        p = Params()
+        pr = cfg["params"]
+        p.rho, p.alpha, p.c0, p.lambda_, p.mu = pr["rho"], pr["alpha"], pr["c0"], pr["lam"], pr["mu"]
+        K = list(pr["K"])
+        if len(K) == 4:
+            K = [K[0], K[1], 0, K[2], K[3], 0, 0, 0, 0]
+        for i in range(9):
+            p.K[i] = float(K[i])
+        p.tau = float(tau if tau is not None else cfg["tau"])
+        p.gamma_a = float(pr.get("gamma_a", -1.0) or -1.0)
+        p.gamma_b = float(pr.get("gamma_b", -1.0) or -1.0)
+        p.hF_mode = hF_mode
+        p.omega = omega
+        p.jmax = jmax
+        p.smoother = 0
+        p.nccl_comm = None
+        p.rank, p.nranks = 0, 1
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        p.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        self.levels = int(levels or cfg["levels"])
+        h = ctypes.c_void_p()
+        _check(self.lib.stgmg_setup(ctypes.byref(m), self.levels, ctypes.byref(o), ctypes.byref(p), ctypes.byref(h)),
+               "stgmg_setup")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.stgmg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def size(self, level=None):
+        n = ctypes.c_int64()
+        lev = self.levels - 1 if level is None else level
+        _check(self.lib.stgmg_local_size(self.h, lev, ctypes.byref(n)), "stgmg_local_size")
+        return n.value
+
+    def info(self, level):
+        nc, mx, npat = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        _check(self.lib.stgmg_info(self.h, level, ctypes.byref(nc), ctypes.byref(mx), ctypes.byref(npat)), "stgmg_info")
+        return dict(n_classes=nc.value, max_patch_dofs=mx.value, n_patches=npat.value)
+
+    def apply(self, x, y, level=None):
+        lev = self.levels - 1 if level is None else level
+        _check(self.lib.stgmg_apply_operator(self.h, lev, _ptr(x), _ptr(y)), "stgmg_apply_operator")
+
+    def residual(self, b, x, r, level=None):
+        lev = self.levels - 1 if level is None else level
+        _check(self.lib.stgmg_residual(self.h, lev, _ptr(b), _ptr(x), _ptr(r)), "stgmg_residual")
+
+    def smooth_sweep(self, b, d, level=None):
+        lev = self.levels - 1 if level is None else level
+        _check(self.lib.stgmg_smooth_sweep(self.h, lev, _ptr(b), _ptr(d)), "stgmg_smooth_sweep")
+
+    def restrict(self, level, rf, bc):
+        _check(self.lib.stgmg_restrict(self.h, level, _ptr(rf), _ptr(bc)), "stgmg_restrict")
+
+    def prolong_add(self, level, dc, df):
+        _check(self.lib.stgmg_prolong_add(self.h, level, _ptr(dc), _ptr(df)), "stgmg_prolong_add")
+
+    def vcycle(self, b, x):
+        _check(self.lib.stgmg_vcycle(self.h, _ptr(b), _ptr(x)), "stgmg_vcycle")
+
+    def solve(self, rhs, x, tol=None, tol_mode=TOL_REL, restart=None, maxit=1000):
+        st = Stats()
+        rc = _check(self.lib.stgmg_solve(self.h, _ptr(rhs), _ptr(x), float(tol if tol else self.cfg["rtol"]),
+                                         tol_mode, int(restart or self.cfg["restart"]), int(maxit), ctypes.byref(st)),
+                    "stgmg_solve")
+        out = st.as_dict()
+        out["converged"] = rc == STGMG_OK
+        return out
+
+    def solve_host(self, rhs_host, x_host, tol=None, tol_mode=TOL_REL, restart=None, maxit=1000):
+        """rhs_host, x_host: contiguous float64 CPU tensors (pinned for speed) or numpy arrays."""
+        st = Stats()
+
+        def hp(a):
+            try:
+                return ctypes.c_void_p(a.data_ptr())
+            except AttributeError:
+                return a.ctypes.data_as(ctypes.c_void_p)
+
+        rc = _check(self.lib.stgmg_solve_host(self.h, hp(rhs_host), hp(x_host), float(tol if tol else self.cfg["rtol"]),
+                                              tol_mode, int(restart or self.cfg["restart"]), int(maxit),
+                                              ctypes.byref(st)), "stgmg_solve_host")
+        out = st.as_dict()
+        out["converged"] = rc == STGMG_OK
+        return out
+
+    def slab_rhs(self, load, x_prev, rhs):
+        lp = _ptr(load) if load is not None else None
+        _check(self.lib.stgmg_slab_rhs(self.h, lp, _ptr(x_prev), _ptr(rhs)), "stgmg_slab_rhs")
+
+    def launch_count(self):
+        return int(self.lib.stgmg_last_launch_count(self.h))
