@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one space-time slab solve (FGMRES(m) + GMG V-cycle with patch Vanka) per step.
+
+Workload (default): BASELINE.json configs[1] — 2D unit square, 64x64 cells, 6 levels, Q2^2/Q2^2/Q1, dG(1)
+(141,578 DoFs), tau = 0.01, GMRES(30), rel tol 1e-8, load = i.i.d. U[-1,1) seed 1 (reading A21), zero initial
+state; each step forms the slab RHS F_n = L + J X_{n-1} on the device (K8) and solves (slab marching).
+Metric: MDoF*iter/s = N_slab * GMRES iterations / solve time / 1e6; ms_per_step = s/slab.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl ours|reference]
+
+--impl reference runs the oracle (plain fp64 CPU implementation, oracle/) as it stands on the host cores.
+N > 1 (torchrun): every rank solves its own copy of the workload (replicas; the domain-decomposed multi-GPU
+path is not built yet), no data-path collective, scaling "weak".
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from stgmg_inputs import config, uniform_load  # noqa: E402
+
+FP64_PEAK_TFLOPS = 37.19   # measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peak_r01.json)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, lrank
+
+
+# ---------------------------------------------------------------------------------------------- clocks -----
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        self.path = os.path.join("/tmp", "stgmg_clocks_%d_%d.csv" % (os.getpid(), gpu_index))
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def nvml_energy_mj(index):
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        return float(pynvml.nvmlDeviceGetTotalEnergyConsumption(h))
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------------- oracle -----
+def oracle_slab_solver(cfg):
+    """The oracle as it stands (CPU), for the cpu_baseline / --impl reference legs."""
+    from oracle.mg import Hierarchy
+    from oracle.gmres import fgmres
+    from oracle.loads import slab_rhs, end_state
+    d = cfg["dim"]
+    p = dict(cfg["params"])
+    p["K"] = np.array(p["K"], dtype=float).reshape(3, 3)[:d, :d].ravel().tolist()
+    H = Hierarchy(d, cfg["cells"][:d], cfg["lo"][:d], cfg["hi"][:d], cfg["r"], cfg["k"], cfg["levels"], p, cfg["tau"],
+                  bc_u=list(cfg["bc_u"][:2 * d]), bc_p=list(cfg["bc_p"][:2 * d]))
+    S = H.ops[-1].assemble_spatial()
+    lev, op, A = H.fine, H.ops[-1], H.A[-1]
+    L = uniform_load(lev.N, cfg["seed"] or 1)
+    state = {"X": np.zeros(lev.N)}
+
+    def step():
+        U, V, P = end_state(lev, state["X"])
+        b = slab_rhs(lev, S, op.chi_m1, op.th, U, V, P, None, None) + L
+        x, info = fgmres(lambda v: A @ v, b, H.vcycle, tol=cfg["rtol"], restart=cfg["restart"])
+        state["X"] = x
+        return info["iterations"]
+
+    return lev.N, step
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info()]
+        return max(n) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, budget_s=25.0):
+    N, step = oracle_slab_solver(cfg)
+    t0 = time.perf_counter()
+    its, n = 0, 0
+    while True:
+        its += step()
+        n += 1
+        if time.perf_counter() - t0 > budget_s / 2 or n >= 3:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": N * its / dt / 1e6, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle",
+            "sample": "%d slab solve(s) of %s (setup excluded), %.2f s/slab, %d GMRES its" % (n, cfg["name"], dt / n, its)}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = config(args.config)
+    N, step = oracle_slab_solver(cfg)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    its = 0
+    for _ in range(args.steps):
+        its += step()
+    dt = time.perf_counter() - t0
+    val = N * its / dt / 1e6
+    cores = blas_threads()
+    sample = "%d slab solves of %s on host cores (oracle as it stands)" % (args.steps, cfg["name"])
+    out = {"impl": "reference", "metric": "slab_solve_throughput", "value": val, "unit": "MDoF*iter/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg["name"], "dofs": N, "gmres_iterations": its},
+           "cpu_baseline": {"value": val, "unit": "MDoF*iter/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": val, "unit": "MDoF*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------- ours -------
+def run_ours(args):
+    import torch
+    ws, rank, lrank = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(lrank)
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    dev = torch.device("cuda", lrank if ws > 1 else 0)
+    from paper_2303_06742_b200 import Solver
+    cfg = config(args.config)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    t_setup = time.perf_counter()
+    s = Solver(cfg, stream=stream)
+    t_setup = time.perf_counter() - t_setup
+    N = s.size()
+    L = torch.as_tensor(uniform_load(N, cfg["seed"] or 1), device=dev)
+    Xp = torch.zeros(N, dtype=torch.float64, device=dev)
+    rhs = torch.zeros_like(Xp)
+    x = torch.zeros_like(Xp)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # > 126 MB L2
+    rhs_launches = 1 << cfg["dim"]
+
+    def step():
+        s.slab_rhs(L, Xp, rhs)
+        x.zero_()
+        st = s.solve(rhs, x, tol=cfg["rtol"], restart=cfg["restart"])
+        Xp.copy_(x)
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(dev.index)
+    e_start = nvml_energy_mj(dev.index)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    its, launches, resid = 0, 0, []
+    for i in range(args.steps):
+        flush.fill_(float(i))                      # L2 flush between timed steps (untimed)
+        ev0[i].record(stream)
+        st = step()
+        ev1[i].record(stream)
+        its += st["iterations"]
+        resid.append(st["rel_residual"])
+        launches += s.launch_count() + rhs_launches
+    torch.cuda.synchronize()
+    e_end = nvml_energy_mj(dev.index)
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    its_t = torch.tensor([float(its)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.all_reduce(its_t, op=dist.ReduceOp.SUM)
+    t_max_s = float(t_local.item()) * 1e-3
+    value = N * float(its_t.item()) / t_max_s / 1e6        # all ranks' DoF*iterations / max time
+    energy_j = (e_end - e_start) * 1e-3 if (e_start is not None and e_end is not None) else None
+
+    # roofline of the dominant kernel: K2 patch GEMM on the fine level (FP64 DMMA), timed alone
+    work = s.level_work()
+    k2_ms = s.time_kernel(0, reps=50)
+    k2_achieved = work["k2_flops"] / (k2_ms * 1e-3) / 1e12
+    vc_ms = s.time_kernel(3, reps=20)
+    k1_ms = s.time_kernel(1, reps=50)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(cfg["name"])
+        except Exception:
+            traffic = None
+
+    # e2e: the same solve through the C ABI with host buffers (H2D rhs + x, D2H x inside the timed region)
+    rhs_h = torch.empty(N, dtype=torch.float64).pin_memory()
+    x_h = torch.zeros(N, dtype=torch.float64).pin_memory()
+    rhs_h.copy_(L.cpu())
+    e2e_its = 0
+    for _ in range(1):
+        x_h.zero_()
+        s.solve_host(rhs_h, x_h)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x_h.zero_()
+        st = s.solve_host(rhs_h, x_h)
+        e2e_its += st["iterations"]
+    e2e_dt = time.perf_counter() - t0
+    e2e_val = N * e2e_its / e2e_dt / 1e6
+    if ws > 1:
+        tt = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
+        import torch.distributed as dist
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_val = N * e2e_its * ws / float(tt.item()) / 1e6
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg)
+        out = {
+            "metric": "slab_solve_throughput", "value": value, "unit": "MDoF*iter/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max_s * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "dofs": N, "levels": cfg["levels"], "r": cfg["r"], "k": cfg["k"],
+                       "restart": cfg["restart"], "rtol": cfg["rtol"], "load": "uniform[-1,1) seed %s" % cfg["seed"],
+                       "gmres_iterations_total": its, "final_rel_residual_max": max(resid),
+                       "l2": "flushed between timed steps (256 MB write, untimed)",
+                       "parallelism": "replicas" if ws > 1 else "single GPU", "setup_s": t_setup,
+                       "s_per_slab": t_max_s / args.steps,
+                       "vcycle_ms": vc_ms, "k1_fine_apply_ms": k1_ms,
+                       "k1_fine_hbm_gbs": work["k1_bytes"] / (k1_ms * 1e-3) / 1e9},
+            "gpu_launches": launches,
+            "energy": {"joules_per_solve": energy_j / args.steps if energy_j is not None else None,
+                       "source": "NVML total energy (board), timed region incl. L2 flushes"},
+            "roofline": {"kernel": "K2 vanka_patch_gemm (fine level)", "bound": "tensor", "achieved": k2_achieved,
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": k2_achieved / FP64_PEAK_TFLOPS,
+                         "traffic": traffic, "avg_launch_ms": k2_ms, "flops_per_launch": work["k2_flops"],
+                         "algorithmic_bytes_per_launch": work["k2_bytes"],
+                         "peak_source": "FP64 DMMA m8n8k4 microbenchmark on this pool (profiles/fp64_peak_r01.json); "
+                                        "MEASURED_PEAKS.json has no fp64 entry"},
+            "clocks": clk,
+            "e2e": {"value": e2e_val, "unit": "MDoF*iter/s", "h2d_bytes_per_step": 16 * N, "d2h_bytes_per_step": 8 * N},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    s.close()
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

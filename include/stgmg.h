@@ -140,6 +140,15 @@ const char* stgmg_last_error(void);
 int stgmg_info(const stgmg_handle* h, int level, int* n_classes, int* max_patch_dofs, int64_t* n_patches);
 int64_t stgmg_last_launch_count(const stgmg_handle* h);
 
+/* Algorithmic work of one launch on level l (measurement): K2 flops = 2 sum_P C_P^2,
+ * K2 bytes = 8 (2 sum_P C_P) + 8 sum_classes C_P^2 (gather, Y write, class inverses), K1 bytes = 16 N_l. */
+int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double* k2_bytes, double* k1_bytes);
+
+/* Times reps back-to-back launches of one hot-path kernel on level l with CUDA events on params.stream:
+ * kind 0 = K2 patch GEMM, 1 = K1 operator apply (all colours), 2 = K3 averaging, 3 = whole V-cycle graph.
+ * Operates on the level's internal work buffers (their contents are overwritten). */
+int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,12 @@ cudaError_t launch_backsub(const double* H, int ldh, const double* gv, double* y
 cudaError_t launch_update_x(double* x, const double* Z, const double* y, int jn, long long n, cudaStream_t s);
 cudaError_t launch_set_scalar(double* dst, const double* src, cudaStream_t s);
 cudaError_t launch_identity(double* X, long long n, cudaStream_t s);
+cudaError_t launch_noop(int blocks, cudaStream_t s);
+cudaError_t launch_op2d_cells(int r, int k1, const LevelGeom& g, const OpConsts* cdev, const double* x, double* Yc,
+                              int batch, long long stride, long long ycstride, cudaStream_t s);
+cudaError_t launch_op_gather(const LevelGeom& g, int r, int k1, const double* Yc, const double* base, double* y,
+                             double alpha, double beta, int batch, long long stride, long long ycstride,
+                             cudaStream_t s);
 
 // ------------------------------------------------------------------------------ host numerics (1D tables) ----
 static void legendre(int n, double x, double& p, double& dp) {
@@ -249,7 +255,7 @@ using namespace stgmg;
 struct LevelData {
   LevelGeom g;
   double *b = nullptr, *d = nullptr, *r = nullptr, *Y = nullptr;
-  int ldy = 0, lda = 0, maxcp = 0, ntiles = 0;
+  int ldy = 0, lda = 0, maxcp = 0, ntiles = 0, k2var = 0;
   long long npatch = 0;
   std::vector<PatchClass> cls;
   PatchClass* cls_dev = nullptr;
@@ -280,6 +286,9 @@ struct stgmg_handle {
   long long launches = 0;
   std::vector<void*> allocs;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  OpConsts* c_dev = nullptr;    // operator constants (device copy, read by the 2D cell kernel)
+  OpConsts* cj_dev = nullptr;   // slab-RHS variant: T'_ba = chi_b(-1) delta_{a,k}, theta = 0 (K8)
+  double* Yc = nullptr;         // element results of the 2D cell kernel (largest level)
 };
 
 template <typename T>
@@ -317,23 +326,57 @@ static int upload(stgmg_handle* h, T** p, const std::vector<T>& v) {
   } while (0)
 
 // ------------------------------------------------------------------------------------- operator wrappers ----
-static int op_apply(stgmg_handle* h, const LevelGeom& g, const double* x, double* y, double sign, int batch = 1,
-                    long long stride = 0) {
-  int nl = 0;
-  cudaError_t e = launch_op_apply(h->d, h->r, h->k1, g, h->c, x, y, sign, batch, stride, h->s, &nl);
-  h->launches += nl;
-  if (e == cudaErrorNotSupported) {
-    set_error("(d, r, k) combination not compiled");
-    return STGMG_ENOTSUP;
+static long long cell_count(const LevelGeom& g) {
+  long long n = 1;
+  for (int a = 0; a < g.d; ++a) n *= g.n[a];
+  return n;
+}
+
+static long long elem_dofs(const stgmg_handle* h) {
+  long long nq = 1, np = 1;
+  for (int a = 0; a < h->d; ++a) { nq *= (h->r + 1); np *= h->r; }
+  return (long long)h->k1 * (2 * h->d * nq + np);
+}
+
+// y = beta * base + alpha * A_g x  (base may be null).  2D: cell kernel + deterministic node gather.
+static int apply_combo(stgmg_handle* h, const LevelGeom& g, const OpConsts* cdev, const OpConsts& chost,
+                       const double* x, double* y, const double* base, double alpha, double beta, int batch = 1,
+                       long long stride = 0, double* Yc = nullptr) {
+  if (h->d == 2) {
+    double* yc = Yc ? Yc : h->Yc;
+    const long long ycs = cell_count(g) * elem_dofs(h);
+    cudaError_t e = launch_op2d_cells(h->r, h->k1, g, cdev, x, yc, batch, stride, ycs, h->s);
+    if (e == cudaErrorNotSupported) { set_error("(d, r, k) combination not compiled"); return STGMG_ENOTSUP; }
+    CKE(e);
+    CKE(launch_op_gather(g, h->r, h->k1, yc, base, y, alpha, beta, batch, stride, ycs, h->s));
+    h->launches += 2;
+    return 0;
   }
+  // 3D: initialise y then accumulate over the 2^d colours
+  for (int bi = 0; bi < batch; ++bi) {
+    if (base) {
+      CKE(cudaMemcpyAsync(y + bi * stride, base + bi * stride, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, h->s));
+      if (beta != 1.0) { set_error("beta != 1 unsupported on the 3D path"); return STGMG_EINVAL; }
+    } else if (batch == 1) {
+      CKE(cudaMemsetAsync(y, 0, sizeof(double) * g.N, h->s));
+    }
+  }
+  if (!base && batch > 1) CKE(cudaMemsetAsync(y, 0, sizeof(double) * g.N * batch, h->s));
+  int nl = 0;
+  cudaError_t e = launch_op_apply(h->d, h->r, h->k1, g, chost, x, y, alpha, batch, stride, h->s, &nl);
+  h->launches += nl;
+  if (e == cudaErrorNotSupported) { set_error("(d, r, k) combination not compiled"); return STGMG_ENOTSUP; }
   CKE(e);
   return 0;
 }
 
+static int apply_into(stgmg_handle* h, const LevelGeom& g, const double* x, double* y, int batch = 1,
+                      long long stride = 0, double* Yc = nullptr) {
+  return apply_combo(h, g, h->c_dev, h->c, x, y, nullptr, 1.0, 0.0, batch, stride, Yc);
+}
+
 static int residual(stgmg_handle* h, int l, const double* b, const double* x, double* r) {
-  const LevelGeom& g = h->lev[l].g;
-  CKE(cudaMemcpyAsync(r, b, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, h->s));
-  return op_apply(h, g, x, r, -1.0);
+  return apply_combo(h, h->lev[l].g, h->c_dev, h->c, x, r, b, -1.0, 1.0);
 }
 
 static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
@@ -343,7 +386,7 @@ static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_s
     CK(residual(h, l, b, d, L.r));
     rin = L.r;
   }
-  CKE(launch_patch_gemm(L.g, h->r, h->k1, L.cls_dev, L.tiles_dev, L.ntiles, L.relidx_dev, L.inv_dev, L.lda, rin, L.Y,
+  CKE(launch_patch_gemm(L.g, h->r, L.k2var, L.cls_dev, L.tiles_dev, L.ntiles, L.relidx_dev, L.inv_dev, L.lda, rin, L.Y,
                         L.ldy, h->s));
   CKE(launch_vanka_average(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero_start ? 1 : 0, d, h->s));
   h->launches += 2;
@@ -459,14 +502,21 @@ static int build_patches(stgmg_handle* h, int l) {
         Lv.cls.push_back(pc);
       }
   const int ncls = (int)Lv.cls.size();
+  if (Lv.maxcp > 2048) {
+    set_error("patch size C_P > 2048 not supported by the K2 gather table");
+    return STGMG_ENOTSUP;
+  }
   Lv.lda = (Lv.maxcp + 15) / 16 * 16;
   Lv.ldy = Lv.maxcp;
   for (int c = 0; c < ncls; ++c) Lv.cls[c].inv_off = (long long)c * Lv.lda * Lv.lda;
   // tiles
   std::vector<TileDesc> tiles;
+  Lv.k2var = k2_pick_variant(Lv.npatch, Lv.maxcp);
+  int tbm = 0, tbn = 0;
+  k2_tile_shape(Lv.k2var, &tbm, &tbn);
   for (int c = 0; c < ncls; ++c)
-    for (int m0 = 0; m0 < Lv.cls[c].cp; m0 += 64)
-      for (int n0 = 0; n0 < Lv.cls[c].ncols; n0 += 32) tiles.push_back({c, m0, n0, 0});
+    for (int m0 = 0; m0 < Lv.cls[c].cp; m0 += tbm)
+      for (int n0 = 0; n0 < Lv.cls[c].ncols; n0 += tbn) tiles.push_back({c, m0, n0, 0});
   Lv.ntiles = (int)tiles.size();
   CK(upload(h, &Lv.cls_dev, Lv.cls));
   CK(upload(h, &Lv.tiles_dev, tiles));
@@ -481,8 +531,13 @@ static int build_patches(stgmg_handle* h, int l) {
   CKE(cudaMemsetAsync(X, 0, sizeof(double) * Nm * Nm, h->s));
   CKE(cudaMemsetAsync(Ym, 0, sizeof(double) * Nm * Nm, h->s));
   CKE(launch_identity(X, Nm, h->s));
-  int rc = op_apply(h, mini, X, Ym, 1.0, (int)Nm, Nm);
-  if (rc) return rc;
+  {
+    double* Ycb = nullptr;
+    if (h->d == 2) CKE(cudaMalloc(&Ycb, sizeof(double) * Nm * cell_count(mini) * elem_dofs(h)));
+    int rc = apply_into(h, mini, X, Ym, (int)Nm, Nm, Ycb);
+    if (Ycb) { CKE(cudaStreamSynchronize(h->s)); CKE(cudaFree(Ycb)); }
+    if (rc) return rc;
+  }
   int* cps_dev = nullptr;
   long long* offs_dev = nullptr;
   int* mdofs_dev = nullptr;
@@ -525,7 +580,13 @@ static int build_coarse(stgmg_handle* h) {
   CKE(cudaMemsetAsync(X, 0, sizeof(double) * N * N, h->s));
   CKE(cudaMemsetAsync(Ym, 0, sizeof(double) * N * N, h->s));
   CKE(launch_identity(X, N, h->s));
-  CK(op_apply(h, g, X, Ym, 1.0, (int)N, N));
+  {
+    double* Ycb = nullptr;
+    if (h->d == 2) CKE(cudaMalloc(&Ycb, sizeof(double) * N * cell_count(g) * elem_dofs(h)));
+    int rc = apply_into(h, g, X, Ym, (int)N, N, Ycb);
+    if (Ycb) { CKE(cudaStreamSynchronize(h->s)); CKE(cudaFree(Ycb)); }
+    if (rc) return rc;
+  }
   std::vector<int> dofs(N);
   for (long long i = 0; i < N; ++i) dofs[i] = (int)i;
   std::vector<int> cps{(int)N};
@@ -686,6 +747,18 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     CK(dalloc(h.get(), &h->lev[l].d, (size_t)N));
     CK(dalloc(h.get(), &h->lev[l].r, (size_t)N));
   }
+  {
+    OpConsts cj = h->c;
+    for (int b = 0; b < kMaxK1; ++b) {
+      cj.theta[b] = 0.0;
+      for (int a = 0; a < kMaxK1; ++a) cj.T[b][a] = (a == h->k1 - 1) ? h->c.chim1[b] : 0.0;
+    }
+    CK(dalloc(h.get(), &h->c_dev, 1));
+    CK(dalloc(h.get(), &h->cj_dev, 1));
+    CKE(cudaMemcpy(h->c_dev, &h->c, sizeof(OpConsts), cudaMemcpyHostToDevice));
+    CKE(cudaMemcpy(h->cj_dev, &cj, sizeof(OpConsts), cudaMemcpyHostToDevice));
+    if (d == 2) CK(dalloc(h.get(), &h->Yc, (size_t)(cell_count(h->lev[levels - 1].g) * elem_dofs(h.get()))));
+  }
   CK(build_coarse(h.get()));
   for (int l = 1; l < levels; ++l) {
     CK(build_patches(h.get(), l));
@@ -748,8 +821,7 @@ int stgmg_apply_operator(stgmg_handle* h, int level, const double* x, double* y)
   if (!h || level < 0 || level >= h->L || !x || !y) { set_error("bad argument"); return STGMG_EINVAL; }
   const LevelGeom& g = h->lev[level].g;
   h->launches = 0;
-  CKE(cudaMemsetAsync(y, 0, sizeof(double) * g.N, h->s));
-  CK(op_apply(h, g, x, y, 1.0));
+  CK(apply_into(h, g, x, y));
   return sync_if_own(h);
 }
 
@@ -799,9 +871,14 @@ int stgmg_vcycle(stgmg_handle* h, const double* b, double* x) {
 int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, double* rhs) {
   if (!h || !x_prev || !rhs) { set_error("bad argument"); return STGMG_EINVAL; }
   const LevelGeom& g = h->lev[h->L - 1].g;
-  int nl = 0;
-  cudaError_t e = launch_slab_rhs(g, h->k1, h->c, h->r, load, x_prev, rhs, h->s, &nl);
-  CKE(e);
+  h->launches = 0;
+  if (h->d == 2) {
+    CK(apply_combo(h, g, h->cj_dev, h->c, x_prev, rhs, load, 1.0, 1.0));
+  } else {
+    int nl = 0;
+    CKE(launch_slab_rhs(g, h->k1, h->c, h->r, load, x_prev, rhs, h->s, &nl));
+    h->launches += nl;
+  }
   return sync_if_own(h);
 }
 
@@ -838,8 +915,7 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
       double* vj = h->V + (long long)j * N;
       double* zj = h->Z + (long long)j * N;
       CK(vcycle_dev(h, vj, zj));                                          // z_j = M^{-1} v_j
-      CKE(cudaMemsetAsync(h->w, 0, sizeof(double) * N, h->s));
-      CK(op_apply(h, g, zj, h->w, 1.0));                                  // w = A z_j
+      CK(apply_into(h, g, zj, h->w));                                     // w = A z_j
       double* hcol = h->H + (long long)j * ldh;
       for (int i = 0; i <= j; ++i)                                        // modified Gram–Schmidt
         CKE(launch_mgs_dot(h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
@@ -897,6 +973,76 @@ int stgmg_solve_host(stgmg_handle* h, const double* rhs_host, double* x_host, do
   CKE(cudaMemcpyAsync(x_host, stage_x, bytes, cudaMemcpyDeviceToHost, h->s));
   CKE(cudaStreamSynchronize(h->s));
   return rc;
+}
+
+int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double* k2_bytes, double* k1_bytes) {
+  if (!h || level < 0 || level >= h->L) { set_error("bad level"); return STGMG_EINVAL; }
+  const LevelData& Lv = h->lev[level];
+  double fl = 0.0, sumcp = 0.0, invb = 0.0;
+  for (const auto& c : Lv.cls) {
+    fl += 2.0 * (double)c.cp * (double)c.cp * (double)c.ncols;
+    sumcp += (double)c.cp * (double)c.ncols;
+    invb += 8.0 * (double)c.cp * (double)c.cp;
+  }
+  if (k2_flops) *k2_flops = fl;
+  if (k2_bytes) *k2_bytes = 8.0 * 2.0 * sumcp + invb;     // gather R_P r + write Y + read the class inverses
+  if (k1_bytes) *k1_bytes = 16.0 * (double)Lv.g.N;         // y = A x: read x, write y
+  return 0;
+}
+
+int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms) {
+  if (!h || level < 0 || level >= h->L || reps < 1 || !avg_ms) { set_error("bad argument"); return STGMG_EINVAL; }
+  if ((kind == 0 || kind == 2) && level < 1) { set_error("smoother kernels need level >= 1"); return STGMG_EINVAL; }
+  LevelData& Lv = h->lev[level];
+  auto one = [&]() -> int {
+    if (kind == 0) {
+      CKE(launch_patch_gemm(Lv.g, h->r, Lv.k2var, Lv.cls_dev, Lv.tiles_dev, Lv.ntiles, Lv.relidx_dev, Lv.inv_dev, Lv.lda,
+                            Lv.r, Lv.Y, Lv.ldy, h->s));
+    } else if (kind == 1) {
+      CK(apply_into(h, Lv.g, Lv.d, Lv.r));
+    } else if (kind == 2) {
+      CKE(launch_vanka_average(Lv.g, h->r, h->k1, Lv.Y, Lv.ldy, h->prm.omega, 0, Lv.d, h->s));
+    } else if (kind == 4) {
+      CKE(launch_noop(1, h->s));
+    } else if (kind == 5) {
+      CKE(launch_noop(148, h->s));
+    } else {
+      CKE(cudaGraphLaunch(h->vgraph, h->s));
+    }
+    return 0;
+  };
+  CK(one());   // warm-up
+  if (kind == 3) {   // a graph launch cannot be captured: time back-to-back graph launches
+    CKE(cudaEventRecord(h->e0, h->s));
+    for (int i = 0; i < reps; ++i) CK(one());
+    CKE(cudaEventRecord(h->e1, h->s));
+    CKE(cudaEventSynchronize(h->e1));
+    float ms3 = 0.f;
+    CKE(cudaEventElapsedTime(&ms3, h->e0, h->e1));
+    *avg_ms = ms3 / reps;
+    return 0;
+  }
+  // capture the reps launches into a CUDA graph so that host launch overhead does not enter the measurement
+  cudaGraph_t gr;
+  cudaGraphExec_t ge;
+  CKE(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < reps; ++i) {
+    int rc = one();
+    if (rc) { cudaStreamEndCapture(h->s, &gr); return rc; }
+  }
+  CKE(cudaStreamEndCapture(h->s, &gr));
+  CKE(cudaGraphInstantiate(&ge, gr, 0));
+  CKE(cudaGraphLaunch(ge, h->s));
+  CKE(cudaEventRecord(h->e0, h->s));
+  CKE(cudaGraphLaunch(ge, h->s));
+  CKE(cudaEventRecord(h->e1, h->s));
+  CKE(cudaEventSynchronize(h->e1));
+  float ms = 0.f;
+  CKE(cudaEventElapsedTime(&ms, h->e0, h->e1));
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(gr);
+  *avg_ms = ms / reps;
+  return 0;
 }
 
 }  // extern "C"

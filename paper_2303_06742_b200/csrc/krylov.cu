@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(RED_THREADS) mgs_dot_kernel(double* __restrict
                                                               double* __restrict__ out, int do_sqrt) {
   __shared__ double sh[32];
   __shared__ bool last;
+  pdl_wait();
   const double coef = vprev ? *hprev : 0.0;
   double s = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -63,21 +64,21 @@ __global__ void __launch_bounds__(RED_THREADS) mgs_dot_kernel(double* __restrict
 
 cudaError_t launch_mgs_dot(double* w, const double* vprev, const double* hprev, const double* vnext, long long n,
                            double* partials, unsigned* counter, double* out, int do_sqrt, cudaStream_t s) {
-  mgs_dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(w, vprev, hprev, vnext, n, partials, counter, out, do_sqrt);
-  return cudaGetLastError();
+  return launch_pdl(mgs_dot_kernel, dim3(RED_BLOCKS), dim3(RED_THREADS), 0, s, w, vprev, hprev, vnext, n, partials,
+                    counter, out, do_sqrt);
 }
 
 // y = x * (*sc) (invert: y = x / *sc)
 __global__ void scale_kernel(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ sc,
                              int invert, long long n) {
+  pdl_wait();
   const double f = invert ? 1.0 / *sc : *sc;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = x[i] * f;
 }
 
 cudaError_t launch_scale(double* y, const double* x, const double* sc, int invert, long long n, cudaStream_t s) {
-  scale_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(y, x, sc, invert, n);
-  return cudaGetLastError();
+  return launch_pdl(scale_kernel, dim3(RED_BLOCKS), dim3(RED_THREADS), 0, s, y, x, sc, invert, n);
 }
 
 // Givens step for Arnoldi column j of H (column-major, ldh = m+1).  scal[0] = |g_{j+1}|, scal[1] = h_{j+1,j}.
@@ -124,6 +125,7 @@ cudaError_t launch_backsub(const double* H, int ldh, const double* gv, double* y
 // x += sum_j y_j Z_j
 __global__ void update_x_kernel(double* __restrict__ x, const double* __restrict__ Z, const double* __restrict__ y,
                                 int jn, long long n) {
+  pdl_wait();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     double s = x[i];
@@ -133,8 +135,16 @@ __global__ void update_x_kernel(double* __restrict__ x, const double* __restrict
 }
 
 cudaError_t launch_update_x(double* x, const double* Z, const double* y, int jn, long long n, cudaStream_t s) {
-  update_x_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, Z, y, jn, n);
-  return cudaGetLastError();
+  return launch_pdl(update_x_kernel, dim3(RED_BLOCKS), dim3(RED_THREADS), 0, s, x, Z, y, jn, n);
+}
+
+__global__ void noop_kernel(int n, double* out) {
+  pdl_wait();
+  if (threadIdx.x + blockIdx.x * blockDim.x < n && out) out[threadIdx.x] = 0.0;
+}
+
+cudaError_t launch_noop(int blocks, cudaStream_t s) {
+  return launch_pdl(noop_kernel, dim3(blocks), dim3(128), 0, s, 0, (double*)nullptr);
 }
 
 __global__ void set_scalar_kernel(double* dst, const double* src) {

@@ -69,12 +69,34 @@ struct TileDesc {              // one CTA tile of the grouped patch GEMM
 
 void set_error(const std::string& msg);
 
+// Programmatic dependent launch (sm_90+): the next kernel of the stream may begin launching while the previous
+// one drains; every hot kernel calls pdl_wait() before it reads what its predecessor wrote.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---- kernels launchers (each returns cudaError_t of the launch) ----
 // K1: y (+)= sign * A_l x over the cells of one colour (or all colours); batch vectors with stride.
 cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpConsts& c, const double* x,
                             double* y, double sign, int batch, long long stride, cudaStream_t s, int* nlaunch);
-// K2: Y[patch][mu_hat] = Ainv_class * R_P r for all patches (grouped DMMA GEMM).
-cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int k1, const PatchClass* cls_dev, const TileDesc* tiles,
+// K2: Y[patch][mu_hat] = Ainv_class * R_P r for all patches (grouped DMMA GEMM); variant = tile shape.
+int k2_pick_variant(long long npatch, int maxcp);
+void k2_tile_shape(int variant, int* bm, int* bn);
+cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
                               int ntiles, const int* relidx, const double* inv, int lda, const double* rvec,
                               double* Y, int ldy, cudaStream_t s);
 // K3: d <- (zero ? 0 : d) + omega * (sum_P Y_P[mu_hat]) / p_mu   (pull form, lexicographic patch order).

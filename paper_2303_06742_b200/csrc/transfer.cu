@@ -45,6 +45,7 @@ __device__ __forceinline__ long long encode(const LevelGeom& g, int m, int fslot
 // b_c = P^T r_f : one thread per coarse DoF, sum over the fine nodes of its 1D supports.
 __global__ void restrict_kernel(LevelGeom f, LevelGeom c, TransferTables t, const double* __restrict__ rf,
                                 double* __restrict__ bc) {
+  pdl_wait();
   const long long mu = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (mu >= c.N) return;
   const Decoded o = decode(c, mu);
@@ -75,6 +76,7 @@ __global__ void restrict_kernel(LevelGeom f, LevelGeom c, TransferTables t, cons
 // d_f += P d_c : one thread per fine DoF.
 __global__ void prolong_kernel(LevelGeom f, LevelGeom c, TransferTables t, const double* __restrict__ dc,
                                double* __restrict__ df) {
+  pdl_wait();
   const long long mu = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (mu >= f.N) return;
   const Decoded o = decode(f, mu);
@@ -105,20 +107,19 @@ __global__ void prolong_kernel(LevelGeom f, LevelGeom c, TransferTables t, const
 cudaError_t launch_restrict(const LevelGeom& fine, const LevelGeom& coarse, int, const TransferTables& t,
                             const double* rf, double* bc, cudaStream_t s) {
   const int bs = 256;
-  restrict_kernel<<<(unsigned)((coarse.N + bs - 1) / bs), bs, 0, s>>>(fine, coarse, t, rf, bc);
-  return cudaGetLastError();
+  return launch_pdl(restrict_kernel, dim3((unsigned)((coarse.N + bs - 1) / bs)), dim3(bs), 0, s, fine, coarse, t, rf, bc);
 }
 
 cudaError_t launch_prolong_add(const LevelGeom& fine, const LevelGeom& coarse, int, const TransferTables& t,
                                const double* dc, double* df, cudaStream_t s) {
   const int bs = 256;
-  prolong_kernel<<<(unsigned)((fine.N + bs - 1) / bs), bs, 0, s>>>(fine, coarse, t, dc, df);
-  return cudaGetLastError();
+  return launch_pdl(prolong_kernel, dim3((unsigned)((fine.N + bs - 1) / bs)), dim3(bs), 0, s, fine, coarse, t, dc, df);
 }
 
 // K6: y = A x, A row-major (n x n, lda); one warp per row, fixed-order lane partials + shuffle tree.
 __global__ void gemv_kernel(const double* __restrict__ A, int n, int lda, const double* __restrict__ x,
                             double* __restrict__ y) {
+  pdl_wait();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -130,8 +131,7 @@ __global__ void gemv_kernel(const double* __restrict__ A, int n, int lda, const 
 }
 
 cudaError_t launch_gemv(const double* A, int n, int lda, const double* x, double* y, cudaStream_t s) {
-  gemv_kernel<<<(n + 7) / 8, 256, 0, s>>>(A, n, lda, x, y);
-  return cudaGetLastError();
+  return launch_pdl(gemv_kernel, dim3((n + 7) / 8), dim3(256), 0, s, A, n, lda, x, y);
 }
 
 }  // namespace stgmg

@@ -12,7 +12,18 @@
 namespace stgmg {
 
 // ------------------------------------------------------------------------------------------------ K2 --------
-constexpr int GBM = 64, GBN = 32, GBK = 16, GTHREADS = 128;
+// Grouped GEMM  Y[:, P] = Ainv_class * R_P r.  A CTA computes a BM (patch-local rows mu_hat) x BN (patches of one
+// class) tile; K runs in chunks of 16 through a multi-stage cp.async pipeline: the A chunk (rows of the class
+// inverse, row-major, L2-resident) and the gathered B chunk (R_P r; zero-filled beyond C_P / past the last patch)
+// are copied asynchronously into shared memory while the previous chunk is multiplied on the FP64 tensor pipe
+// (mma.sync m8n8k4 -> DMMA.8x8x4).  The class's gather table (C_P ints) is staged in shared memory once per CTA.
+// Tile variants (WM x WN warps, each MT x NT m8n8 tiles) are picked per level by the patch count so that small
+// levels spread over many SMs (latency) and large levels reuse A across many patches (L2 traffic):
+//   big 112 x 64 (2x2 warps of 7x4, split-K 2), medium 56 x 32 (1x2 warps of 7x2, split-K 4),
+//   small 32 x 8 (2x1 warps of 2x1, split-K 4), tall 224 x 32 (4x1 warps of 7x4, split-K 2: every patch vector is
+//   gathered once when C_P <= 224); split-K partial sums are added in a fixed order (deterministic).
+constexpr int K2_BK = 16;
+constexpr int K2_MAXCP = 2048;       // largest C_P whose gather table is staged in shared memory
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -20,127 +31,240 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(GTHREADS) patch_gemm_kernel(LevelGeom g, int r, int k1,
-                                                             const PatchClass* __restrict__ cls,
-                                                             const TileDesc* __restrict__ tiles,
-                                                             const int* __restrict__ relidx,
-                                                             const double* __restrict__ inv, int lda,
-                                                             const double* __restrict__ rvec,
-                                                             double* __restrict__ Y, int ldy) {
-  __shared__ double As[GBK][GBM + 4];
-  __shared__ double Bs[GBK][GBN + 4];
-  __shared__ long long baseQ[GBN], baseP[GBN], plin[GBN];
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;   // src-size 0 -> zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int WM, int WN, int MT, int NT, int STAGES, int KS>
+struct K2Cfg {
+  static constexpr int BM = WM * MT * 8, BN = WN * NT * 8, THREADS = 32 * WM * WN * KS, NSTAGE = STAGES;
+  static constexpr int ASLD = K2_BK + 4;   // 20 doubles: a half-warp's 16 fragment loads hit distinct banks
+  static constexpr int BSLD = K2_BK + 4;   // B staged patch-major [BN][16 + 4] (same conflict-free pattern as A)
+  static constexpr size_t PIPE = sizeof(double) * STAGES * (BM * ASLD + BN * BSLD);
+  static constexpr size_t RED = sizeof(double) * (KS - 1) * BM * BN;   // split-K partial sums (reuses the pipe)
+  static constexpr size_t SMEM = PIPE > RED ? PIPE : RED;
+};
+
+template <int WM, int WN, int MT, int NT, int K2_STAGES, int KS>
+__global__ void __launch_bounds__(32 * WM * WN * KS) patch_gemm_kernel(LevelGeom g, int r,
+                                                                  const PatchClass* __restrict__ cls,
+                                                                  const TileDesc* __restrict__ tiles,
+                                                                  const int* __restrict__ relidx,
+                                                                  const double* __restrict__ inv, int lda,
+                                                                  const double* __restrict__ rvec,
+                                                                  double* __restrict__ Y, int ldy) {
+  using C = K2Cfg<WM, WN, MT, NT, K2_STAGES, KS>;
+  constexpr int BM = C::BM, BN = C::BN, NTH = C::THREADS, ASLD = C::ASLD, BSLD = C::BSLD;
+  extern __shared__ __align__(16) double k2smem[];
+  double(*As)[BM][ASLD] = reinterpret_cast<double(*)[BM][ASLD]>(k2smem);
+  double(*Bs)[BN][BSLD] = reinterpret_cast<double(*)[BN][BSLD]>(k2smem + K2_STAGES * BM * ASLD);
+  __shared__ int baseQ[BN], baseP[BN], plin[BN];
+  __shared__ int srel[K2_MAXCP];
   const TileDesc td = tiles[blockIdx.x];
   const PatchClass pc = cls[td.cls];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int d = g.d;
-  if (tid < GBN) {
-    const int col = td.n0 + tid;
-    long long bq = 0, bp = 0, pl = -1;
+  for (int t = tid; t < BN; t += NTH) {
+    const int col = td.n0 + t;
+    int bq = 0, bp = 0, pl = -1;
     if (col < pc.ncols) {
-      int rem = col;
-      long long vs = 1;
+      int rem = col, vs = 1;
       pl = 0;
       for (int a = 0; a < d; ++a) {
         const int v = pc.vlo[a] + rem % pc.cnt[a];
         rem /= pc.cnt[a];
-        const int c0 = v > 0 ? v - 1 : 0;       // lowest patch cell along a
-        bq += (long long)(r * c0) * g.qs[a];
-        bp += (long long)((r - 1) * c0) * g.ps[a];
-        pl += (long long)v * vs;
+        const int c0 = v > 0 ? v - 1 : 0;   // lowest patch cell along a
+        bq += (r * c0) * (int)g.qs[a];
+        bp += ((r - 1) * c0) * (int)g.ps[a];
+        pl += v * vs;
         vs *= (g.n[a] + 1);
       }
     }
-    baseQ[tid] = bq;
-    baseP[tid] = bp;
-    plin[tid] = pl;
+    baseQ[t] = bq;
+    baseP[t] = bp;
+    plin[t] = pl;
   }
-  __syncthreads();
   const double* A = inv + pc.inv_off;
-  const int* rel = relidx + pc.rel_off;
-  // warp tile: 32 (m) x 16 (n) -> 4 x 2 mma tiles
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
-  double acc[4][2][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int kend = pc.cp;
-  for (int k0 = 0; k0 < kend; k0 += GBK) {
-    // A chunk: rows m0..m0+63, cols k0..k0+15 (zero padded in memory up to lda)
-    for (int i = tid; i < GBM * GBK; i += GTHREADS) {
-      const int mm = i / GBK, kk = i % GBK;
-      const int row = td.m0 + mm, col = k0 + kk;
-      As[kk][mm] = (row < lda && col < lda) ? A[(long long)row * lda + col] : 0.0;
+  const int cp = pc.cp;
+  for (int i = tid; i < cp; i += NTH) srel[i] = __ldg(relidx + pc.rel_off + i);
+  __syncthreads();
+  pdl_wait();
+  const int nchunks = (cp + K2_BK - 1) / K2_BK;
+
+  auto load_chunk = [&](int ch, int buf) {
+    const int k0 = ch * K2_BK;
+    for (int e = tid; e < BM * 8; e += NTH) {          // A: BM rows x 16 doubles (8 x 16 B per row)
+      const int mm = e >> 3, kk = (e & 7) * 2;
+      const int row = td.m0 + mm;
+      const bool ok = row < lda;
+      cp_async16(&As[buf][mm][kk], ok ? A + (long long)row * lda + k0 + kk : A, ok);
     }
-    // B chunk: gathered R_P r
-    for (int i = tid; i < GBK * GBN; i += GTHREADS) {
-      const int kk = i / GBN, nn = i % GBN;
+    for (int e = tid; e < K2_BK * BN; e += NTH) {      // B: 16 rows x BN patches, gathered from r
+      const int kk = e % K2_BK, nn = e / K2_BK;       // lanes run along mu_hat: x-contiguous node runs in r
       const int kr = k0 + kk;
-      double v = 0.0;
-      if (kr < kend && plin[nn] >= 0) {
-        const int code = rel[kr];
-        v = rvec[(code >> 1) + ((code & 1) ? baseP[nn] : baseQ[nn])];
+      const bool ok = (kr < cp) && (plin[nn] >= 0);
+      const double* src = rvec;
+      if (ok) {
+        const int code = srel[kr];
+        src = rvec + (code >> 1) + ((code & 1) ? baseP[nn] : baseQ[nn]);
       }
-      Bs[kk][nn] = v;
+      cp_async8(&Bs[buf][nn][kk], src, ok);
     }
-    __syncthreads();
+    cp_async_commit();
+  };
+
+  const int kslice = warp / (WM * WN);            // split-K: warp group kslice takes k4 steps kslice, kslice+KS, ..
+  const int wt = warp % (WM * WN);
+  const int wm = (wt % WM) * (MT * 8), wn = (wt / WM) * (NT * 8);
+  double acc[MT][NT][2];
 #pragma unroll
-    for (int ks = 0; ks < GBK; ks += 4) {
-      double af[4], bf[2];
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[ks + (lane & 3)][wm + i * 8 + (lane >> 2)];
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[ks + (lane & 3)][wn + j * 8 + (lane >> 2)];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-    __syncthreads();
+  for (int st = 0; st < K2_STAGES - 1; ++st) {
+    if (st < nchunks) load_chunk(st, st);
+    else cp_async_commit();
   }
-  // store: C fragment thread t holds C[t/4][2(t%4) + {0,1}] of each 8x8 tile
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int buf = ch % K2_STAGES;
+    cp_async_wait<K2_STAGES - 2>();
+    __syncthreads();
+    {
+      const int nx = ch + K2_STAGES - 1;   // refill the stage consumed in iteration ch-1
+      if (nx < nchunks) load_chunk(nx, nx % K2_STAGES);
+      else cp_async_commit();
+    }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int ks = kslice * 4; ks < K2_BK; ks += 4 * KS) {
+      double af[MT], bf[NT];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+      for (int i = 0; i < MT; ++i) af[i] = As[buf][wm + i * 8 + (lane >> 2)][ks + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = Bs[buf][wn + j * 8 + (lane >> 2)][ks + (lane & 3)];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  if (KS > 1) {   // deterministic split-K reduction: slices 1..KS-1 park their partial sums, slice 0 adds in order
+    __syncthreads();
+    double* red = k2smem;
+    if (kslice > 0) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            red[((kslice - 1) * BM + wm + i * 8 + (lane >> 2)) * BN + wn + j * 8 + 2 * (lane & 3) + e] = acc[i][j][e];
+    }
+    __syncthreads();
+    if (kslice > 0) return;
+    for (int sl = 1; sl < KS; ++sl)
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            acc[i][j][e] += red[((sl - 1) * BM + wm + i * 8 + (lane >> 2)) * BN + wn + j * 8 + 2 * (lane & 3) + e];
+  }
+  // C fragment: thread t holds C[t/4][2(t%4) + e] of each 8x8 tile
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int row = td.m0 + wm + i * 8 + (lane >> 2);
         const int nn = wn + j * 8 + 2 * (lane & 3) + e;
-        if (row < pc.cp && plin[nn] >= 0) Y[plin[nn] * ldy + row] = acc[i][j][e];
+        if (row < cp && plin[nn] >= 0) Y[(long long)plin[nn] * ldy + row] = acc[i][j][e];
       }
 }
 
-cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int k1, const PatchClass* cls_dev, const TileDesc* tiles,
+template <int WM, int WN, int MT, int NT, int ST, int KS>
+static cudaError_t launch_k2(const LevelGeom& g, int r, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
+                             const int* relidx, const double* inv, int lda, const double* rvec, double* Y, int ldy,
+                             cudaStream_t s) {
+  using C = K2Cfg<WM, WN, MT, NT, ST, KS>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
+    attr = true;
+  }
+  return launch_pdl(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, dim3(ntiles), dim3(C::THREADS), C::SMEM, s, g, r, cls_dev, tiles,
+                    relidx, inv, lda, rvec, Y, ldy);
+}
+
+using K2Big = K2Cfg<2, 2, 7, 4, 3, 2>;     // 112 x 64, 8 warps (2-way split-K)
+using K2Med = K2Cfg<1, 2, 7, 2, 3, 4>;     // 56 x 32, 8 warps (4-way split-K)
+using K2Small = K2Cfg<2, 1, 2, 1, 4, 4>;   // 32 x 8, 8 warps (4-way split-K)
+using K2Tall = K2Cfg<4, 1, 7, 4, 3, 2>;    // 224 x 32, 8 warps (2-way split-K): the whole C_P <= 224 in one tile
+
+void k2_tile_shape(int variant, int* bm, int* bn) {
+  if (variant == 3) { *bm = K2Tall::BM; *bn = K2Tall::BN; }
+  else if (variant == 2) { *bm = K2Big::BM; *bn = K2Big::BN; }
+  else if (variant == 1) { *bm = K2Med::BM; *bn = K2Med::BN; }
+  else { *bm = K2Small::BM; *bn = K2Small::BN; }
+}
+
+int k2_pick_variant(long long npatch, int maxcp) {
+  if (maxcp <= 224 && npatch >= 2000) return 3;
+  if (npatch >= 20000) return 2;
+  if (npatch >= 2000) return 1;
+  return 0;
+}
+
+cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
                               int ntiles, const int* relidx, const double* inv, int lda, const double* rvec,
                               double* Y, int ldy, cudaStream_t s) {
-  patch_gemm_kernel<<<ntiles, GTHREADS, 0, s>>>(g, r, k1, cls_dev, tiles, relidx, inv, lda, rvec, Y, ldy);
-  return cudaGetLastError();
+  if (variant == 3) return launch_k2<4, 1, 7, 4, 3, 2>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
+  if (variant == 2) return launch_k2<2, 2, 7, 4, 3, 2>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
+  if (variant == 1) return launch_k2<1, 2, 7, 2, 3, 4>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
+  return launch_k2<2, 1, 2, 1, 4, 4>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
 }
 
 // ------------------------------------------------------------------------------------------------ K3 --------
 __global__ void vanka_average_kernel(LevelGeom g, int r, int k1, const double* __restrict__ Y, int ldy, double omega,
                                      int zero_init, double* __restrict__ dvec) {
-  const long long mu = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (mu >= g.N) return;
+  const int mu = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
+  if (mu >= (int)g.N) return;
+  const int gblock = (int)g.block, gnq = (int)g.nq, gR2 = (int)(2 * g.R);
   const int d = g.d;
-  const int m = (int)(mu / g.block);
-  long long rem = mu - (long long)m * g.block;
+  const int m = mu / gblock;
+  int rem = mu - m * gblock;
   int fslot;   // 0..2d-1 = (f, c) Q_r components, 2d = pressure
-  long long node;
-  if (rem < 2 * g.R) {
-    fslot = (int)(rem / g.nq);
-    node = rem - (long long)fslot * g.nq;
+  int node;
+  if (rem < gR2) {
+    fslot = rem / gnq;
+    node = rem - fslot * gnq;
   } else {
     fslot = 2 * d;
-    node = rem - 2 * g.R;
+    node = rem - gR2;
   }
   const bool pres = (fslot == 2 * d);
   const int deg = pres ? r - 1 : r;
   int idx[3];
   {
-    long long t = node;
+    int t = node;
     for (int a = 0; a < d; ++a) {
       const int na = pres ? g.pn[a] : g.qn[a];
       idx[a] = (int)(t % na);
@@ -163,31 +287,41 @@ __global__ void vanka_average_kernel(LevelGeom g, int r, int k1, const double* _
       pv[a][np_[a]++] = cc + 1;
     }
   }
-  const int n1 = np_[0], n2 = d > 1 ? np_[1] : 1, n3 = d > 2 ? np_[2] : 1;
-  double z = 0.0;
-  for (int i3 = 0; i3 < n3; ++i3)
-    for (int i2 = 0; i2 < n2; ++i2)
-      for (int i1 = 0; i1 < n1; ++i1) {
-        const int sel[3] = {i1, i2, i3};
-        long long plin = 0, vs = 1;
-        int loc = 0, ls = 1;
-        long long nQ = 1, nP = 1;
-        for (int a = 0; a < d; ++a) {
-          const int v = pv[a][sel[a]];
-          const int lo = v > 0 ? v - 1 : 0;
-          const int ncell = (v > 0 ? 1 : 0) + (v < g.n[a] ? 1 : 0);
-          const int boxa = deg * ncell + 1;
-          loc += (idx[a] - deg * lo) * ls;
-          ls *= boxa;
-          nQ *= r * ncell + 1;
-          nP *= (r - 1) * ncell + 1;
-          plin += (long long)v * vs;
-          vs *= (g.n[a] + 1);
+  for (int a = d; a < 3; ++a) { np_[a] = 1; pv[a][0] = 0; }
+  // issue all (<= 27) loads first, then sum in the fixed lexicographic patch order
+  double yv[27];
+#pragma unroll
+  for (int i3 = 0; i3 < 3; ++i3)
+#pragma unroll
+    for (int i2 = 0; i2 < 3; ++i2)
+#pragma unroll
+      for (int i1 = 0; i1 < 3; ++i1) {
+        const int slot = (i3 * 3 + i2) * 3 + i1;
+        yv[slot] = 0.0;
+        if (i1 < np_[0] && i2 < np_[1] && i3 < np_[2]) {
+          const int sel[3] = {i1, i2, i3};
+          int plin = 0, vs = 1, loc = 0, ls = 1, nQ = 1, nP = 1;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (a >= d) break;
+            const int v = pv[a][sel[a]];
+            const int lo = v > 0 ? v - 1 : 0;
+            const int ncell = (v > 0 ? 1 : 0) + (v < g.n[a] ? 1 : 0);
+            loc += (idx[a] - deg * lo) * ls;
+            ls *= deg * ncell + 1;
+            nQ *= r * ncell + 1;
+            nP *= (r - 1) * ncell + 1;
+            plin += v * vs;
+            vs *= (g.n[a] + 1);
+          }
+          const int blk = 2 * d * nQ + nP;
+          const int muh = m * blk + (pres ? 2 * d * nQ : fslot * nQ) + loc;
+          yv[slot] = __ldg(Y + (long long)plin * ldy + muh);
         }
-        const long long blk = 2 * d * nQ + nP;
-        const long long muh = m * blk + (pres ? 2 * d * nQ : fslot * nQ) + loc;
-        z += Y[plin * ldy + muh];
       }
+  double z = 0.0;
+#pragma unroll
+  for (int i = 0; i < 27; ++i) z += yv[i];
   int p = 1;
   for (int a = 0; a < d; ++a) p *= np_[a];
   const double upd = omega * z / (double)p;
@@ -197,8 +331,8 @@ __global__ void vanka_average_kernel(LevelGeom g, int r, int k1, const double* _
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
                                  int zero_init, double* dvec, cudaStream_t s) {
   const int bs = 256;
-  vanka_average_kernel<<<(unsigned)((g.N + bs - 1) / bs), bs, 0, s>>>(g, r, k1, Y, ldy, omega, zero_init, dvec);
-  return cudaGetLastError();
+  return launch_pdl(vanka_average_kernel, dim3((unsigned)((g.N + bs - 1) / bs)), dim3(bs), 0, s, g, r, k1, Y, ldy, omega,
+                    zero_init, dvec);
 }
 
 // ------------------------------------------------------------------------------------------------ K4 --------

@@ -65,6 +65,10 @@ SIGNATURES = {
     "stgmg_info": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                   ctypes.POINTER(ctypes.c_int64)]),
     "stgmg_last_launch_count": (ctypes.c_int64, [_P]),
+    "stgmg_level_work": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "stgmg_time_kernel": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_double)]),
 }
 
 _lib = None
@@ -226,6 +230,20 @@ class Solver:
     def slab_rhs(self, load, x_prev, rhs):
         lp = _ptr(load) if load is not None else None
         _check(self.lib.stgmg_slab_rhs(self.h, lp, _ptr(x_prev), _ptr(rhs)), "stgmg_slab_rhs")
+
+    def level_work(self, level=None):
+        lev = self.levels - 1 if level is None else level
+        f, bb, b1 = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        _check(self.lib.stgmg_level_work(self.h, lev, ctypes.byref(f), ctypes.byref(bb), ctypes.byref(b1)),
+               "stgmg_level_work")
+        return dict(k2_flops=f.value, k2_bytes=bb.value, k1_bytes=b1.value)
+
+    def time_kernel(self, kind, level=None, reps=20):
+        """Average ms of one launch (kind 0 = K2 patch GEMM, 1 = K1 apply, 2 = K3 average, 3 = V-cycle)."""
+        lev = self.levels - 1 if level is None else level
+        ms = ctypes.c_double()
+        _check(self.lib.stgmg_time_kernel(self.h, kind, lev, reps, ctypes.byref(ms)), "stgmg_time_kernel")
+        return ms.value
 
     def launch_count(self):
         return int(self.lib.stgmg_last_launch_count(self.h))
