@@ -29,11 +29,13 @@ cudaError_t launch_update_x(double* x, const double* Z, const double* y, int jn,
 cudaError_t launch_set_scalar(double* dst, const double* src, cudaStream_t s);
 cudaError_t launch_identity(double* X, long long n, cudaStream_t s);
 cudaError_t launch_noop(int blocks, cudaStream_t s);
+cudaError_t launch_extract_elem(const double* Ycb, long long ycstride, int ne, int ntypes, const long long* rep,
+                                const int* mdofs, double* E, int lda, cudaStream_t s);
 cudaError_t launch_op2d_cells(int r, int k1, const LevelGeom& g, const OpConsts* cdev, const double* x, double* Yc,
                               int batch, long long stride, long long ycstride, cudaStream_t s);
 cudaError_t launch_op_gather(const LevelGeom& g, int r, int k1, const double* Yc, const double* base, double* y,
                              double alpha, double beta, int batch, long long stride, long long ycstride,
-                             cudaStream_t s);
+                             cudaStream_t s, int ldpm);
 
 // ------------------------------------------------------------------------------ host numerics (1D tables) ----
 static void legendre(int n, double x, double& p, double& dp) {
@@ -263,6 +265,13 @@ struct LevelData {
   int* relidx_dev = nullptr;
   double* inv_dev = nullptr;
   TransferTables tt;
+  // 3D operator: per-cell-type element matrices applied as a grouped DMMA GEMM (cells play the role of patches)
+  std::vector<PatchClass> ecls;
+  PatchClass* ecls_dev = nullptr;
+  TileDesc* etiles_dev = nullptr;
+  int entiles = 0, elda = 0, ek2var = 0;
+  int* erelidx_dev = nullptr;
+  double* E_dev = nullptr;
 };
 
 struct stgmg_handle {
@@ -289,6 +298,7 @@ struct stgmg_handle {
   OpConsts* c_dev = nullptr;    // operator constants (device copy, read by the 2D cell kernel)
   OpConsts* cj_dev = nullptr;   // slab-RHS variant: T'_ba = chi_b(-1) delta_{a,k}, theta = 0 (K8)
   double* Yc = nullptr;         // element results of the 2D cell kernel (largest level)
+  double* Ycell = nullptr;      // element results of the 3D element GEMM, patch-major (largest level)
 };
 
 template <typename T>
@@ -338,45 +348,55 @@ static long long elem_dofs(const stgmg_handle* h) {
   return (long long)h->k1 * (2 * h->d * nq + np);
 }
 
-// y = beta * base + alpha * A_g x  (base may be null).  2D: cell kernel + deterministic node gather.
-static int apply_combo(stgmg_handle* h, const LevelGeom& g, const OpConsts* cdev, const OpConsts& chost,
-                       const double* x, double* y, const double* base, double alpha, double beta, int batch = 1,
-                       long long stride = 0, double* Yc = nullptr) {
+// y = beta * base + alpha * A_g x on an arbitrary geometry (setup: mini levels, batched unit vectors; K8).
+// 2D: cell kernel + deterministic node gather; 3D: coloured warp-per-cell kernel.
+static int apply_geom(stgmg_handle* h, const LevelGeom& g, const OpConsts* cdev, const double* x, double* y,
+                      const double* base, double alpha, double beta, int batch = 1, long long stride = 0,
+                      double* Yc = nullptr) {
   if (h->d == 2) {
     double* yc = Yc ? Yc : h->Yc;
     const long long ycs = cell_count(g) * elem_dofs(h);
     cudaError_t e = launch_op2d_cells(h->r, h->k1, g, cdev, x, yc, batch, stride, ycs, h->s);
     if (e == cudaErrorNotSupported) { set_error("(d, r, k) combination not compiled"); return STGMG_ENOTSUP; }
     CKE(e);
-    CKE(launch_op_gather(g, h->r, h->k1, yc, base, y, alpha, beta, batch, stride, ycs, h->s));
+    CKE(launch_op_gather(g, h->r, h->k1, yc, base, y, alpha, beta, batch, stride, ycs, h->s, 0));
     h->launches += 2;
     return 0;
   }
-  // 3D: initialise y then accumulate over the 2^d colours
-  for (int bi = 0; bi < batch; ++bi) {
-    if (base) {
-      CKE(cudaMemcpyAsync(y + bi * stride, base + bi * stride, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, h->s));
-      if (beta != 1.0) { set_error("beta != 1 unsupported on the 3D path"); return STGMG_EINVAL; }
-    } else if (batch == 1) {
-      CKE(cudaMemsetAsync(y, 0, sizeof(double) * g.N, h->s));
-    }
+  if (base) {
+    if (beta != 1.0 || batch != 1) { set_error("3D apply_geom: base needs beta = 1, batch = 1"); return STGMG_EINVAL; }
+    CKE(cudaMemcpyAsync(y, base, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, h->s));
+  } else {
+    CKE(cudaMemsetAsync(y, 0, sizeof(double) * g.N * batch, h->s));
   }
-  if (!base && batch > 1) CKE(cudaMemsetAsync(y, 0, sizeof(double) * g.N * batch, h->s));
   int nl = 0;
-  cudaError_t e = launch_op_apply(h->d, h->r, h->k1, g, chost, x, y, alpha, batch, stride, h->s, &nl);
+  cudaError_t e = launch_op_apply(h->d, h->r, h->k1, g, cdev, x, y, nullptr, alpha, batch, stride, 0, h->s, &nl);
   h->launches += nl;
   if (e == cudaErrorNotSupported) { set_error("(d, r, k) combination not compiled"); return STGMG_ENOTSUP; }
   CKE(e);
   return 0;
 }
 
+// y = beta * base + alpha * A_l x on hierarchy level l (the runtime operator apply, K1).
+static int apply_level(stgmg_handle* h, int l, const double* x, double* y, const double* base, double alpha,
+                       double beta) {
+  if (h->d == 2) return apply_geom(h, h->lev[l].g, h->c_dev, x, y, base, alpha, beta);
+  LevelData& Lv = h->lev[l];
+  const int ne = (int)elem_dofs(h);
+  CKE(launch_patch_gemm(Lv.g, h->r, Lv.ek2var, Lv.ecls_dev, Lv.etiles_dev, Lv.entiles, Lv.erelidx_dev, Lv.E_dev,
+                        Lv.elda, x, h->Ycell, ne, h->s));
+  CKE(launch_op_gather(Lv.g, h->r, h->k1, h->Ycell, base, y, alpha, beta, 1, 0, 0, h->s, ne));
+  h->launches += 2;
+  return 0;
+}
+
 static int apply_into(stgmg_handle* h, const LevelGeom& g, const double* x, double* y, int batch = 1,
                       long long stride = 0, double* Yc = nullptr) {
-  return apply_combo(h, g, h->c_dev, h->c, x, y, nullptr, 1.0, 0.0, batch, stride, Yc);
+  return apply_geom(h, g, h->c_dev, x, y, nullptr, 1.0, 0.0, batch, stride, Yc);
 }
 
 static int residual(stgmg_handle* h, int l, const double* b, const double* x, double* r) {
-  return apply_combo(h, h->lev[l].g, h->c_dev, h->c, x, r, b, -1.0, 1.0);
+  return apply_level(h, l, x, r, b, -1.0, 1.0);
 }
 
 static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
@@ -570,6 +590,118 @@ static int build_patches(stgmg_handle* h, int l) {
   return 0;
 }
 
+// 3D operator setup: per-cell-type element matrices (cell types = per-axis {first, interior, last}, every cell its
+// own type when n < 3), produced by the warp-per-cell sum-factorisation kernel on a min(n,3)^3-cell mini level with
+// the same h and boundary conditions, for every unit vector; applied at run time as a grouped DMMA GEMM.
+static int build_cells(stgmg_handle* h, int l) {
+  LevelData& Lv = h->lev[l];
+  const LevelGeom& g = Lv.g;
+  const int d = h->d, r = h->r, k1 = h->k1;
+  const int ne = (int)elem_dofs(h);
+  struct AxCls { int clo, cnt, rep; };
+  std::vector<AxCls> ax[3];
+  int nmini[3] = {1, 1, 1};
+  for (int a = 0; a < 3; ++a) {
+    if (a >= d) { ax[a].push_back({0, 1, 0}); continue; }
+    const int n = g.n[a];
+    nmini[a] = std::min(n, 3);
+    if (n < 3) {
+      for (int c = 0; c < n; ++c) ax[a].push_back({c, 1, c});
+    } else {
+      ax[a].push_back({0, 1, 0});
+      ax[a].push_back({1, n - 2, 1});
+      ax[a].push_back({n - 1, 1, 2});
+    }
+  }
+  LevelGeom mini = make_geom(d, nmini, g.h, r, k1, g.bcu, g.bcp, h->prm.hF_mode);
+  std::vector<int> relidx, mdofs;
+  std::vector<long long> reps;
+  Lv.ecls.clear();
+  for (auto& cz : ax[2])
+    for (auto& cy : ax[1])
+      for (auto& cx : ax[0]) {
+        const AxCls* A3[3] = {&cx, &cy, &cz};
+        PatchClass pc;
+        std::memset(&pc, 0, sizeof(pc));
+        pc.cp = ne;
+        pc.ncols = 1;
+        pc.rel_off = (long long)relidx.size();
+        long long mbq = 0, mbp = 0, rp = 0, vs = 1;
+        for (int a = 0; a < 3; ++a) {
+          pc.vlo[a] = A3[a]->clo + (a < d ? 1 : 0);   // "vertex" = cell + 1, so that the GEMM's lowest cell is the cell
+          pc.cnt[a] = A3[a]->cnt;
+          pc.cells[a] = 1;
+          pc.ncols *= pc.cnt[a];
+          if (a < d) {
+            mbq += (long long)(r * A3[a]->rep) * mini.qs[a];
+            mbp += (long long)((r - 1) * A3[a]->rep) * mini.ps[a];
+            rp += (long long)(A3[a]->rep + 1) * vs;
+            vs *= nmini[a] + 1;
+          }
+        }
+        reps.push_back(rp);
+        for (int m = 0; m < k1; ++m)
+          for (int slot = 0; slot <= 2 * d; ++slot) {
+            const bool pres = slot == 2 * d;
+            const int n1 = pres ? r : r + 1;
+            int tot = 1;
+            for (int a = 0; a < d; ++a) tot *= n1;
+            for (int e = 0; e < tot; ++e) {
+              int rem = e;
+              long long rel = 0, mrel = 0;
+              for (int a = 0; a < d; ++a) {
+                const int la = rem % n1;
+                rem /= n1;
+                rel += (long long)la * (pres ? g.ps[a] : g.qs[a]);
+                mrel += (long long)la * (pres ? mini.ps[a] : mini.qs[a]);
+              }
+              const long long off = (long long)m * g.block + (pres ? 2 * g.R : (long long)slot * g.nq);
+              const long long moff = (long long)m * mini.block + (pres ? 2 * mini.R : (long long)slot * mini.nq);
+              relidx.push_back((int)(2 * (off + rel) + (pres ? 1 : 0)));
+              mdofs.push_back((int)(moff + mrel + (pres ? mbp : mbq)));
+            }
+          }
+        Lv.ecls.push_back(pc);
+      }
+  const int nt = (int)Lv.ecls.size();
+  Lv.elda = (ne + 15) / 16 * 16;
+  for (int t = 0; t < nt; ++t) Lv.ecls[t].inv_off = (long long)t * Lv.elda * Lv.elda;
+  Lv.ek2var = k2_pick_variant(cell_count(g), ne);
+  int tbm = 0, tbn = 0;
+  k2_tile_shape(Lv.ek2var, &tbm, &tbn);
+  std::vector<TileDesc> tiles;
+  for (int t = 0; t < nt; ++t)
+    for (int m0 = 0; m0 < ne; m0 += tbm)
+      for (int n0 = 0; n0 < Lv.ecls[t].ncols; n0 += tbn) tiles.push_back({t, m0, n0, 0});
+  Lv.entiles = (int)tiles.size();
+  CK(upload(h, &Lv.ecls_dev, Lv.ecls));
+  CK(upload(h, &Lv.etiles_dev, tiles));
+  CK(upload(h, &Lv.erelidx_dev, relidx));
+  CK(dalloc(h, &Lv.E_dev, (size_t)nt * Lv.elda * Lv.elda));
+  // element results of the mini level for every unit vector
+  const long long Nm = mini.N;
+  long long nvm = 1;
+  for (int a = 0; a < d; ++a) nvm *= nmini[a] + 1;
+  const long long ycs = nvm * ne;
+  double *X = nullptr, *Ycb = nullptr;
+  long long* reps_dev = nullptr;
+  int* mdofs_dev = nullptr;
+  CKE(cudaMalloc(&X, sizeof(double) * Nm * Nm));
+  CKE(cudaMalloc(&Ycb, sizeof(double) * Nm * ycs));
+  CKE(cudaMemsetAsync(X, 0, sizeof(double) * Nm * Nm, h->s));
+  CKE(cudaMemsetAsync(Ycb, 0, sizeof(double) * Nm * ycs, h->s));
+  CKE(launch_identity(X, Nm, h->s));
+  int nl = 0;
+  CKE(launch_op_apply(d, r, k1, mini, h->c_dev, X, nullptr, Ycb, 1.0, (int)Nm, Nm, ycs, h->s, &nl));
+  CK(upload(h, &reps_dev, reps));
+  CK(upload(h, &mdofs_dev, mdofs));
+  CKE(launch_extract_elem(Ycb, ycs, ne, nt, reps_dev, mdofs_dev, Lv.E_dev, Lv.elda, h->s));
+  CKE(cudaStreamSynchronize(h->s));
+  CKE(cudaFree(X));
+  CKE(cudaFree(Ycb));
+  return 0;
+}
+
 static int build_coarse(stgmg_handle* h) {
   const LevelGeom& g = h->lev[0].g;
   const long long N = g.N;
@@ -758,6 +890,12 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     CKE(cudaMemcpy(h->c_dev, &h->c, sizeof(OpConsts), cudaMemcpyHostToDevice));
     CKE(cudaMemcpy(h->cj_dev, &cj, sizeof(OpConsts), cudaMemcpyHostToDevice));
     if (d == 2) CK(dalloc(h.get(), &h->Yc, (size_t)(cell_count(h->lev[levels - 1].g) * elem_dofs(h.get()))));
+    if (d == 3) {
+      long long nv = 1;
+      for (int a = 0; a < 3; ++a) nv *= h->lev[levels - 1].g.n[a] + 1;
+      CK(dalloc(h.get(), &h->Ycell, (size_t)(nv * elem_dofs(h.get()))));
+      for (int l = 0; l < levels; ++l) CK(build_cells(h.get(), l));
+    }
   }
   CK(build_coarse(h.get()));
   for (int l = 1; l < levels; ++l) {
@@ -819,9 +957,8 @@ static int sync_if_own(stgmg_handle* h) {
 
 int stgmg_apply_operator(stgmg_handle* h, int level, const double* x, double* y) {
   if (!h || level < 0 || level >= h->L || !x || !y) { set_error("bad argument"); return STGMG_EINVAL; }
-  const LevelGeom& g = h->lev[level].g;
   h->launches = 0;
-  CK(apply_into(h, g, x, y));
+  CK(apply_level(h, level, x, y, nullptr, 1.0, 0.0));
   return sync_if_own(h);
 }
 
@@ -872,13 +1009,7 @@ int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, do
   if (!h || !x_prev || !rhs) { set_error("bad argument"); return STGMG_EINVAL; }
   const LevelGeom& g = h->lev[h->L - 1].g;
   h->launches = 0;
-  if (h->d == 2) {
-    CK(apply_combo(h, g, h->cj_dev, h->c, x_prev, rhs, load, 1.0, 1.0));
-  } else {
-    int nl = 0;
-    CKE(launch_slab_rhs(g, h->k1, h->c, h->r, load, x_prev, rhs, h->s, &nl));
-    h->launches += nl;
-  }
+  CK(apply_geom(h, g, h->cj_dev, x_prev, rhs, load, 1.0, 1.0));
   return sync_if_own(h);
 }
 
@@ -915,7 +1046,7 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
       double* vj = h->V + (long long)j * N;
       double* zj = h->Z + (long long)j * N;
       CK(vcycle_dev(h, vj, zj));                                          // z_j = M^{-1} v_j
-      CK(apply_into(h, g, zj, h->w));                                     // w = A z_j
+      CK(apply_level(h, h->L - 1, zj, h->w, nullptr, 1.0, 0.0));        // w = A z_j
       double* hcol = h->H + (long long)j * ldh;
       for (int i = 0; i <= j; ++i)                                        // modified Gram–Schmidt
         CKE(launch_mgs_dot(h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
@@ -999,7 +1130,7 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
       CKE(launch_patch_gemm(Lv.g, h->r, Lv.k2var, Lv.cls_dev, Lv.tiles_dev, Lv.ntiles, Lv.relidx_dev, Lv.inv_dev, Lv.lda,
                             Lv.r, Lv.Y, Lv.ldy, h->s));
     } else if (kind == 1) {
-      CK(apply_into(h, Lv.g, Lv.d, Lv.r));
+      CK(apply_level(h, level, Lv.d, Lv.r, nullptr, 1.0, 0.0));
     } else if (kind == 2) {
       CKE(launch_vanka_average(Lv.g, h->r, h->k1, Lv.Y, Lv.ldy, h->prm.omega, 0, Lv.d, h->s));
     } else if (kind == 4) {

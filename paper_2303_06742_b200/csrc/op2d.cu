@@ -350,9 +350,10 @@ __global__ void __launch_bounds__(OP2D_CPB * 4) op2d_cell_kernel(LevelGeom g, co
 }
 
 // Phase 2: y[mu] = beta * base[mu] + alpha * sum_{cells K containing mu} Yc[e(K, mu)][K]  (D-generic), one thread
-// per DoF, cells summed in the fixed lexicographic order.
+// per DoF, cells summed in the fixed lexicographic order.  ldpm > 0: element results stored patch-major
+// Yc[plin(K)][ldpm] with plin = lexicographic index of vertex (K + 1) (output of the 3D element GEMM).
 __global__ void op_gather_kernel(LevelGeom g, int r, int k1, const double* __restrict__ Yc, const double* base,
-                                 double* y, double alpha, double beta, long long stride, long long ycstride) {
+                                 double* y, double alpha, double beta, long long stride, long long ycstride, int ldpm) {
   const int mu = blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
   if (mu >= (int)g.N) return;
@@ -409,16 +410,19 @@ __global__ void op_gather_kernel(LevelGeom g, int r, int k1, const double* __res
         yv[slot] = 0.0;
         if (i1 < nc[0] && i2 < nc[1] && i3 < nc[2]) {
           const int sel[3] = {i1, i2, i3};
-          int cell = 0, cs = 1, loc = 0, ls = 1;
+          int cell = 0, cs = 1, loc = 0, ls = 1, plin = 0, vs = 1;
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             if (a >= d) break;
             cell += cc[a][sel[a]] * cs;
             cs *= g.n[a];
+            plin += (cc[a][sel[a]] + 1) * vs;
+            vs *= g.n[a] + 1;
             loc += li[a][sel[a]] * ls;
             ls *= n1;
           }
-          yv[slot] = __ldg(Yc + (long long)(m * ne1 + slot_off + loc) * ncell + cell);
+          const int e = m * ne1 + slot_off + loc;
+          yv[slot] = ldpm ? __ldg(Yc + (long long)plin * ldpm + e) : __ldg(Yc + (long long)e * ncell + cell);
         }
       }
   double s = 0.0;
@@ -451,10 +455,11 @@ cudaError_t launch_op2d_cells(int r, int k1, const LevelGeom& g, const OpConsts*
 
 cudaError_t launch_op_gather(const LevelGeom& g, int r, int k1, const double* Yc, const double* base, double* y,
                              double alpha, double beta, int batch, long long stride, long long ycstride,
-                             cudaStream_t s) {
+                             cudaStream_t s, int ldpm) {
   const int bs = 256;
   dim3 grid((unsigned)((g.N + bs - 1) / bs), (unsigned)batch);
-  return launch_pdl(op_gather_kernel, grid, dim3(bs), 0, s, g, r, k1, Yc, base, y, alpha, beta, stride, ycstride);
+  return launch_pdl(op_gather_kernel, grid, dim3(bs), 0, s, g, r, k1, Yc, base, y, alpha, beta, stride, ycstride,
+                    ldpm);
 }
 
 }  // namespace stgmg

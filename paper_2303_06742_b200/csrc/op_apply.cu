@@ -9,7 +9,9 @@
 // contractions along each axis), Nitsche face terms on Dirichlet boundary faces at (r+1)^{d-1} points.
 //
 // Execution: one warp per cell, warp-synchronous shared-memory sum factorisation, cells of one 2^d colour
-// per launch so that no two cells of a launch share a node (deterministic, no atomics).
+// per launch so that no two cells of a launch share a node (deterministic, no atomics).  In 3D this kernel
+// produces the per-cell-type element matrices at setup (Yc output); the runtime 3D apply multiplies them with
+// the gathered cell vectors on the FP64 tensor pipe (grouped K2 GEMM) and sums them with op_gather_kernel.
 #include "stgmg_internal.cuh"
 
 namespace stgmg {
@@ -83,11 +85,20 @@ __device__ __forceinline__ void contract(const double* __restrict__ in, double* 
 }
 
 template <int D, int R, int K1>
-__global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, OpConsts c, const double* __restrict__ x,
-                                                       double* __restrict__ y, double sign, int color,
-                                                       long long stride) {
+__global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, const OpConsts* __restrict__ cdev,
+                                                       const double* __restrict__ x, double* __restrict__ y,
+                                                       double* __restrict__ Yc, double sign, int color,
+                                                       long long stride, long long ycstride) {
   using T = Tr<D, R, K1>;
   extern __shared__ double smem[];
+  __shared__ OpConsts c;
+  {
+    const double* src = reinterpret_cast<const double*>(cdev);
+    double* dst = reinterpret_cast<double*>(&c);
+    for (int i = threadIdx.x; i < (int)(sizeof(OpConsts) / sizeof(double)); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
@@ -100,7 +111,8 @@ __global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, OpConsts c, 
   double* t2 = t1 + T::TMP;
 
   x += blockIdx.y * stride;
-  y += blockIdx.y * stride;
+  if (y) y += blockIdx.y * stride;
+  if (Yc) Yc += blockIdx.y * ycstride;
 
   // cell of this warp within the colour
   int cnt[3] = {1, 1, 1}, bit[3] = {0, 0, 0};
@@ -387,18 +399,30 @@ __global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, OpConsts c, 
         }
       }
     }
-    // 6. scatter-add the rows of node b (no other cell of this colour touches these nodes)
-    for (int i = lane; i < T::NE1; i += 32) {
-      const long long gi = gidx(b, i);
-      y[gi] = fma(sign, ye[i], y[gi]);
+    // 6. scatter-add the rows of node b (no other cell of this colour touches these nodes), or store the element
+    //    result cell-wise: Yc[plin(cell)][b * NE1 + e], plin = lexicographic index of vertex (cell + 1) (setup of
+    //    the element matrices, patch-major like the patch results Y)
+    if (Yc) {
+      long long plin = 0, vs = 1;
+      for (int a = 0; a < D; ++a) {
+        plin += (long long)(cell[a] + 1) * vs;
+        vs *= g.n[a] + 1;
+      }
+      for (int i = lane; i < T::NE1; i += 32) Yc[plin * T::NE + b * T::NE1 + i] = ye[i];
+    } else {
+      for (int i = lane; i < T::NE1; i += 32) {
+        const long long gi = gidx(b, i);
+        y[gi] = fma(sign, ye[i], y[gi]);
+      }
     }
     __syncwarp();
   }
 }
 
 template <int D, int R, int K1>
-static cudaError_t launch_impl(const LevelGeom& g, const OpConsts& c, const double* x, double* y, double sign,
-                               int batch, long long stride, cudaStream_t s, int* nlaunch) {
+static cudaError_t launch_impl(const LevelGeom& g, const OpConsts* cdev, const double* x, double* y, double* Yc,
+                               double sign, int batch, long long stride, long long ycstride, cudaStream_t s,
+                               int* nlaunch) {
   using T = Tr<D, R, K1>;
   const int wpb = 4;
   const size_t smem = (size_t)wpb * T::SMEM * sizeof(double);
@@ -412,19 +436,21 @@ static cudaError_t launch_impl(const LevelGeom& g, const OpConsts& c, const doub
     for (int a = 0; a < D; ++a) ncol *= (g.n[a] - ((color >> a) & 1) + 1) / 2;
     if (ncol == 0) continue;
     dim3 grid((unsigned)((ncol + wpb - 1) / wpb), (unsigned)batch);
-    op_apply_kernel<D, R, K1><<<grid, wpb * 32, smem, s>>>(g, c, x, y, sign, color, stride);
+    cudaError_t e = launch_pdl(op_apply_kernel<D, R, K1>, grid, dim3(wpb * 32), smem, s, g, cdev, x, y, Yc, sign, color,
+                               stride, ycstride);
     if (nlaunch) ++*nlaunch;
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
-#define STGMG_OP_CASE(D_, R_, K1_) \
-  if (d == D_ && r == R_ && k1 == K1_) return launch_impl<D_, R_, K1_>(g, c, x, y, sign, batch, stride, s, nlaunch);
+#define STGMG_OP_CASE(D_, R_, K1_)                                                                          \
+  if (d == D_ && r == R_ && k1 == K1_)                                                                      \
+    return launch_impl<D_, R_, K1_>(g, cdev, x, y, Yc, sign, batch, stride, ycstride, s, nlaunch);
 
-cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpConsts& c, const double* x, double* y,
-                            double sign, int batch, long long stride, cudaStream_t s, int* nlaunch) {
+cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpConsts* cdev, const double* x, double* y,
+                            double* Yc, double sign, int batch, long long stride, long long ycstride, cudaStream_t s,
+                            int* nlaunch) {
   STGMG_OP_CASE(2, 2, 1)
   STGMG_OP_CASE(2, 2, 2)
   STGMG_OP_CASE(2, 2, 3)
@@ -434,23 +460,6 @@ cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpCo
   STGMG_OP_CASE(3, 2, 1)
   STGMG_OP_CASE(3, 2, 2)
   return cudaErrorNotSupported;
-}
-
-// K8: rhs = load + J X_prev — the mass part of K1 with T'_ba = chi_b(-1) delta_{a,k} and theta = 0.
-cudaError_t launch_slab_rhs(const LevelGeom& g, int k1, const OpConsts& c, int r, const double* load,
-                            const double* xprev, double* rhs, cudaStream_t s, int* nlaunch) {
-  OpConsts cj = c;
-  for (int b = 0; b < kMaxK1; ++b) {
-    cj.theta[b] = 0.0;
-    for (int a = 0; a < kMaxK1; ++a) cj.T[b][a] = (a == k1 - 1) ? c.chim1[b] : 0.0;
-  }
-  cudaError_t e;
-  if (load)
-    e = cudaMemcpyAsync(rhs, load, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, s);
-  else
-    e = cudaMemsetAsync(rhs, 0, sizeof(double) * g.N, s);
-  if (e != cudaSuccess) return e;
-  return launch_op_apply(g.d, r, k1, g, cj, xprev, rhs, 1.0, 1, 0, s, nlaunch);
 }
 
 }  // namespace stgmg

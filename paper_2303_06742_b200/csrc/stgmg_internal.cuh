@@ -90,9 +90,10 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 }
 
 // ---- kernels launchers (each returns cudaError_t of the launch) ----
-// K1: y (+)= sign * A_l x over the cells of one colour (or all colours); batch vectors with stride.
-cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpConsts& c, const double* x,
-                            double* y, double sign, int batch, long long stride, cudaStream_t s, int* nlaunch);
+// K1 (warp per cell, 2^d colours): y += sign * A_l x, or (Yc != null) element results Yc[plin(cell)][NE].
+cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpConsts* cdev, const double* x, double* y,
+                            double* Yc, double sign, int batch, long long stride, long long ycstride, cudaStream_t s,
+                            int* nlaunch);
 // K2: Y[patch][mu_hat] = Ainv_class * R_P r for all patches (grouped DMMA GEMM); variant = tile shape.
 int k2_pick_variant(long long npatch, int maxcp);
 void k2_tile_shape(int variant, int* bm, int* bn);
@@ -120,8 +121,5 @@ cudaError_t launch_prolong_add(const LevelGeom& fine, const LevelGeom& coarse, i
                                const double* dc, double* df, cudaStream_t s);
 // K6: y = A x dense (coarse solve, row-major lda).
 cudaError_t launch_gemv(const double* A, int n, int lda, const double* x, double* y, cudaStream_t s);
-// K8: slab RHS.
-cudaError_t launch_slab_rhs(const LevelGeom& g, int k1, const OpConsts& c, int r, const double* load,
-                            const double* xprev, double* rhs, cudaStream_t s, int* nlaunch);
 
 }  // namespace stgmg

@@ -19,7 +19,7 @@ namespace stgmg {
 // (mma.sync m8n8k4 -> DMMA.8x8x4).  The class's gather table (C_P ints) is staged in shared memory once per CTA.
 // Tile variants (WM x WN warps, each MT x NT m8n8 tiles) are picked per level by the patch count so that small
 // levels spread over many SMs (latency) and large levels reuse A across many patches (L2 traffic):
-//   big 112 x 64 (2x2 warps of 7x4, split-K 2), medium 56 x 32 (1x2 warps of 7x2, split-K 4),
+//   big 112 x 32 (2x2 warps of 7x2, split-K 2, two CTAs per SM), medium 56 x 32 (1x2 warps of 7x2, split-K 4),
 //   small 32 x 8 (2x1 warps of 2x1, split-K 4), tall 224 x 32 (4x1 warps of 7x4, split-K 2: every patch vector is
 //   gathered once when C_P <= 224); split-K partial sums are added in a fixed order (deterministic).
 constexpr int K2_BK = 16;
@@ -58,7 +58,7 @@ struct K2Cfg {
 };
 
 template <int WM, int WN, int MT, int NT, int K2_STAGES, int KS>
-__global__ void __launch_bounds__(32 * WM * WN * KS) patch_gemm_kernel(LevelGeom g, int r,
+__global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) patch_gemm_kernel(LevelGeom g, int r,
                                                                   const PatchClass* __restrict__ cls,
                                                                   const TileDesc* __restrict__ tiles,
                                                                   const int* __restrict__ relidx,
@@ -213,8 +213,8 @@ static cudaError_t launch_k2(const LevelGeom& g, int r, const PatchClass* cls_de
                     relidx, inv, lda, rvec, Y, ldy);
 }
 
-using K2Big = K2Cfg<2, 2, 7, 4, 3, 2>;     // 112 x 64, 8 warps (2-way split-K)
-using K2Med = K2Cfg<1, 2, 7, 2, 3, 4>;     // 56 x 32, 8 warps (4-way split-K)
+using K2Big = K2Cfg<2, 2, 7, 2, 4, 2>;     // 112 x 32, 8 warps (2-way split-K), 2 CTAs / SM
+using K2Med = K2Cfg<1, 2, 7, 2, 4, 4>;     // 56 x 32, 8 warps (4-way split-K), 2 CTAs / SM
 using K2Small = K2Cfg<2, 1, 2, 1, 4, 4>;   // 32 x 8, 8 warps (4-way split-K)
 using K2Tall = K2Cfg<4, 1, 7, 4, 3, 2>;    // 224 x 32, 8 warps (2-way split-K): the whole C_P <= 224 in one tile
 
@@ -227,8 +227,8 @@ void k2_tile_shape(int variant, int* bm, int* bn) {
 
 int k2_pick_variant(long long npatch, int maxcp) {
   if (maxcp <= 224 && npatch >= 2000) return 3;
-  if (npatch >= 20000) return 2;
-  if (npatch >= 2000) return 1;
+  if (npatch >= 2000) return 2;
+  if (npatch >= 1000) return 1;
   return 0;
 }
 
@@ -236,8 +236,8 @@ cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const Patc
                               int ntiles, const int* relidx, const double* inv, int lda, const double* rvec,
                               double* Y, int ldy, cudaStream_t s) {
   if (variant == 3) return launch_k2<4, 1, 7, 4, 3, 2>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
-  if (variant == 2) return launch_k2<2, 2, 7, 4, 3, 2>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
-  if (variant == 1) return launch_k2<1, 2, 7, 2, 3, 4>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
+  if (variant == 2) return launch_k2<2, 2, 7, 2, 4, 2>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
+  if (variant == 1) return launch_k2<1, 2, 7, 2, 4, 4>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
   return launch_k2<2, 1, 2, 1, 4, 4>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
 }
 
@@ -357,6 +357,28 @@ cudaError_t launch_extract_patch(const LevelGeom&, int, int, const double* Adens
                                  int nclass, const int* cps, const long long* rel_offs, const int* dofs, double* inv,
                                  int lda, cudaStream_t s) {
   extract_kernel<<<dim3(lda, nclass), 256, 0, s>>>(Adense, ldA, cps, rel_offs, dofs, inv, lda);
+  return cudaGetLastError();
+}
+
+// Element matrices (3D operator): E[t][e][e'] = Ycb[mdof_t(e') * ycstride + rep_t * ne + e], where Ycb holds the
+// element results of the mini level for every unit vector (column j at offset j * ycstride) and rep_t is the
+// patch-major slot of the representative cell of type t.
+__global__ void extract_elem_kernel(const double* __restrict__ Ycb, long long ycstride, int ne,
+                                    const long long* __restrict__ rep, const int* __restrict__ mdofs, double* E,
+                                    int lda) {
+  const int t = blockIdx.y;
+  const int e = blockIdx.x;
+  double* out = E + (long long)t * lda * lda + (long long)e * lda;
+  for (int j = threadIdx.x; j < lda; j += blockDim.x) {
+    double v = (e == j) ? 1.0 : 0.0;   // identity padding
+    if (e < ne && j < ne) v = Ycb[(long long)mdofs[(long long)t * ne + j] * ycstride + rep[t] * ne + e];
+    out[j] = v;
+  }
+}
+
+cudaError_t launch_extract_elem(const double* Ycb, long long ycstride, int ne, int ntypes, const long long* rep,
+                                const int* mdofs, double* E, int lda, cudaStream_t s) {
+  extract_elem_kernel<<<dim3(lda, ntypes), 128, 0, s>>>(Ycb, ycstride, ne, rep, mdofs, E, lda);
   return cudaGetLastError();
 }
 
