@@ -170,3 +170,44 @@ def test_slab_rhs(pair):
     s.slab_rhs(to_gpu(L), to_gpu(Xp), out)
     torch.cuda.synchronize()
     assert rel(to_np(out), ro) < 1e-13
+
+
+def physical_rhs(cfg, H):
+    """F_1 of the first slab with the config's physical data (readings A20, A23, A25, A26): manufactured solution
+    (configs 0/1/3) or the beam traction (config 4), assembled by the oracle."""
+    import math
+    from oracle.loads import (manufactured_baseline, load_vectors, slab_rhs, interpolate_initial,
+                              traction_face_vector)
+    lev, op = H.fine, H.ops[-1]
+    S = op.assemble_spatial()
+    t_nodes = 0.0 + 0.5 * cfg["tau"] * (op.t_hat + 1.0)
+    if cfg["load"] == "manufactured":
+        sol = manufactured_baseline(lev.d, oracle_params(cfg))
+        U, V, P = interpolate_initial(lev, sol, 0.0)
+        FG = [load_vectors(lev, sol, t) for t in t_nodes]
+        return slab_rhs(lev, S, op.chi_m1, op.th, U, V, P, [f for f, g in FG], [g for f, g in FG])
+    if cfg["load"] == "beam":
+        Z = np.zeros(lev.R), np.zeros(lev.R), np.zeros(lev.S)
+        Fl = [traction_face_vector(lev, 1, lev.d - 1, math.sin(math.pi * t / 2)) for t in t_nodes]
+        return slab_rhs(lev, S, op.chi_m1, op.th, *Z, Fl, None)
+    return None
+
+
+def test_physical_load_solve(pair):
+    """Slab 1 with the config's physical load and initial data: GPU solve vs oracle solve (north_star tolerances)."""
+    import torch
+    from oracle.gmres import fgmres
+    cfg, s, H = pair
+    b = physical_rhs(cfg, H)
+    if b is None:
+        pytest.skip("random-load config")
+    x = torch.zeros(H.fine.N, dtype=torch.float64, device="cuda")
+    st = s.solve(to_gpu(b), x, tol=cfg["rtol"], restart=cfg["restart"])
+    torch.cuda.synchronize()
+    A = H.A[-1]
+    xo, info = fgmres(lambda v: A @ v, b, H.vcycle, tol=cfg["rtol"], restart=cfg["restart"])
+    xg = to_np(x)
+    assert st["converged"] and info["converged"]
+    assert abs(st["iterations"] - info["iterations"]) <= 1
+    assert rel(xg, xo) <= 1e-8
+    assert np.linalg.norm((b - A @ xg) - (b - A @ xo)) / np.linalg.norm(b) <= 1e-10

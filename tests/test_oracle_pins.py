@@ -389,3 +389,33 @@ def test_P16_grid_robustness_cfg0_cfg1():
         _, info = fgmres(lambda v: H.A[-1] @ v, b, H.vcycle, tol=1e-8, restart=30)
         its.append(info["iterations"])
     assert max(its) <= 1.5 * min(its) + 1
+
+
+# ---------------------------------------------------------------- sampled evaluations (full-size parity) ---
+@pytest.mark.parametrize("dim,cells,r,k", [(2, (6, 5), 2, 1), (2, (5, 4), 3, 2), (3, (5, 4, 4), 2, 1)])
+def test_sampled_helpers_match_global_definitions(dim, cells, r, k):
+    """oracle/sampled.py (used at BASELINE sizes) reproduces the assembled-matrix definitions: rows of A x,
+    A_P = A[Z,Z] and one Alg. 1 step at sampled DoFs."""
+    from oracle.sampled import LiteOperator
+    bc = [0, 1, 0, 0, 1, 0][:2 * dim]
+    lev = Level(dim, cells, [0.0] * dim, [1.0] * dim, r, k, bc_u=bc, bc_p=bc[::-1])
+    P3 = P0 | {"K": [0.01, 0, 0, 0, 0.01, 0, 0, 0, 0.01]} if dim == 3 else P0
+    op = SlabOperator(lev, P3, 0.01)
+    A = op.assemble()
+    lite = LiteOperator(lev, P3, 0.01)
+    rng = np.random.default_rng(11)
+    x, b = rng.standard_normal(lev.N), rng.standard_normal(lev.N)
+    rows = rng.choice(lev.N, 25, replace=False)
+    assert np.abs(lite.rows(x, rows) - (A @ x)[rows]).max() < 1e-12 * np.abs(A @ x).max()
+    pa = Patches(lev)
+    for i in (0, len(pa.verts) // 2, len(pa.verts) - 1):
+        Z, AP, _ = lite.patch_system(pa.verts[i])
+        assert np.array_equal(Z, pa.dofs[i])
+        ref = pa.extract(A, i)
+        assert np.abs(AP - ref).max() <= 1e-13 * np.abs(ref).max()
+    sm = VankaSmoother(A, pa, 0.7)
+    d = 1e-3 * rng.standard_normal(lev.N)
+    full = sm.sweep(b, d)
+    sample = rng.choice(lev.N, 6, replace=False)
+    got = lite.sampled_sweep(b, d, sample)
+    assert np.abs(got - full[sample]).max() <= 1e-9 * np.abs(full).max()
