@@ -50,6 +50,8 @@ enum { STGMG_BC_DIRICHLET = 0, STGMG_BC_NEUMANN = 1 };
 enum { STGMG_HF_MEASURE = 0 /* h_F = |K|_d, P:L205 (default) */, STGMG_HF_EDGE = 1 /* h_F = h normal to F */ };
 enum { STGMG_TOL_REL = 0 /* ||r|| <= tol ||b|| (BASELINE) */, STGMG_TOL_ABS = 1 /* ||r|| <= tol */ };
 enum { STGMG_SMOOTH_ADDITIVE = 0 /* Alg. 1 (only variant implemented) */ };
+enum { STGMG_COMM_NCCL = 0 /* nccl_comm is an ncclComm_t */,
+       STGMG_COMM_LOOPBACK = 1 /* nccl_comm is an in-process hub (N emulated ranks on one GPU; tests) */ };
 
 /* Structured box, fine level (nested quad/hex levels, h_l = h_{l-1}/2). */
 typedef struct {
@@ -75,9 +77,10 @@ typedef struct {
   double omega;                      /* Vanka under-relaxation, 0.7; <= 0 -> 0.7 */
   int jmax;                          /* smoothing steps per level, 4; <= 0 -> 4 */
   int smoother;                      /* STGMG_SMOOTH_ADDITIVE */
-  void* nccl_comm;                   /* reserved (multi-GPU); must be NULL in this build */
-  int rank, nranks;                  /* 0, 1 */
+  void* nccl_comm;                   /* multi-GPU: ncclComm_t (STGMG_COMM_NCCL) or loopback hub; NULL if nranks = 1 */
+  int rank, nranks;                  /* x-slab domain decomposition over nranks GPUs */
   void* stream;                      /* cudaStream_t for all work; NULL = default stream */
+  int comm_kind;                     /* STGMG_COMM_NCCL | STGMG_COMM_LOOPBACK */
 } stgmg_params;
 
 typedef struct {
@@ -96,8 +99,15 @@ typedef struct {
 int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, const stgmg_params* params,
                 stgmg_handle** out);
 
-/* Number of slab DoFs N_l of a level (0 = coarse .. levels-1 = fine). */
+/* Number of slab DoFs N_l of a level (0 = coarse .. levels-1 = fine).  Multi-GPU: the DoFs of the rank's x-window
+ * (owned cells plus 3 ghost cells per interior side); vectors passed to the library use this local numbering. */
 int stgmg_local_size(const stgmg_handle* h, int level, int64_t* n_owned);
+
+/* Multi-GPU partition of level l (host-only, no GPU needed): global cells along x, window start (global cell),
+ * owned cells [c0, c1) in window-local cell indices, window cells along x, and whether the level is split
+ * (1) or agglomerated / replicated (0).  A level is split while every rank owns >= 4 cells along x. */
+int stgmg_partition_plan(const stgmg_mesh* mesh, int levels, int level, int rank, int nranks, int* split,
+                         int* gnx, int* w0, int* c0, int* c1, int* nx_window);
 
 /* y = A_l x on level l (matrix-free, Problem 3.1 rediscretised on T_l; reading A14).  x, y: device. */
 int stgmg_apply_operator(stgmg_handle* h, int level, const double* x, double* y);
@@ -134,6 +144,17 @@ int stgmg_destroy(stgmg_handle* h);
 
 /* Thread-local message of the last error. */
 const char* stgmg_last_error(void);
+
+/* NCCL bootstrap (libnccl.so.2 is loaded on first use): rank 0 creates the 128-byte id, the caller broadcasts it
+ * (e.g. torch.distributed), every rank creates its communicator; the caller owns and destroys it. */
+int stgmg_nccl_unique_id(unsigned char id_out[128]);
+int stgmg_nccl_comm_create(const unsigned char id[128], int nranks, int rank, void** comm_out);
+int stgmg_nccl_comm_destroy(void* comm);
+
+/* In-process loopback hub for N emulated ranks on one GPU (tests of the decomposition; one host thread per rank,
+ * each with its own handle and stream; the host synchronises at every exchange). */
+void* stgmg_loopback_hub_create(int nranks);
+void stgmg_loopback_hub_destroy(void* hub);
 
 /* Diagnostics: number of patch classes on level l, their sizes C_P and the number of kernels launched by
  * the last stgmg_solve (for the bench's gpu_launches field). */

@@ -13,6 +13,7 @@
 #include <memory>
 
 #include "../../include/stgmg.h"
+#include "dist.cuh"
 #include "stgmg_internal.cuh"
 
 namespace stgmg {
@@ -21,7 +22,9 @@ static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 cudaError_t launch_mgs_dot(double* w, const double* vprev, const double* hprev, const double* vnext, long long n,
-                           double* partials, unsigned* counter, double* out, int do_sqrt, cudaStream_t s);
+                           double* partials, unsigned* counter, double* out, int do_sqrt, const unsigned char* mask,
+                           cudaStream_t s);
+cudaError_t launch_sqrt(double* v, cudaStream_t s);
 cudaError_t launch_scale(double* y, const double* x, const double* sc, int invert, long long n, cudaStream_t s);
 cudaError_t launch_givens(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, cudaStream_t s);
 cudaError_t launch_backsub(const double* H, int ldh, const double* gv, double* y, int jn, cudaStream_t s);
@@ -250,6 +253,38 @@ static Interp1DHost make_interp(int nc, int deg) {
   return o;
 }
 
+
+// The 1D tables of make_interp restricted to x-windows: fine local nodes [0, nf*deg] = global + w0f*deg, coarse
+// local nodes [0, nc*deg] = global + w0c*deg (entries outside a window are dropped; they only feed ghost values).
+static Interp1DHost make_interp_window(int nc_global, int deg, int w0f, int nf, int w0c, int ncw) {
+  const Interp1DHost G = make_interp(nc_global, deg);
+  Interp1DHost o;
+  o.rp_f.push_back(0);
+  for (int f = 0; f <= nf * deg; ++f) {
+    const int fg = f + w0f * deg;
+    for (int e = G.rp_f[fg]; e < G.rp_f[fg + 1]; ++e) {
+      const int J = G.ci_f[e] - w0c * deg;
+      if (J >= 0 && J <= ncw * deg) {
+        o.ci_f.push_back(J);
+        o.v_f.push_back(G.v_f[e]);
+      }
+    }
+    o.rp_f.push_back((int)o.ci_f.size());
+  }
+  o.rp_c.push_back(0);
+  for (int J = 0; J <= ncw * deg; ++J) {
+    const int Jg = J + w0c * deg;
+    for (int e = G.rp_c[Jg]; e < G.rp_c[Jg + 1]; ++e) {
+      const int f = G.ci_c[e] - w0f * deg;
+      if (f >= 0 && f <= nf * deg) {
+        o.ci_c.push_back(f);
+        o.v_c.push_back(G.v_c[e]);
+      }
+    }
+    o.rp_c.push_back((int)o.ci_c.size());
+  }
+  return o;
+}
 }  // namespace stgmg
 
 using namespace stgmg;
@@ -272,6 +307,14 @@ struct LevelData {
   int entiles = 0, elda = 0, ek2var = 0;
   int* erelidx_dev = nullptr;
   double* E_dev = nullptr;
+  // x-slab domain decomposition; a replicated level has part = false, w0 = 0, gnx = n[0]
+  bool part = false, has_left = false, has_right = false;
+  int gnx = 0, w0 = 0, c0 = 0, c1 = 0;   // global cells along x, window start (global cell), owned cells (local)
+  long long npatch_global = 0, ncell_global = 0;
+  double *sl = nullptr, *sr = nullptr, *rl = nullptr, *rr = nullptr;   // halo message buffers
+  long long nsl = 0, nsr = 0, nrl = 0, nrr = 0;
+  double *agsend = nullptr, *agrecv = nullptr;   // transition to an agglomerated (replicated) coarser level
+  long long nag = 0;
 };
 
 struct stgmg_handle {
@@ -289,7 +332,7 @@ struct stgmg_handle {
          *gv = nullptr, *yv = nullptr, *scal = nullptr, *partials = nullptr;
   unsigned* counter = nullptr;
   double* pinned = nullptr;
-  double *stage_rhs = nullptr, *stage_x = nullptr;
+  double *stage_rhs = nullptr, *stage_x = nullptr, *rhs_int = nullptr;
   cudaGraphExec_t vgraph = nullptr;
   int vgraph_launches = 0;
   long long launches = 0;
@@ -299,7 +342,15 @@ struct stgmg_handle {
   OpConsts* cj_dev = nullptr;   // slab-RHS variant: T'_ba = chi_b(-1) delta_{a,k}, theta = 0 (K8)
   double* Yc = nullptr;         // element results of the 2D cell kernel (largest level)
   double* Ycell = nullptr;      // element results of the 3D element GEMM, patch-major (largest level)
+  // multi-GPU
+  Transport* tr = nullptr;
+  int rank = 0, nranks = 1;
+  unsigned char* mask = nullptr;   // owned fine-level DoFs (Krylov inner products)
+  bool graphable = true;
 };
+
+static constexpr int kGhost = 3;   // ghost cells per interior side: one halo exchange of d per smoothing sweep
+
 
 template <typename T>
 static int dalloc(stgmg_handle* h, T** p, size_t count) {
@@ -399,6 +450,41 @@ static int residual(stgmg_handle* h, int l, const double* b, const double* x, do
   return apply_level(h, l, x, r, b, -1.0, 1.0);
 }
 
+// Ghost refresh of a level vector of the x-slab decomposition (no-op on replicated levels): every rank sends the
+// kGhost cells of owned nodes its neighbours hold as ghosts and overwrites its own ghost nodes.
+static int exchange(stgmg_handle* h, int l, double* v) {
+  LevelData& Lv = h->lev[l];
+  if (!Lv.part || h->nranks == 1) return 0;
+  const int G = kGhost, dq = h->r, dp = h->r - 1, nloc = Lv.g.n[0];
+  if (Lv.has_left) CKE(launch_halo(Lv.g, h->k1, Lv.c0 * dq, G * dq + 1, Lv.c0 * dp, G * dp + 1, v, Lv.sl, 0, h->s));
+  if (Lv.has_right)
+    CKE(launch_halo(Lv.g, h->k1, (Lv.c1 - G) * dq, G * dq, (Lv.c1 - G) * dp, G * dp, v, Lv.sr, 0, h->s));
+  const int rc = h->tr->halo(Lv.sl, Lv.nsl, Lv.sr, Lv.nsr, Lv.rl, Lv.nrl, Lv.rr, Lv.nrr, h->s);
+  if (rc) return rc;
+  if (Lv.has_left) CKE(launch_halo(Lv.g, h->k1, 0, Lv.c0 * dq, 0, Lv.c0 * dp, v, Lv.rl, 1, h->s));
+  if (Lv.has_right)
+    CKE(launch_halo(Lv.g, h->k1, Lv.c1 * dq, (nloc - Lv.c1) * dq + 1, Lv.c1 * dp, (nloc - Lv.c1) * dp + 1, v, Lv.rr, 1,
+                    h->s));
+  h->launches += 2 * ((Lv.has_left ? 1 : 0) + (Lv.has_right ? 1 : 0));
+  return 0;
+}
+
+// Partitioned fine level lf -> replicated coarse level lf-1: every rank restricted into the global coarse vector
+// bc, valid on its owned coarse x-nodes [q oc deg, (q+1) oc deg]; allgather the slabs so that bc is complete.
+static int agglomerate(stgmg_handle* h, int lf, double* bc) {
+  LevelData& F = h->lev[lf];
+  const LevelGeom& gc = h->lev[lf - 1].g;
+  const int oc = h->lev[lf - 1].gnx / h->nranks, dq = h->r, dp = h->r - 1;
+  CKE(launch_halo(gc, h->k1, h->rank * oc * dq, oc * dq + 1, h->rank * oc * dp, oc * dp + 1, bc, F.agsend, 0, h->s));
+  const int rc = h->tr->allgather(F.agsend, F.nag, F.agrecv, h->s);
+  if (rc) return rc;
+  for (int q = 0; q < h->nranks; ++q)
+    CKE(launch_halo(gc, h->k1, q * oc * dq, oc * dq + 1, q * oc * dp, oc * dp + 1, bc, F.agrecv + (long long)q * F.nag, 1,
+                    h->s));
+  h->launches += 1 + h->nranks;
+  return 0;
+}
+
 static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
   LevelData& L = h->lev[l];
   const double* rin = b;
@@ -410,7 +496,7 @@ static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_s
                         L.ldy, h->s));
   CKE(launch_vanka_average(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero_start ? 1 : 0, d, h->s));
   h->launches += 2;
-  return 0;
+  return exchange(h, l, d);
 }
 
 static int enqueue_vcycle(stgmg_handle* h) {
@@ -421,6 +507,8 @@ static int enqueue_vcycle(stgmg_handle* h) {
     CK(residual(h, l, Lv.b, Lv.d, Lv.r));
     CKE(launch_restrict(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, Lv.r, h->lev[l - 1].b, h->s));
     h->launches += 1;
+    if (Lv.part && h->lev[l - 1].part) CK(exchange(h, l - 1, h->lev[l - 1].b));
+    else if (Lv.part) CK(agglomerate(h, l, h->lev[l - 1].b));
   }
   CKE(launch_gemv(h->A0inv, h->n0, h->n0, h->lev[0].b, h->lev[0].d, h->s));
   h->launches += 1;
@@ -531,7 +619,7 @@ static int build_patches(stgmg_handle* h, int l) {
   for (int c = 0; c < ncls; ++c) Lv.cls[c].inv_off = (long long)c * Lv.lda * Lv.lda;
   // tiles
   std::vector<TileDesc> tiles;
-  Lv.k2var = k2_pick_variant(Lv.npatch, Lv.maxcp);
+  Lv.k2var = k2_pick_variant(Lv.npatch_global ? Lv.npatch_global : Lv.npatch, Lv.maxcp);
   int tbm = 0, tbn = 0;
   k2_tile_shape(Lv.k2var, &tbm, &tbn);
   for (int c = 0; c < ncls; ++c)
@@ -666,7 +754,7 @@ static int build_cells(stgmg_handle* h, int l) {
   const int nt = (int)Lv.ecls.size();
   Lv.elda = (ne + 15) / 16 * 16;
   for (int t = 0; t < nt; ++t) Lv.ecls[t].inv_off = (long long)t * Lv.elda * Lv.elda;
-  Lv.ek2var = k2_pick_variant(cell_count(g), ne);
+  Lv.ek2var = k2_pick_variant(Lv.ncell_global ? Lv.ncell_global : cell_count(g), ne);
   int tbm = 0, tbn = 0;
   k2_tile_shape(Lv.ek2var, &tbm, &tbn);
   std::vector<TileDesc> tiles;
@@ -762,7 +850,9 @@ static int build_transfer(stgmg_handle* h, int l) {
         T = Interp1D{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
         continue;
       }
-      Interp1DHost ih = make_interp(cg.n[a], pres ? h->r - 1 : h->r);
+      const int deg = pres ? h->r - 1 : h->r;
+      Interp1DHost ih = (a == 0) ? make_interp_window(h->lev[l - 1].gnx, deg, F.w0, F.g.n[0], h->lev[l - 1].w0, cg.n[0])
+                                 : make_interp(cg.n[a], deg);
       int *rpf, *cif, *rpc, *cic;
       double *vf, *vc;
       CK(upload(h, &rpf, ih.rp_f));
@@ -849,11 +939,20 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       set_error("cells must be divisible by 2^(levels-1) and the box non-degenerate");
       return STGMG_EINVAL;
     }
-  if (params->nccl_comm != nullptr || params->nranks > 1) {
-    set_error("multi-GPU path not built in this round");
+  const int nranks = params->nranks > 1 ? params->nranks : 1;
+  if (nranks > 1 && (params->rank < 0 || params->rank >= nranks || params->nccl_comm == nullptr)) {
+    set_error("multi-GPU: need 0 <= rank < nranks and a communicator (nccl_comm) / loopback hub");
     return STGMG_EINVAL;
   }
   auto h = std::make_unique<stgmg_handle>();
+  h->nranks = nranks;
+  h->rank = nranks > 1 ? params->rank : 0;
+  if (nranks > 1) {
+    h->tr = params->comm_kind == STGMG_COMM_LOOPBACK ? make_loopback_transport(params->nccl_comm, h->rank)
+                                                    : make_nccl_transport(params->nccl_comm, h->rank, nranks);
+    if (!h->tr) return STGMG_ENCCL;
+    h->graphable = h->tr->graph_capturable();
+  }
   h->d = d; h->r = r; h->k = k; h->k1 = k + 1; h->L = levels;
   h->prm = *params;
   if (h->prm.omega <= 0) h->prm.omega = 0.7;
@@ -866,18 +965,86 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   }
   h->c = make_consts(d, r, k, h->prm);
   h->lev.resize(levels);
-  for (int l = 0; l < levels; ++l) {
+  for (int l = levels - 1; l >= 0; --l) {
+    LevelData& Lv = h->lev[l];
     int n[3] = {1, 1, 1};
     double hh[3] = {1, 1, 1};
     for (int a = 0; a < d; ++a) {
       n[a] = mesh->cells[a] >> (levels - 1 - l);
       hh[a] = (mesh->hi[a] - mesh->lo[a]) / n[a];
     }
-    h->lev[l].g = make_geom(d, n, hh, r, h->k1, mesh->bc_u, mesh->bc_p, h->prm.hF_mode);
-    const long long N = h->lev[l].g.N;
-    CK(dalloc(h.get(), &h->lev[l].b, (size_t)N));
-    CK(dalloc(h.get(), &h->lev[l].d, (size_t)N));
-    CK(dalloc(h.get(), &h->lev[l].r, (size_t)N));
+    Lv.gnx = n[0];
+    Lv.npatch_global = 1;
+    Lv.ncell_global = 1;
+    for (int a = 0; a < d; ++a) {
+      Lv.npatch_global *= n[a] + 1;
+      Lv.ncell_global *= n[a];
+    }
+    // x-slab partition: a level is split while every rank owns >= 4 cells along x and all finer
+    // levels are split; coarser levels are agglomerated (replicated on every rank)
+    const bool finer_part = (l == levels - 1) || h->lev[l + 1].part;
+    Lv.part = nranks > 1 && l >= 1 && finer_part && n[0] % nranks == 0 && n[0] / nranks >= 4;
+    int bcu[6], bcp[6];
+    for (int f = 0; f < 6; ++f) { bcu[f] = mesh->bc_u[f]; bcp[f] = mesh->bc_p[f]; }
+    if (Lv.part) {
+      const int own = n[0] / nranks, c0g = h->rank * own, c1g = c0g + own;
+      Lv.has_left = h->rank > 0;
+      Lv.has_right = h->rank < nranks - 1;
+      Lv.w0 = Lv.has_left ? c0g - kGhost : 0;
+      const int w1 = Lv.has_right ? c1g + kGhost : n[0];
+      Lv.c0 = c0g - Lv.w0;
+      Lv.c1 = c1g - Lv.w0;
+      n[0] = w1 - Lv.w0;
+      // artificial window faces carry no boundary terms (their ghost values come from the neighbours)
+      if (Lv.has_left) { bcu[0] = STGMG_BC_NEUMANN; bcp[0] = STGMG_BC_NEUMANN; }
+      if (Lv.has_right) { bcu[1] = STGMG_BC_NEUMANN; bcp[1] = STGMG_BC_NEUMANN; }
+    } else {
+      Lv.w0 = 0;
+      Lv.c0 = 0;
+      Lv.c1 = n[0];
+    }
+    Lv.g = make_geom(d, n, hh, r, h->k1, bcu, bcp, h->prm.hF_mode);
+    if (Lv.part) {   // penalty lengths stay those of the physical mesh
+      for (int f = 0; f < 6; ++f) Lv.g.hF[f] = make_geom(d, n, hh, r, h->k1, mesh->bc_u, mesh->bc_p, h->prm.hF_mode).hF[f];
+    }
+    const long long N = Lv.g.N;
+    CK(dalloc(h.get(), &Lv.b, (size_t)N));
+    CK(dalloc(h.get(), &Lv.d, (size_t)N));
+    CK(dalloc(h.get(), &Lv.r, (size_t)N));
+    CKE(cudaMemset(Lv.b, 0, sizeof(double) * N));
+    CKE(cudaMemset(Lv.d, 0, sizeof(double) * N));
+    CKE(cudaMemset(Lv.r, 0, sizeof(double) * N));
+  }
+  if (nranks > 1 && !h->lev[levels - 1].part) {
+    set_error("multi-GPU: the fine level must split into >= 4 cells per rank along x (cells[0] % nranks == 0)");
+    return STGMG_EINVAL;
+  }
+  if (nranks > 1) {
+    const int G = kGhost, dq = r, dp = r - 1;
+    for (int l = 0; l < levels; ++l) {
+      LevelData& Lv = h->lev[l];
+      if (Lv.part) {
+        Lv.nsl = Lv.has_left ? halo_count(Lv.g, h->k1, G * dq + 1, G * dp + 1) : 0;
+        Lv.nrl = Lv.has_left ? halo_count(Lv.g, h->k1, G * dq, G * dp) : 0;
+        Lv.nsr = Lv.has_right ? halo_count(Lv.g, h->k1, G * dq, G * dp) : 0;
+        Lv.nrr = Lv.has_right ? halo_count(Lv.g, h->k1, G * dq + 1, G * dp + 1) : 0;
+        CK(dalloc(h.get(), &Lv.sl, (size_t)Lv.nsl));
+        CK(dalloc(h.get(), &Lv.sr, (size_t)Lv.nsr));
+        CK(dalloc(h.get(), &Lv.rl, (size_t)Lv.nrl));
+        CK(dalloc(h.get(), &Lv.rr, (size_t)Lv.nrr));
+        if (!h->lev[l - 1].part) {   // transition to the agglomerated levels
+          const int oc = h->lev[l - 1].gnx / nranks;
+          Lv.nag = halo_count(h->lev[l - 1].g, h->k1, oc * dq + 1, oc * dp + 1);
+          CK(dalloc(h.get(), &Lv.agsend, (size_t)Lv.nag));
+          CK(dalloc(h.get(), &Lv.agrecv, (size_t)Lv.nag * nranks));
+        }
+      }
+    }
+    LevelData& F = h->lev[levels - 1];
+    CK(dalloc(h.get(), &h->mask, (size_t)F.g.N));
+    const bool last = !F.has_right;
+    CKE(launch_owned_mask(F.g, F.c0 * dq, F.c1 * dq + (last ? 1 : 0), F.c0 * dp, F.c1 * dp + (last ? 1 : 0), h->mask,
+                          h->s));
   }
   {
     OpConsts cj = h->c;
@@ -907,6 +1074,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   CK(dalloc(h.get(), &h->rv, (size_t)Nf));
   CK(dalloc(h.get(), &h->stage_rhs, (size_t)Nf));
   CK(dalloc(h.get(), &h->stage_x, (size_t)Nf));
+  CK(dalloc(h.get(), &h->rhs_int, (size_t)Nf));
   CK(dalloc(h.get(), &h->scal, 16));
   CK(dalloc(h.get(), &h->partials, 2048));
   CK(dalloc(h.get(), &h->counter, 4));
@@ -914,7 +1082,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   CKE(cudaMallocHost(&h->pinned, 16 * sizeof(double)));
   CKE(cudaEventCreate(&h->e0));
   CKE(cudaEventCreate(&h->e1));
-  CK(capture_vcycle(h.get()));
+  if (h->graphable) CK(capture_vcycle(h.get()));
   CKE(cudaStreamSynchronize(h->s));
   *out = h.release();
   return 0;
@@ -925,6 +1093,7 @@ int stgmg_destroy(stgmg_handle* h) {
   cudaStreamSynchronize(h->s);
   if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
   for (void* p : h->allocs) cudaFree(p);
+  delete h->tr;
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->e0) cudaEventDestroy(h->e0);
   if (h->e1) cudaEventDestroy(h->e1);
@@ -992,9 +1161,13 @@ static int vcycle_dev(stgmg_handle* h, const double* b, double* x) {
   LevelData& F = h->lev[h->L - 1];
   const size_t bytes = sizeof(double) * F.g.N;
   CKE(cudaMemcpyAsync(F.b, b, bytes, cudaMemcpyDeviceToDevice, h->s));
-  CKE(cudaGraphLaunch(h->vgraph, h->s));
+  if (h->vgraph) {
+    CKE(cudaGraphLaunch(h->vgraph, h->s));
+    h->launches += h->vgraph_launches;
+  } else {
+    CK(enqueue_vcycle(h));
+  }
   CKE(cudaMemcpyAsync(x, F.d, bytes, cudaMemcpyDeviceToDevice, h->s));
-  h->launches += h->vgraph_launches;
   return 0;
 }
 
@@ -1013,21 +1186,46 @@ int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, do
   return sync_if_own(h);
 }
 
+// Inner product <w, v> (v == nullptr: ||w||^2, sqrt if norm) over the owned DoFs, summed over the ranks; the MGS
+// update w <- w - (*hprev) vprev is fused into the same pass.
+static int dot(stgmg_handle* h, double* w, const double* vprev, const double* hprev, const double* vnext, double* out,
+               bool norm) {
+  const long long N = h->lev[h->L - 1].g.N;
+  const bool dist = h->nranks > 1;
+  CKE(launch_mgs_dot(w, vprev, hprev, vnext, N, h->partials, h->counter, out, (norm && !dist) ? 1 : 0, h->mask, h->s));
+  h->launches += 1;
+  if (dist) {
+    const int rc = h->tr->allreduce_sum(out, 1, h->s);
+    if (rc) return rc;
+    if (norm) {
+      CKE(launch_sqrt(out, h->s));
+      h->launches += 1;
+    }
+  }
+  return 0;
+}
+
 int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int tol_mode, int restart, int maxit,
                 stgmg_stats* stats) {
   if (!h || !rhs || !x || restart < 1 || maxit < 1 || !(tol > 0)) { set_error("bad argument"); return STGMG_EINVAL; }
   CK(ensure_krylov(h, restart));
-  const LevelGeom& g = h->lev[h->L - 1].g;
+  const int Lf = h->L - 1;
+  const LevelGeom& g = h->lev[Lf].g;
   const long long N = g.N;
   const int m = restart, ldh = m + 1;
   h->launches = 0;
   double* scal = h->scal;     // [0] |g_{j+1}|, [1] h_{j+1,j}, [2] beta, [3] ||b||
   double* hp = h->pinned;
   CKE(cudaEventRecord(h->e0, h->s));
-  CKE(launch_mgs_dot(const_cast<double*>(rhs), nullptr, nullptr, nullptr, N, h->partials, h->counter, scal + 3, 1, h->s));
-  CK(residual(h, h->L - 1, rhs, x, h->rv));
-  CKE(launch_mgs_dot(h->rv, nullptr, nullptr, nullptr, N, h->partials, h->counter, scal + 2, 1, h->s));
-  h->launches += 2;
+  if (h->nranks > 1) {        // ghost values of the right-hand side and of the initial guess
+    if (rhs != h->rhs_int) CKE(cudaMemcpyAsync(h->rhs_int, rhs, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->s));
+    CK(exchange(h, Lf, h->rhs_int));
+    CK(exchange(h, Lf, x));
+    rhs = h->rhs_int;
+  }
+  CK(dot(h, const_cast<double*>(rhs), nullptr, nullptr, nullptr, scal + 3, true));
+  CK(residual(h, Lf, rhs, x, h->rv));
+  CK(dot(h, h->rv, nullptr, nullptr, nullptr, scal + 2, true));
   CKE(cudaMemcpyAsync(hp, scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
   CKE(cudaStreamSynchronize(h->s));
   const double bnorm = hp[3];
@@ -1037,6 +1235,7 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
   bool converged = beta <= target;
   while (!converged && its < maxit) {
     CKE(launch_scale(h->V, h->rv, scal + 2, 1, N, h->s));                 // v_0 = r / beta
+    CK(exchange(h, Lf, h->V));
     CKE(cudaMemsetAsync(h->gv, 0, sizeof(double) * (m + 1), h->s));
     CKE(launch_set_scalar(h->gv, scal + 2, h->s));                        // g_0 = beta
     CKE(cudaMemsetAsync(h->H, 0, sizeof(double) * ldh * m, h->s));
@@ -1046,16 +1245,16 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
       double* vj = h->V + (long long)j * N;
       double* zj = h->Z + (long long)j * N;
       CK(vcycle_dev(h, vj, zj));                                          // z_j = M^{-1} v_j
-      CK(apply_level(h, h->L - 1, zj, h->w, nullptr, 1.0, 0.0));        // w = A z_j
+      CK(apply_level(h, Lf, zj, h->w, nullptr, 1.0, 0.0));               // w = A z_j
       double* hcol = h->H + (long long)j * ldh;
       for (int i = 0; i <= j; ++i)                                        // modified Gram–Schmidt
-        CKE(launch_mgs_dot(h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
-                           h->V + (long long)i * N, N, h->partials, h->counter, hcol + i, 0, h->s));
-      CKE(launch_mgs_dot(h->w, h->V + (long long)j * N, hcol + j, nullptr, N, h->partials, h->counter, hcol + j + 1, 1,
-                         h->s));
+        CK(dot(h, h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
+               h->V + (long long)i * N, hcol + i, false));
+      CK(dot(h, h->w, h->V + (long long)j * N, hcol + j, nullptr, hcol + j + 1, true));
       CKE(launch_givens(h->H, ldh, h->cs, h->sn, h->gv, j, scal, h->s));
       CKE(launch_scale(h->V + (long long)(j + 1) * N, h->w, scal + 1, 1, N, h->s));   // v_{j+1} = w / h_{j+1,j}
-      h->launches += j + 4;
+      h->launches += 2;
+      CK(exchange(h, Lf, h->V + (long long)(j + 1) * N));
       CKE(cudaMemcpyAsync(hp, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
       CKE(cudaStreamSynchronize(h->s));
       ++its;
@@ -1064,9 +1263,9 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
     }
     CKE(launch_backsub(h->H, ldh, h->gv, h->yv, jdone, h->s));
     CKE(launch_update_x(x, h->Z, h->yv, jdone, N, h->s));
-    CK(residual(h, h->L - 1, rhs, x, h->rv));
-    CKE(launch_mgs_dot(h->rv, nullptr, nullptr, nullptr, N, h->partials, h->counter, scal + 2, 1, h->s));
-    h->launches += 3;
+    h->launches += 2;
+    CK(residual(h, Lf, rhs, x, h->rv));
+    CK(dot(h, h->rv, nullptr, nullptr, nullptr, scal + 2, true));
     CKE(cudaMemcpyAsync(hp + 2, scal + 2, sizeof(double), cudaMemcpyDeviceToHost, h->s));
     CKE(cudaStreamSynchronize(h->s));
     beta = hp[2];
@@ -1137,8 +1336,10 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
       CKE(launch_noop(1, h->s));
     } else if (kind == 5) {
       CKE(launch_noop(148, h->s));
-    } else {
+    } else if (h->vgraph) {
       CKE(cudaGraphLaunch(h->vgraph, h->s));
+    } else {
+      CK(enqueue_vcycle(h));
     }
     return 0;
   };
@@ -1175,5 +1376,44 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
   *avg_ms = ms / reps;
   return 0;
 }
+
+int stgmg_partition_plan(const stgmg_mesh* mesh, int levels, int level, int rank, int nranks, int* split, int* gnx,
+                         int* w0, int* c0, int* c1, int* nx_window) {
+  if (!mesh || levels < 1 || level < 0 || level >= levels || nranks < 1 || rank < 0 || rank >= nranks) {
+    set_error("bad argument");
+    return STGMG_EINVAL;
+  }
+  bool finer = true;
+  int out[6] = {0, 0, 0, 0, 0, 0};
+  for (int l = levels - 1; l >= level; --l) {
+    const int n = mesh->cells[0] >> (levels - 1 - l);
+    const bool part = nranks > 1 && l >= 1 && finer && n % nranks == 0 && n / nranks >= 4;
+    finer = part;
+    if (l == level) {
+      if (part) {
+        const int own = n / nranks, a = rank * own, b = a + own;
+        const int ws = rank > 0 ? a - kGhost : 0, we = rank < nranks - 1 ? b + kGhost : n;
+        out[0] = 1; out[1] = n; out[2] = ws; out[3] = a - ws; out[4] = b - ws; out[5] = we - ws;
+      } else {
+        out[0] = 0; out[1] = n; out[2] = 0; out[3] = 0; out[4] = n; out[5] = n;
+      }
+    }
+  }
+  if (split) *split = out[0];
+  if (gnx) *gnx = out[1];
+  if (w0) *w0 = out[2];
+  if (c0) *c0 = out[3];
+  if (c1) *c1 = out[4];
+  if (nx_window) *nx_window = out[5];
+  return 0;
+}
+
+int stgmg_nccl_unique_id(unsigned char id_out[128]) { return nccl_unique_id(id_out); }
+int stgmg_nccl_comm_create(const unsigned char id[128], int nranks, int rank, void** comm_out) {
+  return nccl_comm_create(id, nranks, rank, comm_out);
+}
+int stgmg_nccl_comm_destroy(void* comm) { return nccl_comm_destroy(comm); }
+void* stgmg_loopback_hub_create(int nranks) { return loopback_hub_create(nranks); }
+void stgmg_loopback_hub_destroy(void* hub) { loopback_hub_destroy(hub); }
 
 }  // extern "C"

@@ -21,12 +21,14 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return s;   // valid in thread 0
 }
 
-// w <- w - (*hprev) vprev (if vprev), then out = <w, vnext> (vnext == nullptr: <w, w>; do_sqrt: sqrt).
+// w <- w - (*hprev) vprev (if vprev), then out = <w, vnext> (vnext == nullptr: <w, w>; do_sqrt: sqrt), summed over
+// the DoFs with mask[i] != 0 (owned DoFs of the x-slab decomposition; mask == nullptr: all).
 __global__ void __launch_bounds__(RED_THREADS) mgs_dot_kernel(double* __restrict__ w, const double* __restrict__ vprev,
                                                               const double* __restrict__ hprev,
                                                               const double* __restrict__ vnext, long long n,
                                                               double* __restrict__ partials, unsigned* counter,
-                                                              double* __restrict__ out, int do_sqrt) {
+                                                              double* __restrict__ out, int do_sqrt,
+                                                              const unsigned char* __restrict__ mask) {
   __shared__ double sh[32];
   __shared__ bool last;
   pdl_wait();
@@ -40,7 +42,7 @@ __global__ void __launch_bounds__(RED_THREADS) mgs_dot_kernel(double* __restrict
       w[i] = wi;
     }
     const double vi = vnext ? vnext[i] : wi;
-    s = fma(wi, vi, s);
+    if (!mask || mask[i]) s = fma(wi, vi, s);
   }
   const double bsum = block_sum(s, sh);
   if (threadIdx.x == 0) {
@@ -63,9 +65,19 @@ __global__ void __launch_bounds__(RED_THREADS) mgs_dot_kernel(double* __restrict
 }
 
 cudaError_t launch_mgs_dot(double* w, const double* vprev, const double* hprev, const double* vnext, long long n,
-                           double* partials, unsigned* counter, double* out, int do_sqrt, cudaStream_t s) {
+                           double* partials, unsigned* counter, double* out, int do_sqrt, const unsigned char* mask,
+                           cudaStream_t s) {
   return launch_pdl(mgs_dot_kernel, dim3(RED_BLOCKS), dim3(RED_THREADS), 0, s, w, vprev, hprev, vnext, n, partials,
-                    counter, out, do_sqrt);
+                    counter, out, do_sqrt, mask);
+}
+
+__global__ void sqrt_kernel(double* v) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *v = sqrt(*v);
+}
+
+cudaError_t launch_sqrt(double* v, cudaStream_t s) {
+  sqrt_kernel<<<1, 32, 0, s>>>(v);
+  return cudaGetLastError();
 }
 
 // y = x * (*sc) (invert: y = x / *sc)

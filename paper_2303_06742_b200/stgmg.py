@@ -30,7 +30,7 @@ class Params(ctypes.Structure):
                 ("tau", ctypes.c_double), ("gamma_a", ctypes.c_double), ("gamma_b", ctypes.c_double),
                 ("hF_mode", ctypes.c_int), ("omega", ctypes.c_double), ("jmax", ctypes.c_int),
                 ("smoother", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("rank", ctypes.c_int),
-                ("nranks", ctypes.c_int), ("stream", ctypes.c_void_p)]
+                ("nranks", ctypes.c_int), ("stream", ctypes.c_void_p), ("comm_kind", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -69,6 +69,13 @@ SIGNATURES = {
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "stgmg_time_kernel": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_double)]),
+    "stgmg_partition_plan": (ctypes.c_int, [ctypes.POINTER(Mesh), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 6),
+    "stgmg_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "stgmg_nccl_comm_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+    "stgmg_nccl_comm_destroy": (ctypes.c_int, [_P]),
+    "stgmg_loopback_hub_create": (_P, [ctypes.c_int]),
+    "stgmg_loopback_hub_destroy": (None, [_P]),
 }
 
 _lib = None
@@ -113,25 +120,73 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-class Solver:
-    """One slab system A_n X_n = F_n of a structured configuration (see stgmg_inputs.CONFIGS)."""
+COMM_NCCL, COMM_LOOPBACK = 0, 1
 
-    def __init__(self, cfg, stream=None, tau=None, omega=0.7, jmax=4, hF_mode=HF_MEASURE, levels=None):
+
+def make_mesh(cfg):
+    d = cfg["dim"]
+    m = Mesh()
+    m.dim = d
+    for a in range(3):
+        m.cells[a] = int(cfg["cells"][a]) if a < d else 1
+        m.lo[a] = float(cfg["lo"][a])
+        m.hi[a] = float(cfg["hi"][a])
+    for f in range(6):
+        m.bc_u[f] = int(cfg["bc_u"][f])
+        m.bc_p[f] = int(cfg["bc_p"][f])
+    return m
+
+
+def partition_plan(cfg, level, rank, nranks):
+    """Host-only partition of a level (no GPU): dict(split, gnx, w0, c0, c1, nx_window)."""
+    lib = load_library()
+    outs = [ctypes.c_int() for _ in range(6)]
+    _check(lib.stgmg_partition_plan(ctypes.byref(make_mesh(cfg)), int(cfg["levels"]), level, rank, nranks,
+                                    *[ctypes.byref(o) for o in outs]), "stgmg_partition_plan")
+    return dict(zip(["split", "gnx", "w0", "c0", "c1", "nx_window"], [o.value for o in outs]))
+
+
+def nccl_unique_id():
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.stgmg_nccl_unique_id(buf), "stgmg_nccl_unique_id")
+    return bytes(buf.raw)
+
+
+def nccl_comm_create(uid, nranks, rank):
+    lib = load_library()
+    comm = ctypes.c_void_p()
+    _check(lib.stgmg_nccl_comm_create(ctypes.c_char_p(bytes(uid)), nranks, rank, ctypes.byref(comm)),
+           "stgmg_nccl_comm_create")
+    return comm
+
+
+def nccl_comm_destroy(comm):
+    load_library().stgmg_nccl_comm_destroy(comm)
+
+
+def loopback_hub(nranks):
+    return ctypes.c_void_p(load_library().stgmg_loopback_hub_create(nranks))
+
+
+def loopback_hub_destroy(hub):
+    load_library().stgmg_loopback_hub_destroy(hub)
+
+
+class Solver:
+    """One slab system A_n X_n = F_n of a structured configuration (see stgmg_inputs.CONFIGS).
+
+    Multi-GPU (x-slab decomposition): pass rank, nranks and comm (an NCCL communicator from nccl_comm_create, or a
+    loopback hub with comm_kind=COMM_LOOPBACK); vectors are then the rank's window vectors (stgmg_local_size)."""
+
+    def __init__(self, cfg, stream=None, tau=None, omega=0.7, jmax=4, hF_mode=HF_MEASURE, levels=None,
+                 rank=0, nranks=1, comm=None, comm_kind=COMM_NCCL):
         import torch
         if not torch.cuda.is_available():
             raise StgmgError("no CUDA device: the stgmg product path has no CPU fallback")
         self.lib = load_library()
         self.cfg = cfg
-        d = cfg["dim"]
-        m = Mesh()
-        m.dim = d
-        for a in range(3):
-            m.cells[a] = int(cfg["cells"][a]) if a < d else 1
-            m.lo[a] = float(cfg["lo"][a])
-            m.hi[a] = float(cfg["hi"][a])
-        for f in range(6):
-            m.bc_u[f] = int(cfg["bc_u"][f])
-            m.bc_p[f] = int(cfg["bc_p"][f])
+        m = make_mesh(cfg)
         o = Order(int(cfg["r"]), int(cfg["k"]))
         p = Params()
         pr = cfg["params"]
@@ -148,8 +203,9 @@ class Solver:
         p.omega = omega
         p.jmax = jmax
         p.smoother = 0
-        p.nccl_comm = None
-        p.rank, p.nranks = 0, 1
+        p.nccl_comm = comm
+        p.rank, p.nranks = int(rank), int(nranks)
+        p.comm_kind = int(comm_kind)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         p.stream = ctypes.c_void_p(self.stream.cuda_stream)
         self.levels = int(levels or cfg["levels"])

@@ -1,0 +1,151 @@
+"""Multi-rank parity of the x-slab domain decomposition on one GPU (-m gpu).
+
+N ranks are emulated in one process (one host thread, handle and stream per rank) with the library's loopback
+transport: halo messages and reductions pass through the host, which synchronises at every exchange, so no kernel
+ever waits on another rank.  The same library code path (windows with 3 ghost cells, halo exchange after every
+smoothing sweep, agglomeration of the coarse levels, owned-DoF inner products summed over the ranks) runs with NCCL
+on real multi-GPU boxes.  Parity: iteration counts equal (+-1 allowed for the reordered reductions),
+solutions within 1e-10 of the 1-GPU solve, operator apply / sweep / V-cycle bitwise equal on owned DoFs.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from stgmg_inputs import uniform_load, random_vector
+from tests.gpu_common import small_config, to_gpu, to_np
+from tests.multirank import window_index, scatter_owned
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("cfg1s_2ranks", 1, 2), ("cfg2s_2ranks", 2, 2), ("cfg3s_2ranks", 3, 2), ("cfg4s_2ranks", 4, 2),
+         ("cfg4s_4ranks", 4, 4)]
+
+
+def run_ranks(nranks, fn):
+    out, errs = [None] * nranks, []
+
+    def work(q):
+        try:
+            out[q] = fn(q)
+        except Exception as e:   # pragma: no cover - surfaced below
+            errs.append((q, e))
+
+    ts = [threading.Thread(target=work, args=(q,)) for q in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0][1]
+    return out
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
+def ranks(request):
+    import torch
+    from paper_2303_06742_b200.stgmg import Solver, loopback_hub, loopback_hub_destroy, partition_plan, COMM_LOOPBACK
+    _, ci, P = request.param
+    cfg = small_config(ci)
+    if ci == 4:
+        cfg = dict(cfg, cells=(32, 4, 4), hi=(4.0, 1.0, 1.0))
+    hub = loopback_hub(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+
+    def make(q):
+        with torch.cuda.stream(streams[q]):
+            return Solver(cfg, stream=streams[q], rank=q, nranks=P, comm=hub, comm_kind=COMM_LOOPBACK)
+
+    solvers = run_ranks(P, make)
+    single = Solver(cfg)
+    fine = cfg["levels"] - 1
+    maps = [window_index(cfg, fine, partition_plan(cfg, fine, q, P)) for q in range(P)]
+    for q in range(P):
+        assert solvers[q].size() == len(maps[q][0])
+    yield cfg, P, solvers, streams, single, maps
+    for s in solvers:
+        s.close()
+    single.close()
+    loopback_hub_destroy(hub)
+
+
+def test_multirank_sweep_owned_bitwise(ranks):
+    """One smoothing sweep (with its halo exchange) equals the 1-GPU sweep on every owned DoF."""
+    import torch
+    cfg, P, solvers, streams, single, maps = ranks
+    N = single.size()
+    b, d0 = random_vector(N, 301), random_vector(N, 302, 1e-3)
+    dref = to_gpu(d0)
+    single.smooth_sweep(to_gpu(b), dref)
+    torch.cuda.synchronize()
+
+    def work(q):
+        idx, own = maps[q]
+        with torch.cuda.stream(streams[q]):
+            bl, dl = to_gpu(b[idx]), to_gpu(d0[idx])
+            solvers[q].smooth_sweep(bl, dl)
+            streams[q].synchronize()
+            return to_np(dl)
+
+    loc = run_ranks(P, work)
+    got = np.zeros(N)
+    for q in range(P):
+        scatter_owned(got, loc[q], *maps[q])
+        # ghosts were refreshed by the exchange: they hold the neighbours' owned values
+        assert np.array_equal(loc[q], to_np(dref)[maps[q][0]])
+    assert np.array_equal(got, to_np(dref))
+
+
+def test_multirank_vcycle(ranks):
+    import torch
+    cfg, P, solvers, streams, single, maps = ranks
+    N = single.size()
+    b = uniform_load(N, 303)
+    xref = torch.zeros(N, dtype=torch.float64, device="cuda")
+    single.vcycle(to_gpu(b), xref)
+    torch.cuda.synchronize()
+
+    def work(q):
+        idx, own = maps[q]
+        with torch.cuda.stream(streams[q]):
+            x = torch.zeros(len(idx), dtype=torch.float64, device="cuda")
+            solvers[q].vcycle(to_gpu(b[idx]), x)
+            streams[q].synchronize()
+            return to_np(x)
+
+    loc = run_ranks(P, work)
+    got = np.zeros(N)
+    for q in range(P):
+        scatter_owned(got, loc[q], *maps[q])
+    xr = to_np(xref)
+    assert np.abs(got - xr).max() <= 1e-12 * np.abs(xr).max()
+
+
+def test_multirank_solve(ranks):
+    """FGMRES-GMG slab solve on P emulated ranks vs 1 GPU: same iterations (+-1), solutions within 1e-10."""
+    import torch
+    cfg, P, solvers, streams, single, maps = ranks
+    N = single.size()
+    b = uniform_load(N, 304)
+    xref = torch.zeros(N, dtype=torch.float64, device="cuda")
+    st_ref = single.solve(to_gpu(b), xref, tol=cfg["rtol"], restart=cfg["restart"])
+    torch.cuda.synchronize()
+
+    def work(q):
+        idx, own = maps[q]
+        with torch.cuda.stream(streams[q]):
+            x = torch.zeros(len(idx), dtype=torch.float64, device="cuda")
+            st = solvers[q].solve(to_gpu(b[idx]), x, tol=cfg["rtol"], restart=cfg["restart"])
+            streams[q].synchronize()
+            return st, to_np(x)
+
+    res = run_ranks(P, work)
+    its = {r[0]["iterations"] for r in res}
+    assert len(its) == 1                               # every rank takes the same control flow
+    assert abs(its.pop() - st_ref["iterations"]) <= 1
+    assert all(r[0]["converged"] for r in res)
+    got = np.zeros(N)
+    for q in range(P):
+        scatter_owned(got, res[q][1], *maps[q])
+    xr = to_np(xref)
+    assert np.linalg.norm(got - xr) <= 1e-10 * np.linalg.norm(xr)
