@@ -6,7 +6,10 @@
 //   vcycle  : P:L435-440 with Algorithm 1 on l = L..1 and the coarse direct solve on T_0.
 //   solve   : flexible GMRES(m), right preconditioned (readings A2-A4, A35).
 #include <algorithm>
+#include <array>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -32,6 +35,10 @@ cudaError_t launch_update_x(double* x, const double* Z, const double* y, int jn,
 cudaError_t launch_set_scalar(double* dst, const double* src, cudaStream_t s);
 cudaError_t launch_identity(double* X, long long n, cudaStream_t s);
 cudaError_t launch_noop(int blocks, cudaStream_t s);
+cudaError_t launch_csr_spmv(int nrows, int lpr, const int* rp, const int* ci, const double* v, const double* x,
+                            const double* base, double* y, double alpha, double beta, cudaStream_t s);
+cudaError_t launch_avg_table(int d, int N, const int* tab, const double* Y, double omega, int zero_init, double* dvec,
+                             cudaStream_t s);
 cudaError_t launch_extract_elem(const double* Ycb, long long ycstride, int ne, int ntypes, const long long* rep,
                                 const int* mdofs, double* E, int lda, cudaStream_t s);
 cudaError_t launch_op2d_cells(int r, int k1, const LevelGeom& g, const OpConsts* cdev, const double* x, double* Yc,
@@ -292,7 +299,7 @@ using namespace stgmg;
 struct LevelData {
   LevelGeom g;
   double *b = nullptr, *d = nullptr, *r = nullptr, *Y = nullptr;
-  int ldy = 0, lda = 0, maxcp = 0, ntiles = 0, k2var = 0;
+  int ldy = 0, lda = 0, maxcp = 0, ntiles = 0, k2var = 0, cn = 1;
   long long npatch = 0;
   std::vector<PatchClass> cls;
   PatchClass* cls_dev = nullptr;
@@ -304,7 +311,7 @@ struct LevelData {
   std::vector<PatchClass> ecls;
   PatchClass* ecls_dev = nullptr;
   TileDesc* etiles_dev = nullptr;
-  int entiles = 0, elda = 0, ek2var = 0;
+  int entiles = 0, elda = 0, ek2var = 0, ecn = 1;
   int* erelidx_dev = nullptr;
   double* E_dev = nullptr;
   // x-slab domain decomposition; a replicated level has part = false, w0 = 0, gnx = n[0]
@@ -315,6 +322,15 @@ struct LevelData {
   long long nsl = 0, nsr = 0, nrl = 0, nrr = 0;
   double *agsend = nullptr, *agrecv = nullptr;   // transition to an agglomerated (replicated) coarser level
   long long nag = 0;
+  // small-level fast path (csrc/small.cu): assembled CSR operator, CSR transfers to/from level l-1, averaging table
+  Interp1DHost ih_q[3], ih_p[3];                 // host copies of the 1D transfer tables (CSR assembly)
+  int *A_rp = nullptr, *A_ci = nullptr, A_lpr = 32;
+  double* A_v = nullptr;
+  int *P_rp = nullptr, *P_ci = nullptr, P_lpr = 4;   // prolongation: rows = DoFs of this level
+  double* P_v = nullptr;
+  int *R_rp = nullptr, *R_ci = nullptr, R_lpr = 8;   // restriction: rows = DoFs of level l-1
+  double* R_v = nullptr;
+  int* k3tab = nullptr;
 };
 
 struct stgmg_handle {
@@ -347,6 +363,7 @@ struct stgmg_handle {
   int rank = 0, nranks = 1;
   unsigned char* mask = nullptr;   // owned fine-level DoFs (Krylov inner products)
   bool graphable = true;
+  int nsm = 148;                   // SMs of the device (tile balancing)
 };
 
 static constexpr int kGhost = 3;   // ghost cells per interior side: one halo exchange of d per smoothing sweep
@@ -431,11 +448,17 @@ static int apply_geom(stgmg_handle* h, const LevelGeom& g, const OpConsts* cdev,
 // y = beta * base + alpha * A_l x on hierarchy level l (the runtime operator apply, K1).
 static int apply_level(stgmg_handle* h, int l, const double* x, double* y, const double* base, double alpha,
                        double beta) {
+  if (h->lev[l].A_rp) {   // small level: assembled operator, one SpMV
+    const LevelData& Ls = h->lev[l];
+    CKE(launch_csr_spmv((int)Ls.g.N, Ls.A_lpr, Ls.A_rp, Ls.A_ci, Ls.A_v, x, base, y, alpha, beta, h->s));
+    h->launches += 1;
+    return 0;
+  }
   if (h->d == 2) return apply_geom(h, h->lev[l].g, h->c_dev, x, y, base, alpha, beta);
   LevelData& Lv = h->lev[l];
   const int ne = (int)elem_dofs(h);
   CKE(launch_patch_gemm(Lv.g, h->r, Lv.ek2var, Lv.ecls_dev, Lv.etiles_dev, Lv.entiles, Lv.erelidx_dev, Lv.E_dev,
-                        Lv.elda, x, h->Ycell, ne, h->s));
+                        Lv.elda, x, h->Ycell, ne, Lv.ecn, h->s));
   CKE(launch_op_gather(Lv.g, h->r, h->k1, h->Ycell, base, y, alpha, beta, 1, 0, 0, h->s, ne));
   h->launches += 2;
   return 0;
@@ -485,6 +508,37 @@ static int agglomerate(stgmg_handle* h, int lf, double* bc) {
   return 0;
 }
 
+// K5 restriction b_{l-1} = P^T r_l, K5 prolongation d_l += P d_{l-1}, K3 averaging (small levels: table driven)
+static int restrict_level(stgmg_handle* h, int l, const double* rf, double* bc) {
+  LevelData& Lv = h->lev[l];
+  if (Lv.R_rp)
+    CKE(launch_csr_spmv((int)h->lev[l - 1].g.N, Lv.R_lpr, Lv.R_rp, Lv.R_ci, Lv.R_v, rf, nullptr, bc, 1.0, 0.0, h->s));
+  else
+    CKE(launch_restrict(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, rf, bc, h->s));
+  h->launches += 1;
+  return 0;
+}
+
+static int prolong_level(stgmg_handle* h, int l, const double* dc, double* df) {
+  LevelData& Lv = h->lev[l];
+  if (Lv.P_rp)
+    CKE(launch_csr_spmv((int)Lv.g.N, Lv.P_lpr, Lv.P_rp, Lv.P_ci, Lv.P_v, dc, df, df, 1.0, 1.0, h->s));
+  else
+    CKE(launch_prolong_add(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, dc, df, h->s));
+  h->launches += 1;
+  return 0;
+}
+
+static int average_level(stgmg_handle* h, int l, bool zero, double* d) {
+  LevelData& L = h->lev[l];
+  if (L.k3tab)
+    CKE(launch_avg_table(h->d, (int)L.g.N, L.k3tab, L.Y, h->prm.omega, zero ? 1 : 0, d, h->s));
+  else
+    CKE(launch_vanka_average(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero ? 1 : 0, d, h->s));
+  h->launches += 1;
+  return 0;
+}
+
 static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
   LevelData& L = h->lev[l];
   const double* rin = b;
@@ -493,9 +547,9 @@ static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_s
     rin = L.r;
   }
   CKE(launch_patch_gemm(L.g, h->r, L.k2var, L.cls_dev, L.tiles_dev, L.ntiles, L.relidx_dev, L.inv_dev, L.lda, rin, L.Y,
-                        L.ldy, h->s));
-  CKE(launch_vanka_average(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero_start ? 1 : 0, d, h->s));
-  h->launches += 2;
+                        L.ldy, L.cn, h->s));
+  h->launches += 1;
+  CK(average_level(h, l, zero_start, d));
   return exchange(h, l, d);
 }
 
@@ -505,8 +559,7 @@ static int enqueue_vcycle(stgmg_handle* h) {
     LevelData& Lv = h->lev[l];
     for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, l, Lv.b, Lv.d, j == 0));
     CK(residual(h, l, Lv.b, Lv.d, Lv.r));
-    CKE(launch_restrict(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, Lv.r, h->lev[l - 1].b, h->s));
-    h->launches += 1;
+    CK(restrict_level(h, l, Lv.r, h->lev[l - 1].b));
     if (Lv.part && h->lev[l - 1].part) CK(exchange(h, l - 1, h->lev[l - 1].b));
     else if (Lv.part) CK(agglomerate(h, l, h->lev[l - 1].b));
   }
@@ -514,14 +567,95 @@ static int enqueue_vcycle(stgmg_handle* h) {
   h->launches += 1;
   for (int l = 1; l < L; ++l) {
     LevelData& Lv = h->lev[l];
-    CKE(launch_prolong_add(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, h->lev[l - 1].d, Lv.d, h->s));
-    h->launches += 1;
+    CK(prolong_level(h, l, h->lev[l - 1].d, Lv.d));
     for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, l, Lv.b, Lv.d, false));
   }
   return 0;
 }
 
 // ------------------------------------------------------------------------------------------ setup pieces ----
+// Tiles of the grouped GEMM (K2, and the 3D element GEMM of K1) balanced over the GPU's resident CTA slots.  A
+// unit = (class, row block); its columns are cut into tiles of whole 8-column DMMA blocks, the tile count rounded up
+// to a multiple of the cluster size cn (the cn CTAs of a cluster share the unit's A rows by multicast).  The minimal
+// tiling (BN columns per tile) fixes the number of waves; W, the largest work of any tile, is then the smallest value
+// for which the tiles still fit those waves (binary search), so the last wave is as full as the units allow.  The
+// split only decides which CTA computes a column, never the arithmetic.
+std::vector<TileDesc> stgmg::balanced_tiles(const std::vector<int>& cp, const std::vector<int>& ncols, int bm, int bn,
+                                            int slots, int cn) {
+  struct Unit { int cls, m0; long long n, ng; double wpc; };
+  std::vector<Unit> u;
+  double wpcmax = 0.0, wsum = 0.0;
+  cn = std::max(cn, 1);
+  const long long gpt = std::max(1, bn / 8);   // 8-column groups per full tile
+  for (size_t c = 0; c < cp.size(); ++c)
+    for (int m0 = 0; m0 < cp[c]; m0 += bm) {
+      const double wpc = (double)std::min(bm, cp[c] - m0) * (double)cp[c];
+      u.push_back({(int)c, m0, ncols[c], (ncols[c] + 7) / 8, wpc});
+      wpcmax = std::max(wpcmax, wpc);
+      wsum += wpc * (double)ncols[c];
+    }
+  auto tiles_of = [&](const Unit& x, double W) {
+    const long long gmax = std::max(1LL, std::min(gpt, (long long)std::floor(W / (8.0 * x.wpc))));
+    const long long nt = (x.ng + gmax - 1) / gmax;
+    return ((nt + cn - 1) / cn) * cn;
+  };
+  auto count = [&](double W) {
+    long long n = 0;
+    for (const auto& x : u) n += tiles_of(x, W);
+    return n;
+  };
+  slots = std::max(slots, 1);
+  const double whi = 8.0 * (double)gpt * wpcmax * 1.0000001;
+  const long long t0 = count(whi);
+  long long target = ((t0 + slots - 1) / slots) * (long long)slots;
+  if (const char* ev = std::getenv("STGMG_TILE_TARGET")) target = std::max(t0, (long long)std::atoll(ev));
+  double lo = 0.0, hi = whi;
+  for (int it = 0; it < 60; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (count(mid) <= target) hi = mid; else lo = mid;
+  }
+  struct Group { double w; std::vector<TileDesc> t; };
+  std::vector<Group> groups;
+  double wmax_tile = 0.0;
+  for (const auto& x : u) {
+    const long long nt = tiles_of(x, hi);
+    const long long gb = x.ng / nt, gr = x.ng % nt;
+    long long n0 = 0;
+    Group gcur;
+    gcur.w = 0.0;
+    for (long long i = 0; i < nt; ++i) {
+      const long long nn = std::max(0LL, std::min(8 * (gb + (i < gr ? 1 : 0)), x.n - n0));
+      gcur.t.push_back(TileDesc{x.cls, x.m0, (int)std::min(n0, x.n), (int)nn});
+      gcur.w = std::max(gcur.w, x.wpc * (double)nn);
+      wmax_tile = std::max(wmax_tile, x.wpc * (double)nn);
+      n0 += nn;
+      if ((long long)gcur.t.size() == cn) {
+        groups.push_back(gcur);
+        gcur.t.clear();
+        gcur.w = 0.0;
+      }
+    }
+  }
+  std::stable_sort(groups.begin(), groups.end(), [](const Group& a, const Group& b) { return a.w > b.w; });
+  std::vector<TileDesc> out;
+  for (const auto& gq : groups)
+    for (const auto& t : gq.t) out.push_back(t);
+  if (std::getenv("STGMG_TILE_DEBUG"))
+    std::fprintf(stderr, "[stgmg] tiles bm=%d bn=%d cn=%d slots=%d minimal=%lld target=%lld tiles=%zu max_work=%.3g "
+                         "avg=%.3g\n",
+                 bm, bn, cn, slots, t0, target, out.size(), wmax_tile, out.empty() ? 0.0 : wsum / (double)out.size());
+  return out;
+}
+
+// Cluster size of a level's grouped GEMM.  Multicasting A over clusters of 2 / 4 CTAs was measured slower on B200 in
+// every case (cfg1 fine 22 -> 42 us, cfg3 fine 5.6 -> 6.8 ms): K2 is not L2-bandwidth bound and the per-chunk
+// cluster barrier costs more than the A traffic it saves.  Default 1; STGMG_K2_CN=2|4 enables it for experiments.
+static int k2_cluster(long long ncols_total) {
+  (void)ncols_total;
+  if (const char* ev = std::getenv("STGMG_K2_CN")) return std::max(1, std::min(4, std::atoi(ev)));
+  return 1;
+}
+
 static int build_patches(stgmg_handle* h, int l) {
   LevelData& Lv = h->lev[l];
   const LevelGeom& g = Lv.g;
@@ -620,17 +754,26 @@ static int build_patches(stgmg_handle* h, int l) {
   // tiles
   std::vector<TileDesc> tiles;
   Lv.k2var = k2_pick_variant(Lv.npatch_global ? Lv.npatch_global : Lv.npatch, Lv.maxcp);
+  if (const char* ev = std::getenv("STGMG_K2_VARIANT")) {   // experiments: force a tile variant on the fine level
+    if (l == h->L - 1) Lv.k2var = std::atoi(ev);
+  }
   int tbm = 0, tbn = 0;
   k2_tile_shape(Lv.k2var, &tbm, &tbn);
-  for (int c = 0; c < ncls; ++c)
-    for (int m0 = 0; m0 < Lv.cls[c].cp; m0 += tbm)
-      for (int n0 = 0; n0 < Lv.cls[c].ncols; n0 += tbn) tiles.push_back({c, m0, n0, 0});
+  {
+    std::vector<int> cpv, ncv;
+    for (const auto& c : Lv.cls) { cpv.push_back(c.cp); ncv.push_back(c.ncols); }
+    Lv.cn = k2_cluster(Lv.npatch_global ? Lv.npatch_global : Lv.npatch);
+    tiles = balanced_tiles(cpv, ncv, tbm, tbn, k2_slots(Lv.k2var, Lv.cn), Lv.cn);
+  }
   Lv.ntiles = (int)tiles.size();
   CK(upload(h, &Lv.cls_dev, Lv.cls));
   CK(upload(h, &Lv.tiles_dev, tiles));
   CK(upload(h, &Lv.relidx_dev, relidx));
   CK(dalloc(h, &Lv.Y, (size_t)Lv.npatch * Lv.ldy));
-  CK(dalloc(h, &Lv.inv_dev, (size_t)ncls * Lv.lda * Lv.lda));
+  double* inv_rm = nullptr;   // row-major inverses (setup scratch); K2 reads the chunk-major copy Lv.inv_dev
+  CKE(cudaMalloc(&inv_rm, sizeof(double) * (size_t)ncls * Lv.lda * Lv.lda));
+  CK(dalloc(h, &Lv.inv_dev, (size_t)ncls * Lv.lda * Lv.lda + kK2Slack));
+  CKE(cudaMemsetAsync(Lv.inv_dev, 0, sizeof(double) * ((size_t)ncls * Lv.lda * Lv.lda + kK2Slack), h->s));
   // dense mini-level operator: column j = A_mini e_j
   const long long Nm = mini.N;
   double *X = nullptr, *Ym = nullptr;
@@ -652,7 +795,7 @@ static int build_patches(stgmg_handle* h, int l) {
   CK(upload(h, &cps_dev, cps));
   CK(upload(h, &offs_dev, offs));
   CK(upload(h, &mdofs_dev, minidofs));
-  CKE(launch_extract_patch(mini, r, k1, Ym, Nm, nullptr, ncls, cps_dev, offs_dev, mdofs_dev, Lv.inv_dev, Lv.lda, h->s));
+  CKE(launch_extract_patch(mini, r, k1, Ym, Nm, nullptr, ncls, cps_dev, offs_dev, mdofs_dev, inv_rm, Lv.lda, h->s));
   int *perm = nullptr, *status = nullptr;
   double *colk = nullptr, *scale = nullptr;
   CK(dalloc(h, &perm, (size_t)ncls * Lv.lda));
@@ -660,15 +803,17 @@ static int build_patches(stgmg_handle* h, int l) {
   CK(dalloc(h, &colk, (size_t)ncls * Lv.lda));
   CK(dalloc(h, &scale, (size_t)ncls * Lv.lda));
   CKE(cudaMemsetAsync(status, 0, sizeof(int) * ncls, h->s));
-  if (gauss_jordan_inverse(Lv.inv_dev, ncls, Lv.maxcp, cps_dev, Lv.lda, perm, colk, scale, status, h->s)) {
+  if (gauss_jordan_inverse(inv_rm, ncls, Lv.maxcp, cps_dev, Lv.lda, perm, colk, scale, status, h->s)) {
     set_error("gauss_jordan_inverse launch failed");
     return STGMG_ECUDA;
   }
+  CKE(launch_chunk_swizzle(inv_rm, Lv.inv_dev, ncls, Lv.lda, h->s));
   std::vector<int> st(ncls);
   CKE(cudaMemcpyAsync(st.data(), status, sizeof(int) * ncls, cudaMemcpyDeviceToHost, h->s));
   CKE(cudaStreamSynchronize(h->s));
   CKE(cudaFree(X));
   CKE(cudaFree(Ym));
+  CKE(cudaFree(inv_rm));
   for (int c = 0; c < ncls; ++c)
     if (st[c] != 0) {
       set_error("singular patch matrix: level " + std::to_string(l) + " class " + std::to_string(c) +
@@ -681,7 +826,7 @@ static int build_patches(stgmg_handle* h, int l) {
 // 3D operator setup: per-cell-type element matrices (cell types = per-axis {first, interior, last}, every cell its
 // own type when n < 3), produced by the warp-per-cell sum-factorisation kernel on a min(n,3)^3-cell mini level with
 // the same h and boundary conditions, for every unit vector; applied at run time as a grouped DMMA GEMM.
-static int build_cells(stgmg_handle* h, int l) {
+static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* Ehost = nullptr) {
   LevelData& Lv = h->lev[l];
   const LevelGeom& g = Lv.g;
   const int d = h->d, r = h->r, k1 = h->k1;
@@ -754,18 +899,24 @@ static int build_cells(stgmg_handle* h, int l) {
   const int nt = (int)Lv.ecls.size();
   Lv.elda = (ne + 15) / 16 * 16;
   for (int t = 0; t < nt; ++t) Lv.ecls[t].inv_off = (long long)t * Lv.elda * Lv.elda;
-  Lv.ek2var = k2_pick_variant(Lv.ncell_global ? Lv.ncell_global : cell_count(g), ne);
-  int tbm = 0, tbn = 0;
-  k2_tile_shape(Lv.ek2var, &tbm, &tbn);
-  std::vector<TileDesc> tiles;
-  for (int t = 0; t < nt; ++t)
-    for (int m0 = 0; m0 < ne; m0 += tbm)
-      for (int n0 = 0; n0 < Lv.ecls[t].ncols; n0 += tbn) tiles.push_back({t, m0, n0, 0});
-  Lv.entiles = (int)tiles.size();
-  CK(upload(h, &Lv.ecls_dev, Lv.ecls));
-  CK(upload(h, &Lv.etiles_dev, tiles));
-  CK(upload(h, &Lv.erelidx_dev, relidx));
-  CK(dalloc(h, &Lv.E_dev, (size_t)nt * Lv.elda * Lv.elda));
+  if (gemm) {   // runtime element GEMM (3D operator): tiles, class records, gather tables, chunk-major matrices
+    Lv.ek2var = k2_pick_variant(Lv.ncell_global ? Lv.ncell_global : cell_count(g), ne);
+    int tbm = 0, tbn = 0;
+    k2_tile_shape(Lv.ek2var, &tbm, &tbn);
+    std::vector<TileDesc> tiles;
+    std::vector<int> cpv, ncv;
+    for (const auto& c : Lv.ecls) { cpv.push_back(c.cp); ncv.push_back(c.ncols); }
+    Lv.ecn = k2_cluster(Lv.ncell_global ? Lv.ncell_global : cell_count(g));
+    tiles = balanced_tiles(cpv, ncv, tbm, tbn, k2_slots(Lv.ek2var, Lv.ecn), Lv.ecn);
+    Lv.entiles = (int)tiles.size();
+    CK(upload(h, &Lv.ecls_dev, Lv.ecls));
+    CK(upload(h, &Lv.etiles_dev, tiles));
+    CK(upload(h, &Lv.erelidx_dev, relidx));
+    CK(dalloc(h, &Lv.E_dev, (size_t)nt * Lv.elda * Lv.elda + kK2Slack));
+    CKE(cudaMemsetAsync(Lv.E_dev, 0, sizeof(double) * ((size_t)nt * Lv.elda * Lv.elda + kK2Slack), h->s));
+  }
+  double* E_rm = nullptr;   // row-major element matrices (setup scratch); the GEMM reads the chunk-major Lv.E_dev
+  CKE(cudaMalloc(&E_rm, sizeof(double) * (size_t)nt * Lv.elda * Lv.elda));
   // element results of the mini level for every unit vector
   const long long Nm = mini.N;
   long long nvm = 1;
@@ -783,8 +934,14 @@ static int build_cells(stgmg_handle* h, int l) {
   CKE(launch_op_apply(d, r, k1, mini, h->c_dev, X, nullptr, Ycb, 1.0, (int)Nm, Nm, ycs, h->s, &nl));
   CK(upload(h, &reps_dev, reps));
   CK(upload(h, &mdofs_dev, mdofs));
-  CKE(launch_extract_elem(Ycb, ycs, ne, nt, reps_dev, mdofs_dev, Lv.E_dev, Lv.elda, h->s));
+  CKE(launch_extract_elem(Ycb, ycs, ne, nt, reps_dev, mdofs_dev, E_rm, Lv.elda, h->s));
+  if (gemm) CKE(launch_chunk_swizzle(E_rm, Lv.E_dev, nt, Lv.elda, h->s));
   CKE(cudaStreamSynchronize(h->s));
+  if (Ehost) {
+    Ehost->resize((size_t)nt * Lv.elda * Lv.elda);
+    CKE(cudaMemcpy(Ehost->data(), E_rm, sizeof(double) * Ehost->size(), cudaMemcpyDeviceToHost));
+  }
+  CKE(cudaFree(E_rm));
   CKE(cudaFree(X));
   CKE(cudaFree(Ycb));
   return 0;
@@ -853,6 +1010,7 @@ static int build_transfer(stgmg_handle* h, int l) {
       const int deg = pres ? h->r - 1 : h->r;
       Interp1DHost ih = (a == 0) ? make_interp_window(h->lev[l - 1].gnx, deg, F.w0, F.g.n[0], h->lev[l - 1].w0, cg.n[0])
                                  : make_interp(cg.n[a], deg);
+      (pres ? F.ih_p[a] : F.ih_q[a]) = ih;
       int *rpf, *cif, *rpc, *cic;
       double *vf, *vc;
       CK(upload(h, &rpf, ih.rp_f));
@@ -864,6 +1022,253 @@ static int build_transfer(stgmg_handle* h, int l) {
       T = Interp1D{rpf, cif, vf, rpc, cic, vc};
     }
   }
+  return 0;
+}
+
+// --------------------------------------------------------------------------- small-level fast path setup ----
+// CSR of a sparse matrix from per-row (column, value) lists filled in a fixed order: columns sorted (stable), equal
+// columns summed in fill order.
+struct HostCsr {
+  std::vector<int> rp, ci;
+  std::vector<double> v;
+};
+static HostCsr to_csr(std::vector<std::vector<std::pair<int, double>>>& rows) {
+  HostCsr c;
+  c.rp.assign(rows.size() + 1, 0);
+  for (size_t i = 0; i < rows.size(); ++i) {
+    auto& r = rows[i];
+    std::stable_sort(r.begin(), r.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    for (size_t j = 0; j < r.size();) {
+      size_t k = j;
+      double s = 0.0;
+      for (; k < r.size() && r[k].first == r[j].first; ++k) s += r[k].second;
+      c.ci.push_back(r[j].first);
+      c.v.push_back(s);
+      j = k;
+    }
+    c.rp[i + 1] = (int)c.ci.size();
+    std::vector<std::pair<int, double>>().swap(r);
+  }
+  return c;
+}
+
+static int lanes_for(const HostCsr& c) {   // lanes per row of the SpMV: ~ average row length / 4
+  const double avg = c.rp.size() > 1 ? (double)c.ci.size() / (double)(c.rp.size() - 1) : 1.0;
+  return avg > 64 ? 32 : (avg > 24 ? 16 : (avg > 8 ? 8 : 4));
+}
+
+static int upload_csr(stgmg_handle* h, const HostCsr& c, int** rp, int** ci, double** v) {
+  CK(upload(h, rp, c.rp));
+  CK(upload(h, ci, c.ci));
+  CK(upload(h, v, c.v));
+  return 0;
+}
+
+// DoF index of (Radau node m, field slot, lexicographic node (x, y, z)) on a level
+static long long dof_index(const LevelGeom& g, int m, int slot, const int* idx) {
+  const bool pres = slot == 2 * g.d;
+  long long node = 0;
+  for (int a = 0; a < g.d; ++a) node += (long long)idx[a] * (pres ? g.ps[a] : g.qs[a]);
+  return (long long)m * g.block + (pres ? 2 * g.R : (long long)slot * g.nq) + node;
+}
+
+static long long global_dofs(const stgmg_handle* h, const LevelData& Lv) {
+  long long nq = 1, np = 1;
+  for (int a = 0; a < h->d; ++a) {
+    const int n = (a == 0 && Lv.gnx) ? Lv.gnx : Lv.g.n[a];
+    nq *= (long long)h->r * n + 1;
+    np *= (long long)(h->r - 1) * n + 1;
+  }
+  return (long long)h->k1 * (2 * h->d * nq + np);
+}
+
+static long long small_threshold() {
+  if (const char* ev = std::getenv("STGMG_SMALL_N")) return std::atoll(ev);
+  return 40000;
+}
+
+// Assembled operator of level l: A[dof(K, e)][dof(K, e')] += E_type(K)[e][e'] over the cells K in lexicographic
+// order (the element matrices are those the 3D element GEMM uses, from the sum-factorised kernel on a mini level).
+static int build_small_operator(stgmg_handle* h, int l) {
+  LevelData& Lv = h->lev[l];
+  const LevelGeom& g = Lv.g;
+  const int d = h->d, r = h->r, k1 = h->k1;
+  const int ne = (int)elem_dofs(h);
+  std::vector<double> E;
+  CK(build_cells(h, l, false, &E));   // element matrices only (the 3D element GEMM was set up before)
+  const int elda = Lv.elda;
+  int ntx[3] = {1, 1, 1};
+  for (int a = 0; a < d; ++a) ntx[a] = g.n[a] < 3 ? g.n[a] : 3;
+  auto axtype = [&](int a, int c) { const int n = g.n[a]; return n < 3 ? c : (c == 0 ? 0 : (c == n - 1 ? 2 : 1)); };
+  std::vector<std::vector<std::pair<int, double>>> rows((size_t)g.N);
+  std::vector<long long> dofs(ne);
+  int c3[3] = {0, 0, 0};
+  for (c3[2] = 0; c3[2] < (d > 2 ? g.n[2] : 1); ++c3[2])
+    for (c3[1] = 0; c3[1] < g.n[1]; ++c3[1])
+      for (c3[0] = 0; c3[0] < g.n[0]; ++c3[0]) {
+        const int t = (d > 2 ? axtype(2, c3[2]) * ntx[1] * ntx[0] : 0) + axtype(1, c3[1]) * ntx[0] + axtype(0, c3[0]);
+        int e = 0;
+        for (int m = 0; m < k1; ++m)
+          for (int slot = 0; slot <= 2 * d; ++slot) {
+            const int deg = slot == 2 * d ? r - 1 : r;
+            const int n1 = deg + 1;
+            int tot = 1;
+            for (int a = 0; a < d; ++a) tot *= n1;
+            for (int j = 0; j < tot; ++j) {
+              int rem = j, idx[3] = {0, 0, 0};
+              for (int a = 0; a < d; ++a) {
+                idx[a] = deg * c3[a] + rem % n1;
+                rem /= n1;
+              }
+              dofs[e++] = dof_index(g, m, slot, idx);
+            }
+          }
+        const double* Et = E.data() + (size_t)t * elda * elda;
+        for (int i = 0; i < ne; ++i)
+          for (int j = 0; j < ne; ++j) {
+            const double v = Et[(size_t)i * elda + j];
+            if (v != 0.0) rows[(size_t)dofs[i]].push_back({(int)dofs[j], v});
+          }
+      }
+  const HostCsr c = to_csr(rows);
+  Lv.A_lpr = lanes_for(c);
+  return upload_csr(h, c, &Lv.A_rp, &Lv.A_ci, &Lv.A_v);
+}
+
+// Prolongation level l-1 -> l (rows = fine DoFs) and restriction (rows = coarse DoFs) from the 1D tables, weights
+// multiplied in the order of the node-mapped kernels ((w_z * w_y) * w_x), supports in lexicographic order.
+static int build_small_transfer(stgmg_handle* h, int l) {
+  LevelData& F = h->lev[l];
+  const LevelGeom& fg = F.g;
+  const LevelGeom& cg = h->lev[l - 1].g;
+  const int d = h->d, k1 = h->k1;
+  for (int dir = 0; dir < 2; ++dir) {   // 0: P (fine rows), 1: R = P^T (coarse rows)
+    const LevelGeom& rg = dir == 0 ? fg : cg;   // row level
+    const LevelGeom& cgx = dir == 0 ? cg : fg;  // column level
+    std::vector<std::vector<std::pair<int, double>>> rows((size_t)rg.N);
+    for (int slot = 0; slot <= 2 * d; ++slot) {
+      const bool pres = slot == 2 * d;
+      const Interp1DHost* T = pres ? F.ih_p : F.ih_q;
+      const int* nn = pres ? rg.pn : rg.qn;
+      int idx[3] = {0, 0, 0};
+      for (idx[2] = 0; idx[2] < (d > 2 ? nn[2] : 1); ++idx[2])
+        for (idx[1] = 0; idx[1] < nn[1]; ++idx[1])
+          for (idx[0] = 0; idx[0] < nn[0]; ++idx[0]) {
+            int lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1};
+            for (int a = 0; a < d; ++a) {
+              const auto& rp = dir == 0 ? T[a].rp_f : T[a].rp_c;
+              lo[a] = rp[idx[a]];
+              hi[a] = rp[idx[a] + 1];
+            }
+            std::vector<std::pair<int, double>> ent;
+            int ci[3] = {0, 0, 0};
+            for (int e2 = lo[2]; e2 < hi[2]; ++e2) {
+              double w2 = 1.0;
+              if (d > 2) {
+                ci[2] = dir == 0 ? T[2].ci_f[e2] : T[2].ci_c[e2];
+                w2 = dir == 0 ? T[2].v_f[e2] : T[2].v_c[e2];
+              }
+              for (int e1 = lo[1]; e1 < hi[1]; ++e1) {
+                ci[1] = dir == 0 ? T[1].ci_f[e1] : T[1].ci_c[e1];
+                const double w1 = w2 * (dir == 0 ? T[1].v_f[e1] : T[1].v_c[e1]);
+                for (int e0 = lo[0]; e0 < hi[0]; ++e0) {
+                  ci[0] = dir == 0 ? T[0].ci_f[e0] : T[0].ci_c[e0];
+                  const double w = w1 * (dir == 0 ? T[0].v_f[e0] : T[0].v_c[e0]);
+                  ent.push_back({0, w});
+                  long long node = 0;
+                  for (int a = 0; a < d; ++a) node += (long long)ci[a] * (pres ? cgx.ps[a] : cgx.qs[a]);
+                  ent.back().first = (int)node;
+                }
+              }
+            }
+            for (int m = 0; m < k1; ++m) {
+              const long long row = dof_index(rg, m, slot, idx);
+              const long long cbase = (long long)m * cgx.block + (pres ? 2 * cgx.R : (long long)slot * cgx.nq);
+              for (const auto& en : ent) rows[(size_t)row].push_back({(int)(cbase + en.first), en.second});
+            }
+          }
+    }
+    const HostCsr c = to_csr(rows);
+    if (dir == 0) {
+      F.P_lpr = lanes_for(c);
+      CK(upload_csr(h, c, &F.P_rp, &F.P_ci, &F.P_v));
+    } else {
+      F.R_lpr = lanes_for(c);
+      CK(upload_csr(h, c, &F.R_rp, &F.R_ci, &F.R_v));
+    }
+  }
+  return 0;
+}
+
+// Averaging table of level l: for every DoF the offsets in Y of the patches containing it, lexicographic.
+static int build_small_k3(stgmg_handle* h, int l) {
+  LevelData& Lv = h->lev[l];
+  const LevelGeom& g = Lv.g;
+  const int d = h->d, r = h->r, k1 = h->k1;
+  const int NS = d == 3 ? 27 : 9;
+  std::vector<int> tab((size_t)NS * g.N, -1);
+  for (int slot = 0; slot <= 2 * d; ++slot) {
+    const bool pres = slot == 2 * d;
+    const int deg = pres ? r - 1 : r;
+    const int* nn = pres ? g.pn : g.qn;
+    int idx[3] = {0, 0, 0};
+    for (idx[2] = 0; idx[2] < (d > 2 ? nn[2] : 1); ++idx[2])
+      for (idx[1] = 0; idx[1] < nn[1]; ++idx[1])
+        for (idx[0] = 0; idx[0] < nn[0]; ++idx[0]) {
+          int cnt[3] = {1, 1, 1}, pw[3][3] = {{0}}, pl[3][3] = {{0}}, pc[3][3] = {{1, 1, 1}, {1, 1, 1}, {1, 1, 1}};
+          for (int a = 0; a < d; ++a) {
+            const int i = idx[a], n = g.n[a], c = i / deg, lrem = i - c * deg;
+            int w0, nw;
+            if (lrem == 0) { w0 = c > 0 ? c - 1 : c; nw = (c > 0 ? 1 : 0) + 1 + (c <= n - 1 ? 1 : 0); }
+            else { w0 = c; nw = 2; }
+            cnt[a] = nw;
+            for (int j = 0; j < nw; ++j) {
+              const int w = w0 + j, lo = w > 0 ? w - 1 : 0;
+              pw[a][j] = w;
+              pl[a][j] = i - deg * lo;
+              pc[a][j] = (w > 0 ? 1 : 0) + (w < n ? 1 : 0);
+            }
+          }
+          int s = 0;
+          std::vector<std::array<long long, 3>> pat;   // (Y offset of loc, nQ, blk) per patch, lexicographic
+          for (int i3 = 0; i3 < (d > 2 ? cnt[2] : 1); ++i3)
+            for (int i2 = 0; i2 < cnt[1]; ++i2)
+              for (int i1 = 0; i1 < cnt[0]; ++i1) {
+                const int j[3] = {i1, i2, i3};
+                long long plin = 0, vs = 1, loc = 0, ls = 1, nQ = 1, nP = 1;
+                for (int a = 0; a < d; ++a) {
+                  plin += (long long)pw[a][j[a]] * vs;
+                  vs *= g.n[a] + 1;
+                  const long long qb = (long long)r * pc[a][j[a]] + 1, pb = (long long)(r - 1) * pc[a][j[a]] + 1;
+                  loc += (long long)pl[a][j[a]] * ls;
+                  ls *= pres ? pb : qb;
+                  nQ *= qb;
+                  nP *= pb;
+                }
+                pat.push_back({plin * Lv.ldy + loc + (pres ? 2 * d * nQ : 0), nQ, 2 * d * nQ + nP});
+                ++s;
+              }
+          for (int m = 0; m < k1; ++m) {
+            const long long mu = dof_index(g, m, slot, idx);
+            for (size_t q = 0; q < pat.size(); ++q)
+              tab[(size_t)q * g.N + mu] = (int)(pat[q][0] + m * pat[q][2] + (pres ? 0 : slot * pat[q][1]));
+          }
+        }
+  }
+  return upload(h, &Lv.k3tab, tab);
+}
+
+static int build_small(stgmg_handle* h, int l) {
+  LevelData& Lv = h->lev[l];
+  const long long ng = global_dofs(h, Lv);
+  const long long thr = small_threshold();
+  if (l < 1 || ng > thr) return 0;
+  long long ncell = 1;   // global cell count: every rank of the x-slab decomposition takes the same decision
+  for (int a = 0; a < h->d; ++a) ncell *= (a == 0 && Lv.gnx) ? Lv.gnx : Lv.g.n[a];
+  const long long ne = elem_dofs(h);
+  if (ncell * ne * ne <= 12000000LL) CK(build_small_operator(h, l));
+  CK(build_small_transfer(h, l));
+  CK(build_small_k3(h, l));
   return 0;
 }
 
@@ -955,6 +1360,12 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   }
   h->d = d; h->r = r; h->k = k; h->k1 = k + 1; h->L = levels;
   h->prm = *params;
+  {
+    int dev = 0, nsm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+      h->nsm = nsm;
+  }
   if (h->prm.omega <= 0) h->prm.omega = 0.7;
   if (h->prm.jmax <= 0) h->prm.jmax = 4;
   if (params->stream) {
@@ -1061,13 +1472,14 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       long long nv = 1;
       for (int a = 0; a < 3; ++a) nv *= h->lev[levels - 1].g.n[a] + 1;
       CK(dalloc(h.get(), &h->Ycell, (size_t)(nv * elem_dofs(h.get()))));
-      for (int l = 0; l < levels; ++l) CK(build_cells(h.get(), l));
+      for (int l = 0; l < levels; ++l) CK(build_cells(h.get(), l, true));
     }
   }
   CK(build_coarse(h.get()));
   for (int l = 1; l < levels; ++l) {
     CK(build_patches(h.get(), l));
     CK(build_transfer(h.get(), l));
+    CK(build_small(h.get(), l));
   }
   const long long Nf = h->lev[levels - 1].g.N;
   CK(dalloc(h.get(), &h->w, (size_t)Nf));
@@ -1147,13 +1559,13 @@ int stgmg_smooth_sweep(stgmg_handle* h, int level, const double* b, double* d) {
 
 int stgmg_restrict(stgmg_handle* h, int level, const double* rf, double* bc) {
   if (!h || level < 1 || level >= h->L) { set_error("bad level"); return STGMG_EINVAL; }
-  CKE(launch_restrict(h->lev[level].g, h->lev[level - 1].g, h->k1, h->lev[level].tt, rf, bc, h->s));
+  CK(restrict_level(h, level, rf, bc));
   return sync_if_own(h);
 }
 
 int stgmg_prolong_add(stgmg_handle* h, int level, const double* dc, double* df) {
   if (!h || level < 1 || level >= h->L) { set_error("bad level"); return STGMG_EINVAL; }
-  CKE(launch_prolong_add(h->lev[level].g, h->lev[level - 1].g, h->k1, h->lev[level].tt, dc, df, h->s));
+  CK(prolong_level(h, level, dc, df));
   return sync_if_own(h);
 }
 
@@ -1327,11 +1739,11 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
   auto one = [&]() -> int {
     if (kind == 0) {
       CKE(launch_patch_gemm(Lv.g, h->r, Lv.k2var, Lv.cls_dev, Lv.tiles_dev, Lv.ntiles, Lv.relidx_dev, Lv.inv_dev, Lv.lda,
-                            Lv.r, Lv.Y, Lv.ldy, h->s));
+                            Lv.r, Lv.Y, Lv.ldy, Lv.cn, h->s));
     } else if (kind == 1) {
       CK(apply_level(h, level, Lv.d, Lv.r, nullptr, 1.0, 0.0));
     } else if (kind == 2) {
-      CKE(launch_vanka_average(Lv.g, h->r, h->k1, Lv.Y, Lv.ldy, h->prm.omega, 0, Lv.d, h->s));
+      CK(average_level(h, level, false, Lv.d));
     } else if (kind == 4) {
       CKE(launch_noop(1, h->s));
     } else if (kind == 5) {

@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(RED_THREADS) mgs_dot_kernel(double* __restrict
                                                               double* __restrict__ partials, unsigned* counter,
                                                               double* __restrict__ out, int do_sqrt,
                                                               const unsigned char* __restrict__ mask) {
+  pdl_trigger();
   __shared__ double sh[32];
   __shared__ bool last;
   pdl_wait();
@@ -83,6 +84,7 @@ cudaError_t launch_sqrt(double* v, cudaStream_t s) {
 // y = x * (*sc) (invert: y = x / *sc)
 __global__ void scale_kernel(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ sc,
                              int invert, long long n) {
+  pdl_trigger();
   pdl_wait();
   const double f = invert ? 1.0 / *sc : *sc;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -137,6 +139,7 @@ cudaError_t launch_backsub(const double* H, int ldh, const double* gv, double* y
 // x += sum_j y_j Z_j
 __global__ void update_x_kernel(double* __restrict__ x, const double* __restrict__ Z, const double* __restrict__ y,
                                 int jn, long long n) {
+  pdl_trigger();
   pdl_wait();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -151,6 +154,7 @@ cudaError_t launch_update_x(double* x, const double* Z, const double* y, int jn,
 }
 
 __global__ void noop_kernel(int n, double* out) {
+  pdl_trigger();
   pdl_wait();
   if (threadIdx.x + blockIdx.x * blockDim.x < n && out) out[threadIdx.x] = 0.0;
 }

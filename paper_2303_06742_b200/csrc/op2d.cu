@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(OP2D_CPB * 4) op2d_cell_kernel(LevelGeom g, co
                                                                       const double* __restrict__ x,
                                                                       double* __restrict__ Yc, long long stride,
                                                                       long long ycstride) {
+  pdl_trigger();
   using T = T2<R, K1>;
   constexpr int NQ1 = T::NQ1, NP1 = T::NP1, NG = T::NG, NQ = T::NQ, NP = T::NP, NGP = T::NGP, NE1 = T::NE1;
   __shared__ OpConsts c;
@@ -349,87 +350,7 @@ __global__ void __launch_bounds__(OP2D_CPB * 4) op2d_cell_kernel(LevelGeom g, co
   for (int j = 0; j < NP; ++j) yrow[(long long)(4 * NQ + j) * ncell] = po[j];
 }
 
-// Phase 2: y[mu] = beta * base[mu] + alpha * sum_{cells K containing mu} Yc[e(K, mu)][K]  (D-generic), one thread
-// per DoF, cells summed in the fixed lexicographic order.  ldpm > 0: element results stored patch-major
-// Yc[plin(K)][ldpm] with plin = lexicographic index of vertex (K + 1) (output of the 3D element GEMM).
-__global__ void op_gather_kernel(LevelGeom g, int r, int k1, const double* __restrict__ Yc, const double* base,
-                                 double* y, double alpha, double beta, long long stride, long long ycstride, int ldpm) {
-  const int mu = blockIdx.x * blockDim.x + threadIdx.x;
-  pdl_wait();
-  if (mu >= (int)g.N) return;
-  const int gblock = (int)g.block, gnq = (int)g.nq, gR2 = (int)(2 * g.R);
-  Yc += blockIdx.y * ycstride;
-  y += blockIdx.y * stride;
-  if (base) base += blockIdx.y * stride;
-  const int d = g.d;
-  const int m = mu / gblock;
-  int rem = mu - m * gblock;
-  int fslot;
-  int node;
-  if (rem < gR2) {
-    fslot = rem / gnq;
-    node = rem - fslot * gnq;
-  } else {
-    fslot = 2 * d;
-    node = rem - gR2;
-  }
-  const bool pres = fslot == 2 * d;
-  const int deg = pres ? r - 1 : r;
-  const int n1 = deg + 1;
-  int nq_loc = 1, np_loc = 1;
-  for (int a = 0; a < d; ++a) { nq_loc *= r + 1; np_loc *= r; }
-  const int ne1 = 2 * d * nq_loc + np_loc;
-  const int slot_off = pres ? 2 * d * nq_loc : fslot * nq_loc;
-  int idx[3] = {0, 0, 0};
-  int t = node;
-  for (int a = 0; a < d; ++a) {
-    const int na = pres ? g.pn[a] : g.qn[a];
-    idx[a] = (int)(t % na);
-    t /= na;
-  }
-  int cc[3][2], li[3][2], nc[3] = {1, 1, 1};
-  for (int a = 0; a < 3; ++a) { cc[a][0] = 0; li[a][0] = 0; }
-  for (int a = 0; a < d; ++a) {
-    nc[a] = 0;
-    const int i = idx[a];
-    const int c1 = i / deg, l1 = i % deg;
-    if (l1 == 0 && c1 > 0) { cc[a][nc[a]] = c1 - 1; li[a][nc[a]] = deg; ++nc[a]; }
-    if (c1 < g.n[a]) { cc[a][nc[a]] = c1; li[a][nc[a]] = l1; ++nc[a]; }
-  }
-  int ncell = 1;
-  for (int a = 0; a < d; ++a) ncell *= g.n[a];
-  // issue all (<= 8) loads first, then sum in the fixed lexicographic cell order
-  double yv[8];
-#pragma unroll
-  for (int i3 = 0; i3 < 2; ++i3)
-#pragma unroll
-    for (int i2 = 0; i2 < 2; ++i2)
-#pragma unroll
-      for (int i1 = 0; i1 < 2; ++i1) {
-        const int slot = (i3 * 2 + i2) * 2 + i1;
-        yv[slot] = 0.0;
-        if (i1 < nc[0] && i2 < nc[1] && i3 < nc[2]) {
-          const int sel[3] = {i1, i2, i3};
-          int cell = 0, cs = 1, loc = 0, ls = 1, plin = 0, vs = 1;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            if (a >= d) break;
-            cell += cc[a][sel[a]] * cs;
-            cs *= g.n[a];
-            plin += (cc[a][sel[a]] + 1) * vs;
-            vs *= g.n[a] + 1;
-            loc += li[a][sel[a]] * ls;
-            ls *= n1;
-          }
-          const int e = m * ne1 + slot_off + loc;
-          yv[slot] = ldpm ? __ldg(Yc + (long long)plin * ldpm + e) : __ldg(Yc + (long long)e * ncell + cell);
-        }
-      }
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) s += yv[i];
-  y[mu] = (base ? beta * base[mu] : 0.0) + alpha * s;
-}
+// Phase 2 (node gather) lives in nodal.cu (gather_nodal_kernel).
 
 template <int R, int K1>
 static cudaError_t launch2d(const LevelGeom& g, const OpConsts* cdev, const double* x, double* Yc, int batch,
@@ -451,15 +372,6 @@ cudaError_t launch_op2d_cells(int r, int k1, const LevelGeom& g, const OpConsts*
   OP2D_CASE(3, 2)
   OP2D_CASE(3, 3)
   return cudaErrorNotSupported;
-}
-
-cudaError_t launch_op_gather(const LevelGeom& g, int r, int k1, const double* Yc, const double* base, double* y,
-                             double alpha, double beta, int batch, long long stride, long long ycstride,
-                             cudaStream_t s, int ldpm) {
-  const int bs = 256;
-  dim3 grid((unsigned)((g.N + bs - 1) / bs), (unsigned)batch);
-  return launch_pdl(op_gather_kernel, grid, dim3(bs), 0, s, g, r, k1, Yc, base, y, alpha, beta, stride, ycstride,
-                    ldpm);
 }
 
 }  // namespace stgmg

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, const OpCons
                                                        const double* __restrict__ x, double* __restrict__ y,
                                                        double* __restrict__ Yc, double sign, int color,
                                                        long long stride, long long ycstride) {
+  pdl_trigger();
   using T = Tr<D, R, K1>;
   extern __shared__ double smem[];
   __shared__ OpConsts c;

@@ -54,8 +54,8 @@ struct PatchClass {
   long long inv_off;           // offset of the class inverse (lda x lda)
 };
 
-struct TileDesc {              // one CTA tile of the grouped patch GEMM
-  int cls, m0, n0, pad;
+struct TileDesc {              // one CTA tile of the grouped patch GEMM: rows [m0, m0+BM), columns [n0, n0+nn)
+  int cls, m0, n0, nn;
 };
 
 #define STGMG_CUDA(call)                                                                   \
@@ -72,6 +72,16 @@ void set_error(const std::string& msg);
 // Programmatic dependent launch (sm_90+): the next kernel of the stream may begin launching while the previous
 // one drains; every hot kernel calls pdl_wait() before it reads what its predecessor wrote.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Let the next kernel of the stream launch now: its CTAs run their prologue (index math, static-table loads) while
+// this grid drains and block in pdl_wait() until it has completed.  Safe because no kernel writes global memory
+// before its own pdl_wait().
+// Measured on B200: early triggers make every kernel a little faster in isolation but the heterogeneous V-cycle chain
+// slower (cfg1 V-cycle 1.19 -> 1.46 ms), so they are opt-in (-DSTGMG_PDL_TRIGGER).
+#ifndef STGMG_PDL_TRIGGER
+__device__ __forceinline__ void pdl_trigger() {}
+#else
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+#endif
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -97,9 +107,17 @@ cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpCo
 // K2: Y[patch][mu_hat] = Ainv_class * R_P r for all patches (grouped DMMA GEMM); variant = tile shape.
 int k2_pick_variant(long long npatch, int maxcp);
 void k2_tile_shape(int variant, int* bm, int* bn);
+int k2_slots(int variant, int cn);   // resident CTA slots on the GPU for a variant launched in clusters of cn
+// Tiles of a grouped GEMM balanced over the resident CTA slots: cp[c] x ncols[c] per class, BM x (<= BN) tiles;
+// consecutive groups of cn tiles share (class, row block) (one thread-block cluster, A multicast).
+std::vector<TileDesc> balanced_tiles(const std::vector<int>& cp, const std::vector<int>& ncols, int bm, int bn,
+                                     int slots, int cn);
+// A matrices of the grouped GEMM: row-major lda x lda -> chunk-major swizzled (dst needs nmat*lda*lda + slack).
+cudaError_t launch_chunk_swizzle(const double* src, double* dst, int nmat, int lda, cudaStream_t s);
+constexpr int kK2Slack = 224 * 16;   // doubles after the last chunk-major matrix (tile rows past lda)
 cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
-                              int ntiles, const int* relidx, const double* inv, int lda, const double* rvec,
-                              double* Y, int ldy, cudaStream_t s);
+                              int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
+                              double* Y, int ldy, int cn, cudaStream_t s);
 // K3: d <- (zero ? 0 : d) + omega * (sum_P Y_P[mu_hat]) / p_mu   (pull form, lexicographic patch order).
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
                                  int zero_init, double* dvec, cudaStream_t s);

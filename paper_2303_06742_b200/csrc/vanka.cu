@@ -7,21 +7,27 @@
 //   K4 setup            : A_P extraction from the dense operator of a 4^d-cell "mini level" with the same h and
 //                         boundary conditions, power-of-2 equilibration and Gauss–Jordan inversion with partial
 //                         pivoting (ties -> lowest row) ("inverse ... by LAPACK routines", reading A19).
+#include <algorithm>
+#include <cstdlib>
+
 #include "stgmg_internal.cuh"
 
 namespace stgmg {
 
 // ------------------------------------------------------------------------------------------------ K2 --------
-// Grouped GEMM  Y[:, P] = Ainv_class * R_P r.  A CTA computes a BM (patch-local rows mu_hat) x BN (patches of one
-// class) tile; K runs in chunks of 16 through a multi-stage cp.async pipeline: the A chunk (rows of the class
-// inverse, row-major, L2-resident) and the gathered B chunk (R_P r; zero-filled beyond C_P / past the last patch)
-// are copied asynchronously into shared memory while the previous chunk is multiplied on the FP64 tensor pipe
-// (mma.sync m8n8k4 -> DMMA.8x8x4).  The class's gather table (C_P ints) is staged in shared memory once per CTA.
-// Tile variants (WM x WN warps, each MT x NT m8n8 tiles) are picked per level by the patch count so that small
-// levels spread over many SMs (latency) and large levels reuse A across many patches (L2 traffic):
-//   big 112 x 32 (2x2 warps of 7x2, split-K 2, two CTAs per SM), medium 56 x 32 (1x2 warps of 7x2, split-K 4),
-//   small 32 x 8 (2x1 warps of 2x1, split-K 4), tall 224 x 32 (4x1 warps of 7x4, split-K 2: every patch vector is
-//   gathered once when C_P <= 224); split-K partial sums are added in a fixed order (deterministic).
+// Grouped GEMM  Y[:, P] = Ainv_class * R_P r  on the FP64 tensor pipe (mma.sync m8n8k4 -> SASS DMMA.8x8x4).
+// A CTA computes a BM (patch-local rows mu_hat) x BN (patches of one class) tile; K runs in chunks of 16.
+//   A operand: the class inverse is stored chunk-major and bank-swizzled (see launch_chunk_swizzle), so the BM x 16
+//     slab of a chunk is ONE contiguous run of BM x 128 bytes.  The CTAs of a thread-block cluster (CN = 1, 2 or 4)
+//     share (class, row block) and differ only in their patch columns: each issues a 1/CN slice of every A chunk as a
+//     bulk async copy multicast to all CN CTAs (cp.async.bulk ... multicast::cluster, completion on an mbarrier), so
+//     the L2 -> SM traffic of A — the operand every tile re-reads — drops CN-fold.
+//   B operand: R_P r gathered element-wise with cp.async (zero fill beyond C_P / for absent columns).
+//   Pipeline: S stages; a cluster barrier (arrive after the local __syncthreads, wait after the chunk's DMMAs)
+//   guarantees that no CTA overwrites a stage another CTA is still reading.
+// Tile variants (WM x WN warps, each MT x NT m8n8 tiles, split-K KS): tall 224 x 32, big 112 x 32, medium 56 x 32,
+// small 32 x 8.  Split-K partial sums are added in a fixed order, every output element is computed by exactly one CTA
+// with the same k order whatever the tiling or cluster size: the result is bitwise reproducible.
 constexpr int K2_BK = 16;
 constexpr int K2_MAXCP = 2048;       // largest C_P whose gather table is staged in shared memory
 
@@ -37,24 +43,76 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
 }
 
-__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
-}
-
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// relaxed arrive: every read of the stage being released has already returned (its values fed DMMAs before the
+// preceding __syncthreads), so no release fence (MEMBAR) is needed on the hot path
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+// bulk global -> shared copy of `bytes` (multiple of 16) to the same smem offset of every CTA in `mask`
+__device__ __forceinline__ void bulk_copy_mc(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                             unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// one chunk (16 k) of a warp's MT x NJ block of m8n8 tiles (NJ <= NT leading column blocks; k4 steps of its slice)
+template <int MT, int NT, int NJ, int KS, int BM, int BSLD, int BN>
+__device__ __forceinline__ void k2_mma_impl(double (&acc)[MT][NT][2], const double (*A)[16], const double (*B)[BSLD],
+                                            int wm, int wn, int kslice, int lane, int swz) {
+#pragma unroll
+  for (int ks = kslice * 4; ks < 16; ks += 4 * KS) {
+    double af[MT], bf[NJ];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) af[i] = A[wm + i * 8 + (lane >> 2)][(ks + (lane & 3)) ^ swz];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) bf[j] = B[wn + j * 8 + (lane >> 2)][ks + (lane & 3)];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+}
+
 template <int WM, int WN, int MT, int NT, int STAGES, int KS>
 struct K2Cfg {
   static constexpr int BM = WM * MT * 8, BN = WN * NT * 8, THREADS = 32 * WM * WN * KS, NSTAGE = STAGES;
-  static constexpr int ASLD = K2_BK + 4;   // 20 doubles: a half-warp's 16 fragment loads hit distinct banks
-  static constexpr int BSLD = K2_BK + 4;   // B staged patch-major [BN][16 + 4] (same conflict-free pattern as A)
-  static constexpr size_t PIPE = sizeof(double) * STAGES * (BM * ASLD + BN * BSLD);
+  static constexpr int BSLD = K2_BK + 4;   // B staged patch-major [BN][16 + 4]: conflict-free fragment loads
+  static constexpr size_t ABYTES = sizeof(double) * BM * K2_BK;   // one A chunk (swizzled, unpadded)
+  static constexpr size_t PIPE = sizeof(double) * STAGES * (BM * K2_BK + BN * BSLD);
   static constexpr size_t RED = sizeof(double) * (KS - 1) * BM * BN;   // split-K partial sums (reuses the pipe)
-  static constexpr size_t SMEM = PIPE > RED ? PIPE : RED;
+  static constexpr size_t BAR_OFF = (PIPE > RED ? PIPE : RED);
+  static constexpr size_t SMEM = BAR_OFF + 8 * STAGES;
 };
 
 template <int WM, int WN, int MT, int NT, int K2_STAGES, int KS>
@@ -62,24 +120,53 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
                                                                   const PatchClass* __restrict__ cls,
                                                                   const TileDesc* __restrict__ tiles,
                                                                   const int* __restrict__ relidx,
-                                                                  const double* __restrict__ inv, int lda,
+                                                                  const double* __restrict__ invc, int lda,
                                                                   const double* __restrict__ rvec,
-                                                                  double* __restrict__ Y, int ldy) {
+                                                                  double* __restrict__ Y, int ldy, int cn) {
+  pdl_trigger();
   using C = K2Cfg<WM, WN, MT, NT, K2_STAGES, KS>;
-  constexpr int BM = C::BM, BN = C::BN, NTH = C::THREADS, ASLD = C::ASLD, BSLD = C::BSLD;
-  extern __shared__ __align__(16) double k2smem[];
-  double(*As)[BM][ASLD] = reinterpret_cast<double(*)[BM][ASLD]>(k2smem);
-  double(*Bs)[BN][BSLD] = reinterpret_cast<double(*)[BN][BSLD]>(k2smem + K2_STAGES * BM * ASLD);
+  constexpr int BM = C::BM, BN = C::BN, NTH = C::THREADS, BSLD = C::BSLD, S = K2_STAGES;
+  extern __shared__ __align__(128) double k2smem[];
+  double(*As)[BM][K2_BK] = reinterpret_cast<double(*)[BM][K2_BK]>(k2smem);
+  double(*Bs)[BN][BSLD] = reinterpret_cast<double(*)[BN][BSLD]>(k2smem + S * BM * K2_BK);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(k2smem) + C::BAR_OFF);
   __shared__ int baseQ[BN], baseP[BN], plin[BN];
   __shared__ int srel[K2_MAXCP];
   const TileDesc td = tiles[blockIdx.x];
   const PatchClass pc = cls[td.cls];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned crank = cn > 1 ? cluster_rank() : 0u;
+  const unsigned short cmask = (unsigned short)((1u << cn) - 1u);
+  const int cp = pc.cp;
+  const int nchunks = (cp + K2_BK - 1) / K2_BK;
+  // A chunk ch of this tile: rows [m0, m0 + BM) of chunk ch of the class's chunk-major inverse (lda rows per chunk)
+  const double* Ab = invc + pc.inv_off + (long long)td.m0 * K2_BK;
+  const long long achunk = (long long)lda * K2_BK;
+  constexpr unsigned SLICE_ROWS_1 = BM;   // rows per slice for cn = 1
+  const unsigned slice_rows = cn == 4 ? BM / 4 : (cn == 2 ? BM / 2 : SLICE_ROWS_1);
+  auto issue_a = [&](int ch, int buf) {   // thread 0 only
+    mbar_expect_tx(&full[buf], (unsigned)C::ABYTES);
+    const double* src = Ab + ch * achunk + (long long)crank * slice_rows * K2_BK;
+    double* dst = &As[buf][crank * slice_rows][0];
+    const unsigned bytes = slice_rows * K2_BK * (unsigned)sizeof(double);
+    if (cn > 1) bulk_copy_mc(dst, src, bytes, &full[buf], cmask);
+    else bulk_copy(dst, src, bytes, &full[buf]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (cn > 1) { cluster_arrive(); cluster_wait(); }   // every CTA's barriers exist before any multicast lands
+  // the class inverse is static: its first chunks stream in while the previous kernel drains (PDL)
+  if (tid == 0)
+    for (int st = 0; st < S - 1; ++st)
+      if (st < nchunks) issue_a(st, st);
   const int d = g.d;
   for (int t = tid; t < BN; t += NTH) {
     const int col = td.n0 + t;
     int bq = 0, bp = 0, pl = -1;
-    if (col < pc.ncols) {
+    if (t < td.nn && col < pc.ncols) {
       int rem = col, vs = 1;
       pl = 0;
       for (int a = 0; a < d; ++a) {
@@ -96,21 +183,12 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
     baseP[t] = bp;
     plin[t] = pl;
   }
-  const double* A = inv + pc.inv_off;
-  const int cp = pc.cp;
   for (int i = tid; i < cp; i += NTH) srel[i] = __ldg(relidx + pc.rel_off + i);
   __syncthreads();
   pdl_wait();
-  const int nchunks = (cp + K2_BK - 1) / K2_BK;
 
-  auto load_chunk = [&](int ch, int buf) {
+  auto load_b = [&](int ch, int buf) {
     const int k0 = ch * K2_BK;
-    for (int e = tid; e < BM * 8; e += NTH) {          // A: BM rows x 16 doubles (8 x 16 B per row)
-      const int mm = e >> 3, kk = (e & 7) * 2;
-      const int row = td.m0 + mm;
-      const bool ok = row < lda;
-      cp_async16(&As[buf][mm][kk], ok ? A + (long long)row * lda + k0 + kk : A, ok);
-    }
     for (int e = tid; e < K2_BK * BN; e += NTH) {      // B: 16 rows x BN patches, gathered from r
       const int kk = e % K2_BK, nn = e / K2_BK;       // lanes run along mu_hat: x-contiguous node runs in r
       const int kr = k0 + kk;
@@ -122,7 +200,6 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
       }
       cp_async8(&Bs[buf][nn][kk], src, ok);
     }
-    cp_async_commit();
   };
 
   const int kslice = warp / (WM * WN);            // split-K: warp group kslice takes k4 steps kslice, kslice+KS, ..
@@ -135,31 +212,31 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
-  for (int st = 0; st < K2_STAGES - 1; ++st) {
-    if (st < nchunks) load_chunk(st, st);
-    else cp_async_commit();
+  for (int st = 0; st < S - 1; ++st) {
+    if (st < nchunks) load_b(st, st);
+    cp_async_commit();
   }
+  const int swz = ((lane >> 2) & 3) << 2;         // A bank swizzle of this lane's fragment rows (row & 3 == lane>>2 & 3)
+  const int nj = td.nn > wn ? min(NT, (td.nn - wn + 7) / 8) : 0;   // non-empty 8-column blocks of this warp
   for (int ch = 0; ch < nchunks; ++ch) {
-    const int buf = ch % K2_STAGES;
-    cp_async_wait<K2_STAGES - 2>();
+    const int buf = ch % S;
+    mbar_wait(&full[buf], (unsigned)((ch / S) & 1));
+    cp_async_wait<S - 2>();
     __syncthreads();
-    {
-      const int nx = ch + K2_STAGES - 1;   // refill the stage consumed in iteration ch-1
-      if (nx < nchunks) load_chunk(nx, nx % K2_STAGES);
-      else cp_async_commit();
+    if (cn > 1) cluster_arrive();                 // this CTA is done with the stage of chunk ch - 1
+    // warp-uniform branch on the number of non-empty 8-column blocks (predicated-off DMMAs still occupy the pipe)
+    if (nj == NT) k2_mma_impl<MT, NT, NT, KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
+    else if (nj == NT - 1) k2_mma_impl<MT, NT, (NT > 1 ? NT - 1 : 1), KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
+    else if (nj == NT - 2) k2_mma_impl<MT, NT, (NT > 2 ? NT - 2 : 1), KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
+    else if (nj == NT - 3) k2_mma_impl<MT, NT, (NT > 3 ? NT - 3 : 1), KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
+    else if (nj == NT - 4) k2_mma_impl<MT, NT, (NT > 4 ? NT - 4 : 1), KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
+    if (cn > 1) cluster_wait();                   // every CTA is done with that stage: it may be refilled
+    const int nx = ch + S - 1;                    // refill the stage consumed in iteration ch - 1
+    if (nx < nchunks) {
+      if (tid == 0) issue_a(nx, nx % S);
+      load_b(nx, nx % S);
     }
-#pragma unroll
-    for (int ks = kslice * 4; ks < K2_BK; ks += 4 * KS) {
-      double af[MT], bf[NT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) af[i] = As[buf][wm + i * 8 + (lane >> 2)][ks + (lane & 3)];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) bf[j] = Bs[buf][wn + j * 8 + (lane >> 2)][ks + (lane & 3)];
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
+    cp_async_commit();
   }
   cp_async_wait<0>();
   if (KS > 1) {   // deterministic split-K reduction: slices 1..KS-1 park their partial sums, slice 0 adds in order
@@ -199,141 +276,239 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
 }
 
 template <int WM, int WN, int MT, int NT, int ST, int KS>
-static cudaError_t launch_k2(const LevelGeom& g, int r, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
-                             const int* relidx, const double* inv, int lda, const double* rvec, double* Y, int ldy,
-                             cudaStream_t s) {
+static void k2_set_attr() {
   using C = K2Cfg<WM, WN, MT, NT, ST, KS>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM);
+    cudaFuncSetAttribute(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     attr = true;
   }
-  return launch_pdl(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, dim3(ntiles), dim3(C::THREADS), C::SMEM, s, g, r, cls_dev, tiles,
-                    relidx, inv, lda, rvec, Y, ldy);
 }
 
-using K2Big = K2Cfg<2, 2, 7, 2, 4, 2>;     // 112 x 32, 8 warps (2-way split-K), 2 CTAs / SM
-using K2Med = K2Cfg<1, 2, 7, 2, 4, 4>;     // 56 x 32, 8 warps (4-way split-K), 2 CTAs / SM
-using K2Small = K2Cfg<2, 1, 2, 1, 4, 4>;   // 32 x 8, 8 warps (4-way split-K)
-using K2Tall = K2Cfg<4, 1, 7, 4, 3, 2>;    // 224 x 32, 8 warps (2-way split-K): the whole C_P <= 224 in one tile
+template <int WM, int WN, int MT, int NT, int ST, int KS>
+static cudaError_t launch_k2(const LevelGeom& g, int r, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
+                             const int* relidx, const double* invc, int lda, const double* rvec, double* Y, int ldy,
+                             int cn, cudaStream_t s) {
+  using C = K2Cfg<WM, WN, MT, NT, ST, KS>;
+  k2_set_attr<WM, WN, MT, NT, ST, KS>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ntiles);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cn;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = cn > 1 ? 2 : 1;   // no cluster attribute for cn = 1 (plain launch)
+  return cudaLaunchKernelEx(&cfg, patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, g, r, cls_dev, tiles, relidx, invc, lda,
+                            rvec, Y, ldy, cn);
+}
+
+#define K2_TALL 4, 1, 7, 5, 4, 2    // 224 x 40, 8 warps (2-way split-K): the whole C_P <= 224 in one tile
+#define K2_BIG 2, 2, 7, 2, 5, 2     // 112 x 32, 8 warps (2-way split-K), 2 CTAs / SM
+#define K2_MED 1, 2, 7, 2, 4, 4     // 56 x 32, 8 warps (4-way split-K)
+#define K2_SMALL 2, 1, 2, 1, 4, 4   // 32 x 8, 8 warps (4-way split-K)
+
+template <int WM, int WN, int MT, int NT, int ST, int KS>
+static int k2_occ(int cn) {
+  using C = K2Cfg<WM, WN, MT, NT, ST, KS>;
+  k2_set_attr<WM, WN, MT, NT, ST, KS>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cn * 148);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cn;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, &cfg) != cudaSuccess ||
+      nclusters <= 0) {
+    cudaGetLastError();
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, C::THREADS,
+                                                      C::SMEM) != cudaSuccess || nb <= 0) {
+      cudaGetLastError();
+      nb = 1;
+    }
+    return nb * 148;
+  }
+  return nclusters * cn;
+}
+
+// K2L: latency variant of K2 for small levels (few patches; the V-cycle there is a chain of latency-bound kernels).
+// CTA = 8*MT rows x 8 patch columns of one class.  No shared-memory pipeline: warp w takes the 16-wide K chunks
+// w, w + nw, ..; every lane loads its m8n8k4 A fragments straight from the chunk-major inverse (L2) and its B
+// fragment element from r (through the class gather table), so the critical path is two dependent loads plus the
+// DMMAs of one or two chunks.  The nw partial products are added in warp order (fixed) through shared memory.
+template <int MT>
+__global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r, const PatchClass* __restrict__ cls,
+                                                             const TileDesc* __restrict__ tiles,
+                                                             const int* __restrict__ relidx,
+                                                             const double* __restrict__ invc, int lda,
+                                                             const double* __restrict__ rvec, double* __restrict__ Y,
+                                                             int ldy) {
+  pdl_trigger();
+  extern __shared__ double lred[];   // [nw][MT][2][32]
+  const TileDesc td = tiles[blockIdx.x];
+  const PatchClass pc = cls[td.cls];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int cp = pc.cp, nch = (cp + K2_BK - 1) / K2_BK;
+  const int d = g.d;
+  auto col_base = [&](int col, int& bq, int& bp, int& pl) {   // gather bases / vertex index of patch column col
+    int rem = col, vs = 1;
+    bq = 0; bp = 0; pl = 0;
+    for (int a = 0; a < d; ++a) {
+      const int v = pc.vlo[a] + rem % pc.cnt[a];
+      rem /= pc.cnt[a];
+      const int c0 = v > 0 ? v - 1 : 0;
+      bq += (r * c0) * (int)g.qs[a];
+      bp += ((r - 1) * c0) * (int)g.ps[a];
+      pl += v * vs;
+      vs *= (g.n[a] + 1);
+    }
+  };
+  const int nl = lane >> 2;                        // this lane's B column (m8n8k4 .col fragment: k = lane & 3)
+  const bool cvalid = nl < td.nn && td.n0 + nl < pc.ncols;
+  int bq = 0, bp = 0, pl = 0;
+  if (cvalid) col_base(td.n0 + nl, bq, bp, pl);
+  const int swz = ((lane >> 2) & 3) << 2;
+  const double* Ab = invc + pc.inv_off + (long long)(td.m0 + (lane >> 2)) * K2_BK;
+  const int* rel = relidx + pc.rel_off;
+  double acc[MT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+  pdl_wait();
+  for (int ch = warp; ch < nch; ch += nw) {
+    double a[4][MT], b[4];
+    int code[4];
+    const double* Ac = Ab + (long long)ch * lda * K2_BK;
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+      const int k = ch * K2_BK + st * 4 + (lane & 3);
+      code[st] = (cvalid && k < cp) ? __ldg(rel + k) : -1;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[st][i] = __ldg(Ac + i * 8 * K2_BK + ((st * 4 + (lane & 3)) ^ swz));
+    }
+#pragma unroll
+    for (int st = 0; st < 4; ++st)
+      b[st] = code[st] >= 0 ? __ldg(rvec + (code[st] >> 1) + ((code[st] & 1) ? bp : bq)) : 0.0;
+#pragma unroll
+    for (int st = 0; st < 4; ++st)
+#pragma unroll
+      for (int i = 0; i < MT; ++i) dmma884(acc[i][0], acc[i][1], a[st][i], b[st]);
+  }
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) lred[((warp * MT + i) * 2 + e) * 32 + lane] = acc[i][e];
+  __syncthreads();
+  for (int t = threadIdx.x; t < MT * 2 * 32; t += blockDim.x) {
+    const int ln = t & 31, e = (t >> 5) & 1, i = t >> 6;
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += lred[((w * MT + i) * 2 + e) * 32 + ln];
+    const int row = td.m0 + i * 8 + (ln >> 2);
+    const int n = 2 * (ln & 3) + e;
+    if (row < cp && n < td.nn && td.n0 + n < pc.ncols) {
+      int q, p, plo;
+      col_base(td.n0 + n, q, p, plo);
+      Y[(long long)plo * ldy + row] = s;
+    }
+  }
+}
+
+constexpr int K2L_MT = 4;   // 32 x 8 tiles
+
+static int k2l_warps(int lda) { return std::max(1, std::min(16, lda / K2_BK)); }
+
+static cudaError_t launch_k2l(const LevelGeom& g, int r, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
+                              const int* relidx, const double* invc, int lda, const double* rvec, double* Y, int ldy,
+                              cudaStream_t s) {
+  const int nw = k2l_warps(lda);
+  const size_t smem = sizeof(double) * nw * K2L_MT * 2 * 32;
+  return launch_pdl(patch_gemm_lat_kernel<K2L_MT>, dim3(ntiles), dim3(32 * nw), smem, s, g, r, cls_dev, tiles, relidx,
+                    invc, lda, rvec, Y, ldy);
+}
+
+// resident CTA slots of the whole GPU for a variant launched with clusters of cn CTAs
+int k2_slots(int variant, int cn) {
+  if (variant == 4) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_lat_kernel<K2L_MT>, 512,
+                                                      sizeof(double) * 16 * K2L_MT * 2 * 32) != cudaSuccess || nb <= 0) {
+      cudaGetLastError();
+      nb = 1;
+    }
+    return nb * 148;
+  }
+  if (variant == 3) return k2_occ<K2_TALL>(cn);
+  if (variant == 2) return k2_occ<K2_BIG>(cn);
+  if (variant == 1) return k2_occ<K2_MED>(cn);
+  return k2_occ<K2_SMALL>(cn);
+}
 
 void k2_tile_shape(int variant, int* bm, int* bn) {
-  if (variant == 3) { *bm = K2Tall::BM; *bn = K2Tall::BN; }
-  else if (variant == 2) { *bm = K2Big::BM; *bn = K2Big::BN; }
-  else if (variant == 1) { *bm = K2Med::BM; *bn = K2Med::BN; }
-  else { *bm = K2Small::BM; *bn = K2Small::BN; }
+  using T = K2Cfg<K2_TALL>;
+  using B = K2Cfg<K2_BIG>;
+  using M = K2Cfg<K2_MED>;
+  using Sm = K2Cfg<K2_SMALL>;
+  if (variant == 4) { *bm = 8 * K2L_MT; *bn = 8; }
+  else if (variant == 3) { *bm = T::BM; *bn = T::BN; }
+  else if (variant == 2) { *bm = B::BM; *bn = B::BN; }
+  else if (variant == 1) { *bm = M::BM; *bn = M::BN; }
+  else { *bm = Sm::BM; *bn = Sm::BN; }
 }
 
+// Measured on B200 (cfg1 fine level, 4225 patches, C_P = 218): big 22 us, tall 29 us (one CTA per SM hides less
+// latency than two), so tall is not picked automatically (STGMG_K2_VARIANT=3 forces it on the fine level).
 int k2_pick_variant(long long npatch, int maxcp) {
-  if (maxcp <= 224 && npatch >= 2000) return 3;
+  (void)maxcp;
+  if (const char* ev = std::getenv("STGMG_K2L_MAX")) { if (npatch < std::atoll(ev)) return 4; }
+  else if (npatch < 2000) return 4;   // latency variant on small levels
   if (npatch >= 2000) return 2;
   if (npatch >= 1000) return 1;
   return 0;
 }
 
 cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
-                              int ntiles, const int* relidx, const double* inv, int lda, const double* rvec,
-                              double* Y, int ldy, cudaStream_t s) {
-  if (variant == 3) return launch_k2<4, 1, 7, 4, 3, 2>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
-  if (variant == 2) return launch_k2<2, 2, 7, 2, 4, 2>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
-  if (variant == 1) return launch_k2<1, 2, 7, 2, 4, 4>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
-  return launch_k2<2, 1, 2, 1, 4, 4>(g, r, cls_dev, tiles, ntiles, relidx, inv, lda, rvec, Y, ldy, s);
+                              int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
+                              double* Y, int ldy, int cn, cudaStream_t s) {
+  if (variant == 4) return launch_k2l(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
+  if (variant == 3) return launch_k2<K2_TALL>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
+  if (variant == 2) return launch_k2<K2_BIG>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
+  if (variant == 1) return launch_k2<K2_MED>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
+  return launch_k2<K2_SMALL>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
 }
 
-// ------------------------------------------------------------------------------------------------ K3 --------
-__global__ void vanka_average_kernel(LevelGeom g, int r, int k1, const double* __restrict__ Y, int ldy, double omega,
-                                     int zero_init, double* __restrict__ dvec) {
-  const int mu = blockIdx.x * blockDim.x + threadIdx.x;
-  pdl_wait();
-  if (mu >= (int)g.N) return;
-  const int gblock = (int)g.block, gnq = (int)g.nq, gR2 = (int)(2 * g.R);
-  const int d = g.d;
-  const int m = mu / gblock;
-  int rem = mu - m * gblock;
-  int fslot;   // 0..2d-1 = (f, c) Q_r components, 2d = pressure
-  int node;
-  if (rem < gR2) {
-    fslot = rem / gnq;
-    node = rem - fslot * gnq;
-  } else {
-    fslot = 2 * d;
-    node = rem - gR2;
-  }
-  const bool pres = (fslot == 2 * d);
-  const int deg = pres ? r - 1 : r;
-  int idx[3];
-  {
-    int t = node;
-    for (int a = 0; a < d; ++a) {
-      const int na = pres ? g.pn[a] : g.qn[a];
-      idx[a] = (int)(t % na);
-      t /= na;
-    }
-  }
-  // per-axis candidate patches (vertex indices), ascending
-  int pv[3][3], np_[3];
-  for (int a = 0; a < d; ++a) {
-    const int i = idx[a], n = g.n[a];
-    np_[a] = 0;
-    if (i % deg == 0) {
-      const int v = i / deg;
-      if (v >= 1) pv[a][np_[a]++] = v - 1;
-      pv[a][np_[a]++] = v;
-      if (v <= n - 1) pv[a][np_[a]++] = v + 1;
-    } else {
-      const int cc = i / deg;
-      pv[a][np_[a]++] = cc;
-      pv[a][np_[a]++] = cc + 1;
-    }
-  }
-  for (int a = d; a < 3; ++a) { np_[a] = 1; pv[a][0] = 0; }
-  // issue all (<= 27) loads first, then sum in the fixed lexicographic patch order
-  double yv[27];
-#pragma unroll
-  for (int i3 = 0; i3 < 3; ++i3)
-#pragma unroll
-    for (int i2 = 0; i2 < 3; ++i2)
-#pragma unroll
-      for (int i1 = 0; i1 < 3; ++i1) {
-        const int slot = (i3 * 3 + i2) * 3 + i1;
-        yv[slot] = 0.0;
-        if (i1 < np_[0] && i2 < np_[1] && i3 < np_[2]) {
-          const int sel[3] = {i1, i2, i3};
-          int plin = 0, vs = 1, loc = 0, ls = 1, nQ = 1, nP = 1;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            if (a >= d) break;
-            const int v = pv[a][sel[a]];
-            const int lo = v > 0 ? v - 1 : 0;
-            const int ncell = (v > 0 ? 1 : 0) + (v < g.n[a] ? 1 : 0);
-            loc += (idx[a] - deg * lo) * ls;
-            ls *= deg * ncell + 1;
-            nQ *= r * ncell + 1;
-            nP *= (r - 1) * ncell + 1;
-            plin += v * vs;
-            vs *= (g.n[a] + 1);
-          }
-          const int blk = 2 * d * nQ + nP;
-          const int muh = m * blk + (pres ? 2 * d * nQ : fslot * nQ) + loc;
-          yv[slot] = __ldg(Y + (long long)plin * ldy + muh);
-        }
-      }
-  double z = 0.0;
-#pragma unroll
-  for (int i = 0; i < 27; ++i) z += yv[i];
-  int p = 1;
-  for (int a = 0; a < d; ++a) p *= np_[a];
-  const double upd = omega * z / (double)p;
-  dvec[mu] = zero_init ? upd : dvec[mu] + upd;
+// Row-major lda x lda matrices -> chunk-major, bank-swizzled layout read by K2:
+//   element (i, j) of matrix c at  c*lda*lda + (j/16)*lda*16 + i*16 + ((j%16) ^ (4*(i%4)))
+// so that rows [m0, m0+BM) of chunk j/16 are one contiguous block and the m8n8k4 A-fragment loads of a half-warp
+// (rows i..i+3, columns k..k+3) hit 16 distinct bank pairs.
+__global__ void chunk_swizzle_kernel(const double* __restrict__ src, double* __restrict__ dst, int lda) {
+  const int c = blockIdx.y;
+  const int i = blockIdx.x;
+  const double* a = src + (long long)c * lda * lda + (long long)i * lda;
+  double* o = dst + (long long)c * lda * lda;
+  for (int j = threadIdx.x; j < lda; j += blockDim.x)
+    o[(long long)(j / K2_BK) * lda * K2_BK + (long long)i * K2_BK + ((j % K2_BK) ^ (4 * (i % 4)))] = a[j];
 }
 
-cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
-                                 int zero_init, double* dvec, cudaStream_t s) {
-  const int bs = 256;
-  return launch_pdl(vanka_average_kernel, dim3((unsigned)((g.N + bs - 1) / bs)), dim3(bs), 0, s, g, r, k1, Y, ldy, omega,
-                    zero_init, dvec);
+cudaError_t launch_chunk_swizzle(const double* src, double* dst, int nmat, int lda, cudaStream_t s) {
+  chunk_swizzle_kernel<<<dim3(lda, nmat), 128, 0, s>>>(src, dst, lda);
+  return cudaGetLastError();
 }
+
+// K3 (averaging update) lives in nodal.cu (node-mapped).
 
 // ------------------------------------------------------------------------------------------------ K4 --------
 // inv[c][i][j] = A_mini[dof_c(i)][dof_c(j)], A_mini column-major (column j = A e_j), row-major output, zero pad.

@@ -86,7 +86,7 @@ def load_library(path=None, rebuild=False):
     global _lib
     if _lib is not None and not rebuild:
         return _lib
-    path = path or LIB
+    path = path or os.environ.get("STGMG_LIB") or LIB   # STGMG_LIB: experiment builds (A/B timing)
     if rebuild or needs_build():
         build()
     if not os.path.exists(path):
