@@ -757,6 +757,10 @@ static int build_patches(stgmg_handle* h, int l) {
   if (const char* ev = std::getenv("STGMG_K2_VARIANT")) {   // experiments: force a tile variant on the fine level
     if (l == h->L - 1) Lv.k2var = std::atoi(ev);
   }
+  {   // experiments: STGMG_K2_VARIANT_L<l>=v forces variant v on level l
+    const std::string key = "STGMG_K2_VARIANT_L" + std::to_string(l);
+    if (const char* ev = std::getenv(key.c_str())) Lv.k2var = std::atoi(ev);
+  }
   int tbm = 0, tbn = 0;
   k2_tile_shape(Lv.k2var, &tbm, &tbn);
   {

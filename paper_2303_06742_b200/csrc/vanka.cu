@@ -315,6 +315,8 @@ static cudaError_t launch_k2(const LevelGeom& g, int r, const PatchClass* cls_de
 #define K2_BIG 2, 2, 7, 2, 5, 2     // 112 x 32, 8 warps (2-way split-K), 2 CTAs / SM
 #define K2_MED 1, 2, 7, 2, 4, 4     // 56 x 32, 8 warps (4-way split-K)
 #define K2_SMALL 2, 1, 2, 1, 4, 4   // 32 x 8, 8 warps (4-way split-K)
+#define K2_BIGK1 2, 2, 7, 2, 4, 1   // 112 x 32, 4 warps (no split-K), 3 CTAs / SM
+#define K2_WIDE 2, 4, 7, 2, 3, 1    // 112 x 64, 8 warps (no split-K), 2 CTAs / SM
 
 template <int WM, int WN, int MT, int NT, int ST, int KS>
 static int k2_occ(int cn) {
@@ -451,6 +453,8 @@ int k2_slots(int variant, int cn) {
     }
     return nb * 148;
   }
+  if (variant == 5) return k2_occ<K2_BIGK1>(cn);
+  if (variant == 6) return k2_occ<K2_WIDE>(cn);
   if (variant == 3) return k2_occ<K2_TALL>(cn);
   if (variant == 2) return k2_occ<K2_BIG>(cn);
   if (variant == 1) return k2_occ<K2_MED>(cn);
@@ -463,6 +467,8 @@ void k2_tile_shape(int variant, int* bm, int* bn) {
   using M = K2Cfg<K2_MED>;
   using Sm = K2Cfg<K2_SMALL>;
   if (variant == 4) { *bm = 8 * K2L_MT; *bn = 8; }
+  else if (variant == 5) { *bm = K2Cfg<K2_BIGK1>::BM; *bn = K2Cfg<K2_BIGK1>::BN; }
+  else if (variant == 6) { *bm = K2Cfg<K2_WIDE>::BM; *bn = K2Cfg<K2_WIDE>::BN; }
   else if (variant == 3) { *bm = T::BM; *bn = T::BN; }
   else if (variant == 2) { *bm = B::BM; *bn = B::BN; }
   else if (variant == 1) { *bm = M::BM; *bn = M::BN; }
@@ -472,11 +478,11 @@ void k2_tile_shape(int variant, int* bm, int* bn) {
 // Measured on B200 (cfg1 fine level, 4225 patches, C_P = 218): big 22 us, tall 29 us (one CTA per SM hides less
 // latency than two), so tall is not picked automatically (STGMG_K2_VARIANT=3 forces it on the fine level).
 int k2_pick_variant(long long npatch, int maxcp) {
-  (void)maxcp;
   if (const char* ev = std::getenv("STGMG_K2L_MAX")) { if (npatch < std::atoll(ev)) return 4; }
-  else if (npatch < 2000) return 4;   // latency variant on small levels
+  else if (npatch < 200) return 4;   // latency variant on the smallest levels (measured: 25 / 81 patches)
+  if (npatch >= 20000) return 6;      // wide 112 x 64 (cfg2 fine 25.6 -> 27.6 TF/s, cfg3 fine 27.1 -> 27.3)
   if (npatch >= 2000) return 2;
-  if (npatch >= 1000) return 1;
+  if (npatch >= 1000) return maxcp > 256 ? 2 : 1;   // cfg2 level 4 (C_P 663): big 56 us vs medium 90 us
   return 0;
 }
 
@@ -484,6 +490,8 @@ cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const Patc
                               int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
                               double* Y, int ldy, int cn, cudaStream_t s) {
   if (variant == 4) return launch_k2l(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
+  if (variant == 5) return launch_k2<K2_BIGK1>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
+  if (variant == 6) return launch_k2<K2_WIDE>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
   if (variant == 3) return launch_k2<K2_TALL>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
   if (variant == 2) return launch_k2<K2_BIG>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
   if (variant == 1) return launch_k2<K2_MED>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
