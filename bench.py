@@ -9,8 +9,10 @@ Metric: MDoF*iter/s = N_slab * GMRES iterations / solve time / 1e6 (SURVEY §8(d
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl ours|reference]
 
 --impl reference runs the oracle (plain fp64 CPU implementation, oracle/) as it stands on the host cores.
-N > 1 (torchrun): every rank solves its own copy of the workload (replicas; the domain-decomposed multi-GPU
-path is not built yet), no data-path collective, scaling "weak".
+N > 1 (torchrun, one rank per GPU): the x-slab domain decomposition of SURVEY §8(e) — every rank owns a slab of
+cells of the SAME global slab problem (window vectors, halo exchange over NCCL after every smoothing sweep, GMRES
+inner products allreduced), so the scaling is "strong"; value = global DoFs x iterations / max-over-ranks time.
+--replicas instead runs N independent copies of the workload ("weak" scaling, no data-path collective).
 """
 import argparse
 import json
@@ -24,7 +26,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from stgmg_inputs import config, uniform_load  # noqa: E402
+from stgmg_inputs import config, uniform_load, dof_count  # noqa: E402
 
 FP64_PEAK_TFLOPS = 37.19   # measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peak_r01.json)
 
@@ -37,6 +39,7 @@ def parse():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of the decomposition")
     return ap.parse_args()
 
 
@@ -182,14 +185,30 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
     dev = torch.device("cuda", lrank if ws > 1 else 0)
     from paper_2303_06742_b200 import Solver
+    from paper_2303_06742_b200.stgmg import nccl_unique_id, nccl_comm_create, nccl_comm_destroy, partition_plan
+    from paper_2303_06742_b200.partition import window_index
     cfg = config(args.config)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
+    dd = ws > 1 and not args.replicas
+    comm = None
     t_setup = time.perf_counter()
-    s = Solver(cfg, stream=stream)
+    if dd:
+        # the library's own NCCL communicator: rank 0 draws the id, torch.distributed broadcasts it (stgmg.h)
+        uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
+        torch.distributed.broadcast(uid, 0)
+        comm = nccl_comm_create(bytes(uid.cpu().tolist()), ws, rank)
+        s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm)
+    else:
+        s = Solver(cfg, stream=stream)
     t_setup = time.perf_counter() - t_setup
-    N = s.size()
-    L = torch.as_tensor(uniform_load(N, cfg["seed"] or 1), device=dev)
+    N = s.size()                       # this rank's (window) vector length
+    Nglob = dof_count(cfg)             # DoFs of the global slab problem
+    Lg = uniform_load(Nglob, cfg["seed"] or 1)
+    if dd:
+        idx, _own = window_index(cfg, cfg["levels"] - 1, partition_plan(cfg, cfg["levels"] - 1, rank, ws))
+        Lg = Lg[idx]
+    L = torch.as_tensor(Lg, device=dev)
     Xp = torch.zeros(N, dtype=torch.float64, device=dev)
     rhs = torch.zeros_like(Xp)
     x = torch.zeros_like(Xp)
@@ -240,13 +259,18 @@ def run_ours(args):
     clk = clocks.stop()
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     its_t = torch.tensor([float(its)], dtype=torch.float64, device=dev)
+    energy_j = (e_end - e_start) * 1e-3 if (e_start is not None and e_end is not None) else None
     if ws > 1:
         import torch.distributed as dist
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-        dist.all_reduce(its_t, op=dist.ReduceOp.SUM)
+        if not dd:                     # replicas: every rank solved its own copy
+            dist.all_reduce(its_t, op=dist.ReduceOp.SUM)
+        if energy_j is not None:       # board energy of every participating GPU
+            et = torch.tensor([energy_j], dtype=torch.float64, device=dev)
+            dist.all_reduce(et, op=dist.ReduceOp.SUM)
+            energy_j = float(et.item())
     t_max_s = float(t_local.item()) * 1e-3
-    value = N * float(its_t.item()) / t_max_s / 1e6        # all ranks' DoF*iterations / max time
-    energy_j = (e_end - e_start) * 1e-3 if (e_start is not None and e_end is not None) else None
+    value = Nglob * float(its_t.item()) / t_max_s / 1e6    # DoF*iterations of the job / max-over-ranks time
     energy = {"joules_per_solve": energy_j / n_e if energy_j is not None else None,
               "avg_watts": energy_j / t_e if energy_j is not None else None, "solves": n_e, "window_s": t_e,
               "source": "NVML nvmlDeviceGetTotalEnergyConsumption (board), >= 1.5 s window of back-to-back solves"}
@@ -280,12 +304,12 @@ def run_ours(args):
         st = s.solve_host(rhs_h, x_h)
         e2e_its += st["iterations"]
     e2e_dt = time.perf_counter() - t0
-    e2e_val = N * e2e_its / e2e_dt / 1e6
+    e2e_val = Nglob * e2e_its / e2e_dt / 1e6
     if ws > 1:
         tt = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
         import torch.distributed as dist
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_val = N * e2e_its * ws / float(tt.item()) / 1e6
+        e2e_val = Nglob * e2e_its * (1 if dd else ws) / float(tt.item()) / 1e6
 
     out = None
     if rank == 0:
@@ -295,12 +319,14 @@ def run_ours(args):
         out = {
             "metric": "slab_solve_throughput", "value": value, "unit": "MDoF*iter/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max_s * 1e3 / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "dofs": N, "levels": cfg["levels"], "r": cfg["r"], "k": cfg["k"],
+            "higher_is_better": True, "scaling": "strong" if dd else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg["name"], "dofs": Nglob, "levels": cfg["levels"], "r": cfg["r"], "k": cfg["k"],
                        "restart": cfg["restart"], "rtol": cfg["rtol"], "load": "uniform[-1,1) seed %s" % cfg["seed"],
                        "gmres_iterations_total": its, "final_rel_residual_max": max(resid),
                        "l2": "flushed between timed steps (256 MB write, untimed)",
-                       "parallelism": "replicas" if ws > 1 else "single GPU", "setup_s": t_setup,
+                       "parallelism": ("x-slab decomposition over %d GPUs (NCCL halo exchange)" % ws) if dd else
+                                      ("%d replicas" % ws if ws > 1 else "single GPU"), "setup_s": t_setup,
                        "s_per_slab": t_max_s / args.steps,
                        "vcycle_ms": vc_ms, "k1_fine_apply_ms": k1_ms,
                        "k1_fine_hbm_gbs": work["k1_bytes"] / (k1_ms * 1e-3) / 1e9},
@@ -313,11 +339,14 @@ def run_ours(args):
                          "peak_source": "FP64 DMMA m8n8k4 microbenchmark on this pool (profiles/fp64_peak_r01.json); "
                                         "MEASURED_PEAKS.json has no fp64 entry"},
             "clocks": clk,
-            "e2e": {"value": e2e_val, "unit": "MDoF*iter/s", "h2d_bytes_per_step": 16 * N, "d2h_bytes_per_step": 8 * N},
+            "e2e": {"value": e2e_val, "unit": "MDoF*iter/s", "h2d_bytes_per_step": 16 * N * ws,
+                    "d2h_bytes_per_step": 8 * N * ws},
             "cpu_baseline": cpu,
         }
         print(json.dumps(out), flush=True)
     s.close()
+    if comm is not None:
+        nccl_comm_destroy(comm)
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()

@@ -1,5 +1,6 @@
-"""Host-side helpers for the x-slab domain decomposition tests: map a global level vector to a rank's window vector
-(owned cells + ghost cells, stgmg_partition_plan) and back.  Pure index bookkeeping, no arithmetic of the method."""
+"""Host-side index bookkeeping of the x-slab domain decomposition: map a global level vector to a
+rank's window vector (owned cells + ghost cells, stgmg_partition_plan) and back.  Used by bench.py (N > 1) to hand
+every rank its slice of the global load and by the multi-rank tests; no arithmetic of the method."""
 import numpy as np
 
 
@@ -51,3 +52,11 @@ def window_index(cfg, level, plan):
 
 def scatter_owned(global_vec, local_vec, idx, own):
     global_vec[idx[own]] = local_vec[own]
+
+
+def gather_owned(local_vecs, maps, n_global):
+    """Assemble a global vector from every rank's window vector (owned DoFs only)."""
+    out = np.zeros(n_global)
+    for v, (idx, own) in zip(local_vecs, maps):
+        scatter_owned(out, v, idx, own)
+    return out

@@ -14,7 +14,7 @@ import pytest
 
 from stgmg_inputs import uniform_load, random_vector
 from tests.gpu_common import small_config, to_gpu, to_np
-from tests.multirank import window_index, scatter_owned
+from paper_2303_06742_b200.partition import window_index, scatter_owned
 
 pytestmark = pytest.mark.gpu
 
