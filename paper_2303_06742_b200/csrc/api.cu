@@ -1262,17 +1262,22 @@ static int build_small_k3(stgmg_handle* h, int l) {
   return upload(h, &Lv.k3tab, tab);
 }
 
+// Decisions use global sizes so that every rank of the x-slab decomposition takes the same one (bitwise 1-vs-n).
 static int build_small(stgmg_handle* h, int l) {
   LevelData& Lv = h->lev[l];
+  if (l < 1) return 0;
   const long long ng = global_dofs(h, Lv);
   const long long thr = small_threshold();
-  if (l < 1 || ng > thr) return 0;
-  long long ncell = 1;   // global cell count: every rank of the x-slab decomposition takes the same decision
+  long long ncell = 1;
   for (int a = 0; a < h->d; ++a) ncell *= (a == 0 && Lv.gnx) ? Lv.gnx : Lv.g.n[a];
   const long long ne = elem_dofs(h);
-  if (ncell * ne * ne <= 12000000LL) CK(build_small_operator(h, l));
-  CK(build_small_transfer(h, l));
-  CK(build_small_k3(h, l));
+  // assembled operator: small levels only (its CSR re-reads ~100-600 values per row from L2)
+  if (ng <= thr && ncell * ne * ne <= 12000000LL) CK(build_small_operator(h, l));
+  // transfer CSR and averaging tables: a few int32 per DoF, cheaper than the node-mapped index math up to ~10 x thr
+  if (ng <= 10 * thr) {
+    CK(build_small_transfer(h, l));
+    CK(build_small_k3(h, l));
+  }
   return 0;
 }
 

@@ -479,7 +479,8 @@ void k2_tile_shape(int variant, int* bm, int* bn) {
 // latency than two), so tall is not picked automatically (STGMG_K2_VARIANT=3 forces it on the fine level).
 int k2_pick_variant(long long npatch, int maxcp) {
   if (const char* ev = std::getenv("STGMG_K2L_MAX")) { if (npatch < std::atoll(ev)) return 4; }
-  else if (npatch < 200) return 4;   // latency variant on the smallest levels (measured: 25 / 81 patches)
+  else if (npatch < 200 && maxcp <= 700) return 4;   // latency variant on the smallest 2D levels (25 / 81 patches);
+                                                     // 3D coarse levels stream ~1 GB of inverses: pipelined is faster
   if (npatch >= 20000) return 6;      // wide 112 x 64 (cfg2 fine 25.6 -> 27.6 TF/s, cfg3 fine 27.1 -> 27.3)
   if (npatch >= 2000) return 2;
   if (npatch >= 1000) return maxcp > 256 ? 2 : 1;   // cfg2 level 4 (C_P 663): big 56 us vs medium 90 us
