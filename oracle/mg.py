@@ -15,12 +15,13 @@ from .vanka import Patches, VankaSmoother, equilibrated_inverse
 
 class Hierarchy:
     def __init__(self, d, cells, lo, hi, r, k, nlevels, params, tau, bc_u=None, bc_p=None,
-                 omega=0.7, jmax=4, share_classes=True):
+                 omega=0.7, jmax=4, share_classes=True, colored=False):
         self.levels = hierarchy(d, cells, lo, hi, r, k, nlevels, bc_u, bc_p)
         self.ops = [SlabOperator(lv, params, tau) for lv in self.levels]
         self.A = [op.assemble() for op in self.ops]
         self.P = [None] + [prolongation(self.levels[l - 1], self.levels[l]) for l in range(1, nlevels)]
         self.jmax = jmax
+        self.colored = colored   # N2(i): multiplicative colour-ordered smoother instead of Alg. 1
         self.smoothers = [None] + [VankaSmoother(self.A[l], Patches(self.levels[l]), omega, share_classes)
                                    for l in range(1, nlevels)]
         self.coarse_inv = equilibrated_inverse(self.A[0].toarray())
@@ -36,8 +37,8 @@ class Hierarchy:
         if l == 0:
             return self.coarse_inv @ b
         sm = self.smoothers[l]
-        d = sm.smooth(b, None, self.jmax)
+        d = sm.smooth(b, None, self.jmax, self.colored)
         r = b - self.A[l] @ d
         dc = self.vcycle(self.P[l].T @ r, l - 1)
         d = d + self.P[l] @ dc
-        return sm.smooth(b, d, self.jmax)
+        return sm.smooth(b, d, self.jmax, self.colored)

@@ -12,6 +12,15 @@ Main form (reading A17): d <- d + omega * (sum_P E_P A_P^{-1} R_P r) / p, patche
 lexicographic vertex order; the literal form d <- (sum_P E_P S_P(d)) / p is ``sweep_literal``.
 Class sharing: A_P depends only on the per-axis class of the vertex index
 ({0}, {1}, {2..n-2}, {n-1}, {n} for n >= 4; every index its own class for n < 4).
+
+Smoother variant (the north star's "cell-coloured multiplicative patch sweeps"): the patch
+loop of Def:VankaOP with SUCCESSIVE OVERWRITING, which P:L527-529 (Remark after alg:smoother) names as the
+alternative to averaging: d[Z(P)] <- S_P(d) for one patch after the other, each with the current d.  Patches are
+ordered by vertex colour (v_a mod 4 per axis, colours lexicographic, x fastest; patches of one colour in
+lexicographic vertex order).  Two patches of one colour share no cell (their vertices differ by >= 4 along some
+axis), so A_l does not couple their DoFs and the colour's patches can be updated from ONE residual: that is
+``sweep_colored`` (what the GPU computes); ``sweep_sequential`` is the literal one-patch-at-a-time loop, used as
+its pin.
 """
 import itertools
 import numpy as np
@@ -139,9 +148,41 @@ class VankaSmoother:
         np.add.at(z, self.P.flat_idx, d[self.P.flat_idx] + self.omega * y)
         return z / self.P.p
 
-    def smooth(self, b, d=None, steps=4):
+    # ---------------------------------------------------------------- multiplicative variant (N2(i))
+    NCOL = 4   # colours per axis: same-colour patches share no cell
+
+    def colour_order(self):
+        """Patch indices grouped by vertex colour (v mod 4 per axis, lexicographic, x fastest)."""
+        d = self.P.lev.d
+        key = [sum((v[a] % self.NCOL) * self.NCOL ** a for a in range(d)) for v in self.P.verts]
+        groups = {}
+        for i, c in enumerate(key):            # self.P.verts is in lexicographic vertex order
+            groups.setdefault(c, []).append(i)
+        return [groups[c] for c in sorted(groups)]
+
+    def sweep_colored(self, b, d):
+        """One multiplicative sweep: for each colour, r = b - A d, then d[Z(P)] += omega A_P^{-1} R_P r for the
+        colour's patches (Eq:VankaOP0 with overwriting)."""
+        d = d.copy()
+        for group in self.colour_order():
+            r = b - self.A @ d
+            for i in group:
+                z = self.P.dofs[i]
+                d[z] = d[z] + self.omega * (self.inv[i] @ r[z])
+        return d
+
+    def sweep_sequential(self, b, d):
+        """Literal successive overwriting d[Z(P)] <- S_P(d), one patch at a time with its own residual."""
+        d = d.copy()
+        for group in self.colour_order():
+            for i in group:
+                z = self.P.dofs[i]
+                d[z] = d[z] + self.omega * (self.inv[i] @ (b - self.A @ d)[z])
+        return d
+
+    def smooth(self, b, d=None, steps=4, colored=False):
         """Alg. 1: d initialised with 0 (pre-smoothing) or continued (post-smoothing, reading A13)."""
         d = np.zeros_like(b) if d is None else d.copy()
         for _ in range(steps):
-            d = self.sweep(b, d)
+            d = self.sweep_colored(b, d) if colored else self.sweep(b, d)
         return d

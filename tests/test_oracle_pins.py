@@ -419,3 +419,65 @@ def test_sampled_helpers_match_global_definitions(dim, cells, r, k):
     sample = rng.choice(lev.N, 6, replace=False)
     got = lite.sampled_sweep(b, d, sample)
     assert np.abs(got - full[sample]).max() <= 1e-9 * np.abs(full).max()
+
+
+# ---------------------------------------------------------------- N2(i): multiplicative coloured Vanka -------
+@pytest.fixture(scope="module")
+def mesh8():
+    """8 x 6 cells, Q2/Q1, dG(1): large enough for several patches per colour (vertex colours v mod 4)."""
+    lev = Level(2, [8, 6], [0, 0], [1, 0.75], 2, 1)
+    A = SlabOperator(lev, P0, 0.01).assemble()
+    return lev, A, VankaSmoother(A, Patches(lev), omega=0.7)
+
+
+def test_N2_same_colour_patches_share_no_cell(mesh8):
+    """Colour batching is exact only if A_l couples no two patches of one colour: A[Z(P), Z(Q)] = 0."""
+    lev, A, sm = mesh8
+    Ad = A.tocsr()
+    for group in sm.colour_order():
+        assert len(group) >= 1
+        for a in range(len(group)):
+            for b in range(a + 1, len(group)):
+                zp, zq = sm.P.dofs[group[a]], sm.P.dofs[group[b]]
+                assert len(np.intersect1d(zp, zq)) == 0
+                assert abs(Ad[zp][:, zq]).sum() == 0.0
+
+
+def test_N2_colour_batched_equals_sequential_overwrite(mesh8):
+    """P:L527-529 ('overwriting successively ... within the patch loop'): the colour-batched sweep equals the
+    literal one-patch-at-a-time overwrite loop in the same order (a different computation: one residual per patch)."""
+    lev, A, sm = mesh8
+    rng = np.random.default_rng(11)
+    b, d = rng.standard_normal(lev.N), rng.standard_normal(lev.N)
+    s1, s2 = sm.sweep_colored(b, d), sm.sweep_sequential(b, d)
+    assert np.abs(s1 - s2).max() < 1e-12 * np.abs(s2).max()
+
+
+def test_N2_fixed_point_and_exact_local_solves(mesh8):
+    """Eq:VankaOP0: b = A d is a fixed point; with omega = 1 each patch update is an exact local solve, so right after
+    a colour is processed the residual vanishes on every DoF of that colour's patches."""
+    lev, A, sm = mesh8
+    rng = np.random.default_rng(12)
+    d = rng.standard_normal(lev.N)
+    assert np.abs(sm.sweep_colored(A @ d, d) - d).max() < 1e-12 * np.abs(d).max()
+    sm1 = VankaSmoother(A, sm.P, omega=1.0)
+    b, x = rng.standard_normal(lev.N), np.zeros(lev.N)
+    for group in sm1.colour_order():
+        r = b - A @ x
+        for i in group:
+            z = sm1.P.dofs[i]
+            x[z] = x[z] + sm1.inv[i] @ r[z]
+        res = b - A @ x
+        for i in group:
+            assert np.abs(res[sm1.P.dofs[i]]).max() < 1e-9 * np.abs(b).max()
+
+
+def test_N2_multiplicative_gmg_converges(cfg0):
+    """The colour-ordered multiplicative smoother inside the V-cycle preconditions FGMRES to the direct solution."""
+    c = config(0)
+    Hm = Hierarchy(2, c["cells"], c["lo"], c["hi"], c["r"], c["k"], c["levels"], P0, c["tau"], colored=True)
+    b = uniform_load(Hm.fine.N, 7)
+    x, info = fgmres(lambda v: Hm.A[-1] @ v, b, Hm.vcycle, tol=1e-10, restart=30)
+    xs = spla.spsolve(Hm.A[-1].tocsc(), b)
+    assert info["iterations"] <= 30
+    assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
