@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of the decomposition")
+    ap.add_argument("--smoother", default="additive", choices=["additive", "colored"],
+                    help="additive = Alg. 1 (paper, default); colored = multiplicative colour-ordered Vanka (N2(i))")
     return ap.parse_args()
 
 
@@ -191,6 +193,7 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     dd = ws > 1 and not args.replicas
+    smoother = 1 if args.smoother == "colored" else 0
     comm = None
     t_setup = time.perf_counter()
     if dd:
@@ -198,9 +201,9 @@ def run_ours(args):
         uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
         torch.distributed.broadcast(uid, 0)
         comm = nccl_comm_create(bytes(uid.cpu().tolist()), ws, rank)
-        s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm)
+        s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm, smoother=smoother)
     else:
-        s = Solver(cfg, stream=stream)
+        s = Solver(cfg, stream=stream, smoother=smoother)
     t_setup = time.perf_counter() - t_setup
     N = s.size()                       # this rank's (window) vector length
     Nglob = dof_count(cfg)             # DoFs of the global slab problem
@@ -323,6 +326,7 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": cfg["name"], "dofs": Nglob, "levels": cfg["levels"], "r": cfg["r"], "k": cfg["k"],
                        "restart": cfg["restart"], "rtol": cfg["rtol"], "load": "uniform[-1,1) seed %s" % cfg["seed"],
+                       "smoother": args.smoother,
                        "gmres_iterations_total": its, "final_rel_residual_max": max(resid),
                        "l2": "flushed between timed steps (256 MB write, untimed)",
                        "parallelism": ("x-slab decomposition over %d GPUs (NCCL halo exchange)" % ws) if dd else

@@ -49,7 +49,9 @@ enum {
 enum { STGMG_BC_DIRICHLET = 0, STGMG_BC_NEUMANN = 1 };
 enum { STGMG_HF_MEASURE = 0 /* h_F = |K|_d, P:L205 (default) */, STGMG_HF_EDGE = 1 /* h_F = h normal to F */ };
 enum { STGMG_TOL_REL = 0 /* ||r|| <= tol ||b|| (BASELINE) */, STGMG_TOL_ABS = 1 /* ||r|| <= tol */ };
-enum { STGMG_SMOOTH_ADDITIVE = 0 /* Alg. 1 (only variant implemented) */ };
+enum { STGMG_SMOOTH_ADDITIVE = 0 /* Alg. 1 with averaging, P:L488-524 (default) */,
+       STGMG_SMOOTH_COLORED_MULT = 1 /* Eq:VankaOP0 with successive overwriting, patches
+                                        ordered by vertex colour (v mod 4 per axis); single GPU only */ };
 enum { STGMG_COMM_NCCL = 0 /* nccl_comm is an ncclComm_t */,
        STGMG_COMM_LOOPBACK = 1 /* nccl_comm is an in-process hub (N emulated ranks on one GPU; tests) */ };
 
@@ -76,7 +78,7 @@ typedef struct {
   int hF_mode;                       /* STGMG_HF_MEASURE (default) | STGMG_HF_EDGE */
   double omega;                      /* Vanka under-relaxation, 0.7; <= 0 -> 0.7 */
   int jmax;                          /* smoothing steps per level, 4; <= 0 -> 4 */
-  int smoother;                      /* STGMG_SMOOTH_ADDITIVE */
+  int smoother;                      /* STGMG_SMOOTH_ADDITIVE (default) | STGMG_SMOOTH_COLORED_MULT */
   void* nccl_comm;                   /* multi-GPU: ncclComm_t (STGMG_COMM_NCCL) or loopback hub; NULL if nranks = 1 */
   int rank, nranks;                  /* x-slab domain decomposition over nranks GPUs */
   void* stream;                      /* cudaStream_t for all work; NULL = default stream */

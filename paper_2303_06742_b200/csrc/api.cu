@@ -331,6 +331,16 @@ struct LevelData {
   int *R_rp = nullptr, *R_ci = nullptr, R_lpr = 8;   // restriction: rows = DoFs of level l-1
   double* R_v = nullptr;
   int* k3tab = nullptr;
+  // multiplicative colour-ordered smoother: per vertex colour, the colour's sub-classes, K2 tiles and
+  // (sub-class, column) items of the update kernel
+  struct Colour {
+    PatchClass* cls_dev = nullptr;
+    TileDesc* tiles_dev = nullptr;
+    int ntiles = 0, k2var = 0;
+    int2* items_dev = nullptr;
+    int nitems = 0;
+  };
+  std::vector<Colour> colours;
 };
 
 struct stgmg_handle {
@@ -539,7 +549,31 @@ static int average_level(stgmg_handle* h, int l, bool zero, double* d) {
   return 0;
 }
 
+// Multiplicative colour-ordered sweep: per colour, r = b - A d (r = b for the first colour of a
+// sweep from d = 0), the colour's patch solves, d[Z(P)] += omega y_P.
+static int sweep_colored(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
+  LevelData& L = h->lev[l];
+  if (zero_start) CKE(cudaMemsetAsync(d, 0, sizeof(double) * L.g.N, h->s));
+  bool first = true;
+  for (const auto& C : L.colours) {
+    if (C.nitems == 0) continue;
+    const double* rin = b;
+    if (!(zero_start && first)) {
+      CK(residual(h, l, b, d, L.r));
+      rin = L.r;
+    }
+    first = false;
+    CKE(launch_patch_gemm(L.g, h->r, C.k2var, C.cls_dev, C.tiles_dev, C.ntiles, L.relidx_dev, L.inv_dev, L.lda, rin,
+                          L.Y, L.ldy, 1, h->s));
+    CKE(launch_colour_update(L.g, h->r, C.cls_dev, C.items_dev, C.nitems, L.relidx_dev, L.Y, L.ldy, h->prm.omega, d,
+                             h->s));
+    h->launches += 2;
+  }
+  return 0;
+}
+
 static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
+  if (h->prm.smoother == STGMG_SMOOTH_COLORED_MULT) return sweep_colored(h, l, b, d, zero_start);
   LevelData& L = h->lev[l];
   const double* rin = b;
   if (!zero_start) {
@@ -694,6 +728,7 @@ static int build_patches(stgmg_handle* h, int l) {
         PatchClass pc;
         std::memset(&pc, 0, sizeof(pc));
         pc.ncols = 1;
+        pc.vst = 1;
         long long nQ = 1, nP = 1;
         int qbox[3] = {1, 1, 1}, pbox[3] = {1, 1, 1};
         for (int a = 0; a < 3; ++a) {
@@ -773,6 +808,49 @@ static int build_patches(stgmg_handle* h, int l) {
   CK(upload(h, &Lv.cls_dev, Lv.cls));
   CK(upload(h, &Lv.tiles_dev, tiles));
   CK(upload(h, &Lv.relidx_dev, relidx));
+  if (h->prm.smoother == STGMG_SMOOTH_COLORED_MULT) {   // vertex colours v_a mod 4, lexicographic (x fastest)
+    constexpr int NCOL = 4;
+    int ncol = 1;
+    for (int a = 0; a < d; ++a) ncol *= NCOL;
+    Lv.colours.assign(ncol, LevelData::Colour());
+    for (int c = 0; c < ncol; ++c) {
+      int cc[3] = {0, 0, 0};
+      for (int a = 0, t = c; a < d; ++a, t /= NCOL) cc[a] = t % NCOL;
+      std::vector<PatchClass> sub;
+      std::vector<int2> items;
+      for (const auto& pc : Lv.cls) {
+        PatchClass q = pc;
+        q.vst = NCOL;
+        q.ncols = 1;
+        bool empty = false;
+        for (int a = 0; a < 3; ++a) {
+          if (a >= d) continue;
+          const int v0 = pc.vlo[a] + (((cc[a] - pc.vlo[a]) % NCOL) + NCOL) % NCOL;
+          const int last = pc.vlo[a] + pc.cnt[a] - 1;
+          q.vlo[a] = v0;
+          q.cnt[a] = v0 <= last ? (last - v0) / NCOL + 1 : 0;
+          if (q.cnt[a] == 0) empty = true;
+          q.ncols *= q.cnt[a];
+        }
+        if (empty) continue;
+        for (int col = 0; col < q.ncols; ++col) items.push_back(make_int2((int)sub.size(), col));
+        sub.push_back(q);
+      }
+      auto& C = Lv.colours[c];
+      C.nitems = (int)items.size();
+      if (sub.empty()) continue;
+      std::vector<int> cpv, ncv;
+      for (const auto& q : sub) { cpv.push_back(q.cp); ncv.push_back(q.ncols); }
+      C.k2var = k2_pick_variant((long long)items.size(), Lv.maxcp);
+      int cbm = 0, cbn = 0;
+      k2_tile_shape(C.k2var, &cbm, &cbn);
+      std::vector<TileDesc> ct = balanced_tiles(cpv, ncv, cbm, cbn, k2_slots(C.k2var, 1), 1);
+      C.ntiles = (int)ct.size();
+      CK(upload(h, &C.cls_dev, sub));
+      CK(upload(h, &C.tiles_dev, ct));
+      CK(upload(h, &C.items_dev, items));
+    }
+  }
   CK(dalloc(h, &Lv.Y, (size_t)Lv.npatch * Lv.ldy));
   double* inv_rm = nullptr;   // row-major inverses (setup scratch); K2 reads the chunk-major copy Lv.inv_dev
   CKE(cudaMalloc(&inv_rm, sizeof(double) * (size_t)ncls * Lv.lda * Lv.lda));
@@ -862,6 +940,7 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
         std::memset(&pc, 0, sizeof(pc));
         pc.cp = ne;
         pc.ncols = 1;
+        pc.vst = 1;
         pc.rel_off = (long long)relidx.size();
         long long mbq = 0, mbp = 0, rp = 0, vs = 1;
         for (int a = 0; a < 3; ++a) {
@@ -1354,6 +1433,14 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       return STGMG_EINVAL;
     }
   const int nranks = params->nranks > 1 ? params->nranks : 1;
+  if (params->smoother != STGMG_SMOOTH_ADDITIVE && params->smoother != STGMG_SMOOTH_COLORED_MULT) {
+    set_error("unknown smoother");
+    return STGMG_EINVAL;
+  }
+  if (params->smoother == STGMG_SMOOTH_COLORED_MULT && nranks > 1) {
+    set_error("the multiplicative colour-ordered smoother is single-GPU only");
+    return STGMG_ENOTSUP;
+  }
   if (nranks > 1 && (params->rank < 0 || params->rank >= nranks || params->nccl_comm == nullptr)) {
     set_error("multi-GPU: need 0 <= rank < nranks and a communicator (nccl_comm) / loopback hub");
     return STGMG_EINVAL;

@@ -48,7 +48,8 @@ struct LevelGeom {
 struct PatchClass {
   int cp;                      // C_P
   int ncols;                   // number of patches in the class
-  int vlo[3], cnt[3];
+  int vlo[3], cnt[3];          // vertices vlo[a] + i * vst, i < cnt[a], per axis
+  int vst;                     // vertex stride (1; 4 for the colour sub-classes of the multiplicative smoother)
   int cells[3];                // cells of the patch per axis (1 or 2)
   long long rel_off;           // offset of this class's relidx table (cp entries)
   long long inv_off;           // offset of the class inverse (lda x lda)
@@ -118,6 +119,11 @@ constexpr int kK2Slack = 224 * 16;   // doubles after the last chunk-major matri
 cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
                               int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
                               double* Y, int ldy, int cn, cudaStream_t s);
+// Multiplicative colour-ordered smoother: d[dof(P, mu_hat)] += omega * Y[P][mu_hat] for the patches
+// (sub-class, column) of one colour; same-colour patches are DoF-disjoint, so there are no conflicting writes.
+cudaError_t launch_colour_update(const LevelGeom& g, int r, const PatchClass* cls, const int2* items, int nitems,
+                                 const int* relidx, const double* Y, int ldy, double omega, double* dvec,
+                                 cudaStream_t s);
 // K3: d <- (zero ? 0 : d) + omega * (sum_P Y_P[mu_hat]) / p_mu   (pull form, lexicographic patch order).
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
                                  int zero_init, double* dvec, cudaStream_t s);

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
       int rem = col, vs = 1;
       pl = 0;
       for (int a = 0; a < d; ++a) {
-        const int v = pc.vlo[a] + rem % pc.cnt[a];
+        const int v = pc.vlo[a] + (rem % pc.cnt[a]) * pc.vst;
         rem /= pc.cnt[a];
         const int c0 = v > 0 ? v - 1 : 0;   // lowest patch cell along a
         bq += (r * c0) * (int)g.qs[a];
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r,
     int rem = col, vs = 1;
     bq = 0; bp = 0; pl = 0;
     for (int a = 0; a < d; ++a) {
-      const int v = pc.vlo[a] + rem % pc.cnt[a];
+      const int v = pc.vlo[a] + (rem % pc.cnt[a]) * pc.vst;
       rem /= pc.cnt[a];
       const int c0 = v > 0 ? v - 1 : 0;
       bq += (r * c0) * (int)g.qs[a];
@@ -518,6 +518,39 @@ cudaError_t launch_chunk_swizzle(const double* src, double* dst, int nmat, int l
 }
 
 // K3 (averaging update) lives in nodal.cu (node-mapped).
+
+// Multiplicative colour-ordered Vanka: the update d[Z(P)] += omega y_P of one colour's
+// patches; one block per patch, threads over the patch-local DoFs mu_hat.
+__global__ void colour_update_kernel(LevelGeom g, int r, const PatchClass* __restrict__ cls, const int2* __restrict__ items,
+                                     const int* __restrict__ relidx, const double* __restrict__ Y, int ldy,
+                                     double omega, double* __restrict__ dvec) {
+  const int2 it = items[blockIdx.x];
+  const PatchClass pc = cls[it.x];
+  int rem = it.y, vs = 1, bq = 0, bp = 0, pl = 0;
+  for (int a = 0; a < g.d; ++a) {
+    const int v = pc.vlo[a] + (rem % pc.cnt[a]) * pc.vst;
+    rem /= pc.cnt[a];
+    const int c0 = v > 0 ? v - 1 : 0;
+    bq += (r * c0) * (int)g.qs[a];
+    bp += ((r - 1) * c0) * (int)g.ps[a];
+    pl += v * vs;
+    vs *= (g.n[a] + 1);
+  }
+  pdl_wait();
+  const double* y = Y + (long long)pl * ldy;
+  for (int mh = threadIdx.x; mh < pc.cp; mh += blockDim.x) {
+    const int code = __ldg(relidx + pc.rel_off + mh);
+    const long long dof = (code >> 1) + ((code & 1) ? bp : bq);
+    dvec[dof] += omega * y[mh];
+  }
+}
+
+cudaError_t launch_colour_update(const LevelGeom& g, int r, const PatchClass* cls, const int2* items, int nitems,
+                                 const int* relidx, const double* Y, int ldy, double omega, double* dvec,
+                                 cudaStream_t s) {
+  if (nitems == 0) return cudaSuccess;
+  return launch_pdl(colour_update_kernel, dim3(nitems), dim3(128), 0, s, g, r, cls, items, relidx, Y, ldy, omega, dvec);
+}
 
 // ------------------------------------------------------------------------------------------------ K4 --------
 // inv[c][i][j] = A_mini[dof_c(i)][dof_c(j)], A_mini column-major (column j = A e_j), row-major output, zero pad.

@@ -13,6 +13,7 @@ STGMG_OK, STGMG_NOT_CONVERGED = 0, 1
 TOL_REL, TOL_ABS = 0, 1
 BC_DIRICHLET, BC_NEUMANN = 0, 1
 HF_MEASURE, HF_EDGE = 0, 1
+SMOOTH_ADDITIVE, SMOOTH_COLORED_MULT = 0, 1
 
 
 class Mesh(ctypes.Structure):
@@ -180,7 +181,7 @@ class Solver:
     loopback hub with comm_kind=COMM_LOOPBACK); vectors are then the rank's window vectors (stgmg_local_size)."""
 
     def __init__(self, cfg, stream=None, tau=None, omega=0.7, jmax=4, hF_mode=HF_MEASURE, levels=None,
-                 rank=0, nranks=1, comm=None, comm_kind=COMM_NCCL):
+                 rank=0, nranks=1, comm=None, comm_kind=COMM_NCCL, smoother=0):
         import torch
         if not torch.cuda.is_available():
             raise StgmgError("no CUDA device: the stgmg product path has no CPU fallback")
@@ -202,7 +203,7 @@ class Solver:
         p.hF_mode = hF_mode
         p.omega = omega
         p.jmax = jmax
-        p.smoother = 0
+        p.smoother = int(smoother)   # SMOOTH_ADDITIVE (Alg. 1) | SMOOTH_COLORED_MULT
         p.nccl_comm = comm
         p.rank, p.nranks = int(rank), int(nranks)
         p.comm_kind = int(comm_kind)
