@@ -341,6 +341,10 @@ struct LevelData {
     int nitems = 0;
   };
   std::vector<Colour> colours;
+  // dense K2: the residual expanded per (patch, mu_hat), class chunk-major swizzled (csrc/nodal.cu gather_expand)
+  bool dense = false;
+  double* Rexp = nullptr;
+  long long nrexp = 0;
 };
 
 struct stgmg_handle {
@@ -572,9 +576,39 @@ static int sweep_colored(stgmg_handle* h, int l, const double* b, double* d, boo
   return 0;
 }
 
+// r = b - A_l d written straight into the patch-expanded B operand of the dense K2 (d == nullptr: r = b)
+static int residual_expand(stgmg_handle* h, int l, const double* b, const double* d) {
+  LevelData& L = h->lev[l];
+  if (!d) {
+    CKE(launch_gather_expand(L.g, h->r, h->k1, nullptr, b, 0.0, 1.0, 0, L.cls_dev, L.Rexp, h->s));
+    h->launches += 1;
+    return 0;
+  }
+  if (h->d == 2) {
+    const long long ycs = cell_count(L.g) * elem_dofs(h);
+    CKE(launch_op2d_cells(h->r, h->k1, L.g, h->c_dev, d, h->Yc, 1, 0, ycs, h->s));
+    CKE(launch_gather_expand(L.g, h->r, h->k1, h->Yc, b, -1.0, 1.0, 0, L.cls_dev, L.Rexp, h->s));
+  } else {
+    const int ne = (int)elem_dofs(h);
+    CKE(launch_patch_gemm(L.g, h->r, L.ek2var, L.ecls_dev, L.etiles_dev, L.entiles, L.erelidx_dev, L.E_dev, L.elda, d,
+                          h->Ycell, ne, L.ecn, h->s));
+    CKE(launch_gather_expand(L.g, h->r, h->k1, h->Ycell, b, -1.0, 1.0, ne, L.cls_dev, L.Rexp, h->s));
+  }
+  h->launches += 2;
+  return 0;
+}
+
 static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
   if (h->prm.smoother == STGMG_SMOOTH_COLORED_MULT) return sweep_colored(h, l, b, d, zero_start);
   LevelData& L = h->lev[l];
+  if (L.dense) {
+    CK(residual_expand(h, l, b, zero_start ? nullptr : d));
+    CKE(launch_patch_gemm_dense(L.g, L.k2var, L.cls_dev, L.tiles_dev, L.ntiles, L.inv_dev, L.lda, L.Rexp, L.Y, L.ldy,
+                                h->s));
+    h->launches += 1;
+    CK(average_level(h, l, zero_start, d));
+    return exchange(h, l, d);
+  }
   const double* rin = b;
   if (!zero_start) {
     CK(residual(h, l, b, d, L.r));
@@ -798,13 +832,33 @@ static int build_patches(stgmg_handle* h, int l) {
   }
   int tbm = 0, tbn = 0;
   k2_tile_shape(Lv.k2var, &tbm, &tbn);
+  // dense K2 (bulk-copied B from the patch-expanded residual) on the levels of the big / wide tile variants
+  // (measured: the expansion stores ~C_P values per patch, K2 does ~2 C_P^2 flops per patch; on cfg1's fine level,
+  // C_P = 218 and 4,225 patches, the expansion costs more than the dense K2 saves: 0.80 -> 0.84 ms per V-cycle; on
+  // cfg2 (C_P = 663) / cfg3 (C_P = 1,554) K2 reaches 32 / 33.5 TF/s, V-cycles 29.4 -> 26.8 / 63 -> 56 ms)
+  Lv.dense = (Lv.k2var == 2 || Lv.k2var == 6) && h->prm.smoother == STGMG_SMOOTH_ADDITIVE &&
+             (Lv.maxcp > 256 || (Lv.npatch_global ? Lv.npatch_global : Lv.npatch) >= 20000);
+  if (const char* ev = std::getenv("STGMG_K2_DENSE"))   // experiments / tests: 0 = never, 1 = on big / wide levels
+    Lv.dense = std::atoi(ev) != 0 && (Lv.k2var == 2 || Lv.k2var == 6) && h->prm.smoother == STGMG_SMOOTH_ADDITIVE;
+  {
+    long long off = 0;
+    for (auto& c : Lv.cls) {
+      c.rexp_off = off;
+      off += (long long)((c.cp + 15) / 16) * c.ncols * 16;
+    }
+    Lv.nrexp = off;
+  }
   {
     std::vector<int> cpv, ncv;
     for (const auto& c : Lv.cls) { cpv.push_back(c.cp); ncv.push_back(c.ncols); }
     Lv.cn = k2_cluster(Lv.npatch_global ? Lv.npatch_global : Lv.npatch);
-    tiles = balanced_tiles(cpv, ncv, tbm, tbn, k2_slots(Lv.k2var, Lv.cn), Lv.cn);
+    tiles = balanced_tiles(cpv, ncv, tbm, tbn, Lv.dense ? k2d_slots(Lv.k2var) : k2_slots(Lv.k2var, Lv.cn), Lv.cn);
   }
   Lv.ntiles = (int)tiles.size();
+  if (Lv.dense) {
+    CK(dalloc(h, &Lv.Rexp, (size_t)Lv.nrexp));
+    CKE(cudaMemsetAsync(Lv.Rexp, 0, sizeof(double) * (size_t)Lv.nrexp, h->s));   // slots past C_P stay zero
+  }
   CK(upload(h, &Lv.cls_dev, Lv.cls));
   CK(upload(h, &Lv.tiles_dev, tiles));
   CK(upload(h, &Lv.relidx_dev, relidx));
@@ -1834,8 +1888,12 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
   LevelData& Lv = h->lev[level];
   auto one = [&]() -> int {
     if (kind == 0) {
-      CKE(launch_patch_gemm(Lv.g, h->r, Lv.k2var, Lv.cls_dev, Lv.tiles_dev, Lv.ntiles, Lv.relidx_dev, Lv.inv_dev, Lv.lda,
-                            Lv.r, Lv.Y, Lv.ldy, Lv.cn, h->s));
+      if (Lv.dense)
+        CKE(launch_patch_gemm_dense(Lv.g, Lv.k2var, Lv.cls_dev, Lv.tiles_dev, Lv.ntiles, Lv.inv_dev, Lv.lda, Lv.Rexp,
+                                    Lv.Y, Lv.ldy, h->s));
+      else
+        CKE(launch_patch_gemm(Lv.g, h->r, Lv.k2var, Lv.cls_dev, Lv.tiles_dev, Lv.ntiles, Lv.relidx_dev, Lv.inv_dev,
+                              Lv.lda, Lv.r, Lv.Y, Lv.ldy, Lv.cn, h->s));
     } else if (kind == 1) {
       CK(apply_level(h, level, Lv.d, Lv.r, nullptr, 1.0, 0.0));
     } else if (kind == 2) {

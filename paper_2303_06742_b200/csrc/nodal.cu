@@ -220,6 +220,165 @@ __global__ void __launch_bounds__(128) gather_nodal_kernel(LevelGeom g, const do
   }
 }
 
+// ------------------------------------------------------------------------------------------------ K1e -------
+// Residual in "patch-expanded" form for the dense K2 (large levels): r[mu] = beta * base[mu] + alpha * (sum of the
+// element results of the cells containing mu, lexicographic) exactly as gather_nodal computes it, then stored at
+// every (patch P containing mu, mu_hat) slot of Rexp, the B operand of K2 laid out per class chunk-major and
+// bank-swizzled: class block at cls[c].rexp_off, element (column col, mu_hat) at
+//   (mu_hat / 16) * ncols * 16 + col * 16 + ((mu_hat % 16) XOR 4 * (col % 4)),
+// so every K2 tile reads its B chunk as one contiguous bulk copy (no gather in K2).  Yc == nullptr: r = beta * base.
+// Patch classes per axis (App. A.4, as build_patches): n < 4: vertex w is its own class; else {0},{1},{2..n-2},{n-1},{n}.
+template <int D, int R, int K1>
+__global__ void __launch_bounds__(128) gather_expand_kernel(LevelGeom g, const double* __restrict__ Yc,
+                                                            const double* __restrict__ base, double alpha, double beta,
+                                                            int ldpm, const PatchClass* __restrict__ cls,
+                                                            double* __restrict__ rexp) {
+  pdl_trigger();
+  constexpr int NQE = D == 3 ? (R + 1) * (R + 1) * (R + 1) : (R + 1) * (R + 1);
+  constexpr int NPE = D == 3 ? R * R * R : R * R;
+  constexpr int NE1 = 2 * D * NQE + NPE;
+  constexpr int NC = 1 << D;
+  constexpr int NPMAX = D == 3 ? 27 : 9;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nq = (int)g.nq, np = (int)g.np;
+  if (t >= nq + np) return;
+  const bool pres = t >= nq;
+  const int node = pres ? t - nq : t;
+  const int deg = pres ? R - 1 : R;
+  int idx[3];
+  node_coords<D>(node, pres ? g.pn : g.qn, idx);
+  // ---- cells containing the node (as gather_nodal)
+  int nc[3] = {1, 1, 1}, cc[3][2], li[3][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) { cc[a][0] = cc[a][1] = 0; li[a][0] = li[a][1] = 0; }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int i = idx[a];
+    int c1, l1;
+    if (pres) { c1 = i / (R - 1); l1 = i - c1 * (R - 1); } else { c1 = i / R; l1 = i - c1 * R; }
+    int k = 0;
+    if (l1 == 0 && c1 > 0) { cc[a][k] = c1 - 1; li[a][k] = deg; ++k; }
+    if (c1 < g.n[a]) { cc[a][k] = c1; li[a][k] = l1; ++k; }
+    nc[a] = k;
+  }
+  int ncell = 1;
+#pragma unroll
+  for (int a = 0; a < D; ++a) ncell *= g.n[a];
+  const int n1 = pres ? R : R + 1;
+  const int estride = ldpm ? 1 : ncell;
+  int off[NC];
+#pragma unroll
+  for (int s = 0; s < NC; ++s) {
+    const int j[3] = {s & 1, (s >> 1) & 1, (s >> 2) & 1};
+    bool ok = Yc != nullptr;
+    int cell = 0, cs = 1, plin = 0, vs = 1, loc = 0, ls = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      ok = ok && j[a] < nc[a];
+      cell += cc[a][j[a]] * cs;
+      cs *= g.n[a];
+      plin += (cc[a][j[a]] + 1) * vs;
+      vs *= g.n[a] + 1;
+      loc += li[a][j[a]] * ls;
+      ls *= n1;
+    }
+    const int e0 = loc + (pres ? 2 * D * NQE : 0);
+    off[s] = ok ? (ldpm ? plin * ldpm + e0 : e0 * ncell + cell) : -1;
+  }
+  // ---- patches containing the node (as avg_nodal) and their class / column
+  int cnt[3] = {1, 1, 1}, pw[3][3], pl[3][3], pc[3][3], pac[3][3], ppos[3][3], pcn[3][3], ncls[3] = {1, 1, 1};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) { pw[a][j] = 0; pl[a][j] = 0; pc[a][j] = 1; pac[a][j] = 0; ppos[a][j] = 0; pcn[a][j] = 1; }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int i = idx[a], n = g.n[a];
+    ncls[a] = n < 4 ? n + 1 : 5;
+    int c, l;
+    if (pres) { c = i / (R - 1); l = i - c * (R - 1); } else { c = i / R; l = i - c * R; }
+    int w0, nw;
+    if (l == 0) { w0 = c > 0 ? c - 1 : c; nw = (c > 0 ? 1 : 0) + 1 + (c <= n - 1 ? 1 : 0); }
+    else { w0 = c; nw = 2; }
+    cnt[a] = nw;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int w = w0 + j;
+      const int lo = w > 0 ? w - 1 : 0;
+      pw[a][j] = w;
+      pl[a][j] = i - deg * lo;
+      pc[a][j] = (w > 0 ? 1 : 0) + (w < n ? 1 : 0);
+      if (n < 4) { pac[a][j] = w; ppos[a][j] = 0; pcn[a][j] = 1; }
+      else {
+        const int ac = w == 0 ? 0 : (w == 1 ? 1 : (w == n ? 4 : (w == n - 1 ? 3 : 2)));
+        pac[a][j] = ac;
+        ppos[a][j] = ac == 2 ? w - 2 : 0;
+        pcn[a][j] = ac == 2 ? n - 3 : 1;
+      }
+    }
+  }
+  long long pbase[NPMAX];
+  int pcol[NPMAX], pnc[NPMAX], pmh[NPMAX], pnq[NPMAX], pblk[NPMAX];
+#pragma unroll
+  for (int i3 = 0; i3 < (D == 3 ? 3 : 1); ++i3)
+#pragma unroll
+    for (int i2 = 0; i2 < 3; ++i2)
+#pragma unroll
+      for (int i1 = 0; i1 < 3; ++i1) {
+        const int s = (i3 * 3 + i2) * 3 + i1;
+        if (s >= NPMAX) continue;
+        const bool ok = i1 < cnt[0] && i2 < cnt[1] && (D == 2 || i3 < cnt[2]);
+        const int j[3] = {i1, i2, i3};
+        int loc = 0, ls = 1, nQ = 1, nP = 1, cid = 0, cstr = 1, col = 0, colstr = 1;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const int qb = R * pc[a][j[a]] + 1, pb = (R - 1) * pc[a][j[a]] + 1;
+          loc += pl[a][j[a]] * ls;
+          ls *= pres ? pb : qb;
+          nQ *= qb;
+          nP *= pb;
+          cid += pac[a][j[a]] * cstr;
+          cstr *= ncls[a];
+          col += ppos[a][j[a]] * colstr;
+          colstr *= pcn[a][j[a]];
+        }
+        pbase[s] = ok ? cls[cid].rexp_off : -1;
+        pnc[s] = ok ? cls[cid].ncols : 0;
+        pcol[s] = col;
+        pmh[s] = loc + (pres ? 2 * D * nQ : 0);
+        pnq[s] = nQ;
+        pblk[s] = 2 * D * nQ + nP;
+      }
+  const long long blockN = g.block;
+  const long long node_off = pres ? 2 * g.R + node : (long long)node;
+  const double* Yv[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) Yv[c] = Yc + (off[c] >= 0 ? off[c] : 0);
+  const int nsl = pres ? 1 : 2 * D;
+  pdl_wait();
+#pragma unroll 1
+  for (int m = 0; m < K1; ++m) {
+#pragma unroll 1
+    for (int sl = 0; sl < nsl; ++sl) {
+      const long long eadd = (long long)(m * NE1 + sl * NQE) * estride;
+      double v[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) v[c] = off[c] >= 0 ? __ldg(Yv[c] + eadd) : 0.0;
+      double sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sum += off[c] >= 0 ? v[c] : 0.0;
+      const long long mu = m * blockN + node_off + (pres ? 0 : (long long)sl * g.nq);
+      const double val = beta * base[mu] + alpha * sum;
+#pragma unroll
+      for (int s = 0; s < NPMAX; ++s) {
+        if (pbase[s] < 0) continue;
+        const int mh = pmh[s] + m * pblk[s] + (pres ? 0 : sl * pnq[s]);
+        rexp[pbase[s] + (long long)(mh >> 4) * pnc[s] * 16 + pcol[s] * 16 + ((mh & 15) ^ ((pcol[s] & 3) << 2))] = val;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------------ K5 --------
 // b_c = P^T r_f: one thread per coarse node, 1D supports from the coarse-row CSR tables.
 template <int D, int K1>
@@ -371,6 +530,14 @@ cudaError_t launch_op_gather(const LevelGeom& g, int r, int k1, const double* Yc
   STGMG_DRK(g.d, r, k1,
             return launch_pdl(gather_nodal_kernel<D_, R_, K_>, dim3(node_blocks(g), (unsigned)batch), dim3(128), 0, s,
                               g, Yc, base, y, alpha, beta, stride, ycstride, ldpm));
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_gather_expand(const LevelGeom& g, int r, int k1, const double* Yc, const double* base, double alpha,
+                                 double beta, int ldpm, const PatchClass* cls, double* rexp, cudaStream_t s) {
+  STGMG_DRK(g.d, r, k1,
+            return launch_pdl(gather_expand_kernel<D_, R_, K_>, dim3(node_blocks(g)), dim3(128), 0, s, g, Yc, base,
+                              alpha, beta, ldpm, cls, rexp));
   return cudaErrorNotSupported;
 }
 

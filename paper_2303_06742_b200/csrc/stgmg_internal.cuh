@@ -53,6 +53,7 @@ struct PatchClass {
   int cells[3];                // cells of the patch per axis (1 or 2)
   long long rel_off;           // offset of this class's relidx table (cp entries)
   long long inv_off;           // offset of the class inverse (lda x lda)
+  long long rexp_off;          // offset of the class block of the expanded residual (dense K2), -1 if unused
 };
 
 struct TileDesc {              // one CTA tile of the grouped patch GEMM: rows [m0, m0+BM), columns [n0, n0+nn)
@@ -124,6 +125,14 @@ cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const Patc
 cudaError_t launch_colour_update(const LevelGeom& g, int r, const PatchClass* cls, const int2* items, int nitems,
                                  const int* relidx, const double* Y, int ldy, double omega, double* dvec,
                                  cudaStream_t s);
+// K2D: dense K2 on the patch-expanded residual (variant 2 = 112 x 32 tiles, 6 = 112 x 64), bulk copies only.
+cudaError_t launch_patch_gemm_dense(const LevelGeom& g, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
+                                    int ntiles, const double* invc, int lda, const double* rexp, double* Y, int ldy,
+                                    cudaStream_t s);
+int k2d_slots(int variant);
+// K1e: residual written in patch-expanded, class chunk-major swizzled form (B operand of the dense K2).
+cudaError_t launch_gather_expand(const LevelGeom& g, int r, int k1, const double* Yc, const double* base, double alpha,
+                                 double beta, int ldpm, const PatchClass* cls, double* rexp, cudaStream_t s);
 // K3: d <- (zero ? 0 : d) + omega * (sum_P Y_P[mu_hat]) / p_mu   (pull form, lexicographic patch order).
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
                                  int zero_init, double* dvec, cudaStream_t s);

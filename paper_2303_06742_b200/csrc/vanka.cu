@@ -348,6 +348,200 @@ static int k2_occ(int cn) {
   return nclusters * cn;
 }
 
+// K2D: dense variant of K2 for large levels.  The residual arrives patch-expanded (gather_expand_kernel: class
+// chunk-major, bank-swizzled, zero beyond C_P), so BOTH operands of a chunk are single contiguous bulk async copies.
+// Warp-specialised: one producer warp (one elected lane issues the two copies per chunk; completion counted on the
+// stage's "full" mbarrier by transaction bytes), NCONS consumer warps wait on "full", run the DMMAs and release the
+// stage on its "empty" mbarrier.  Same k order and split-K reduction as K2: identical arithmetic.
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <int MT, int NT, int NJ, int KS>
+__device__ __forceinline__ void k2d_mma(double (&acc)[MT][NT][2], const double (*A)[16], const double (*B)[16], int wm,
+                                        int wn, int kslice, int lane, int swz) {
+#pragma unroll
+  for (int ks = kslice * 4; ks < 16; ks += 4 * KS) {
+    double af[MT], bf[NJ];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) af[i] = A[wm + i * 8 + (lane >> 2)][(ks + (lane & 3)) ^ swz];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) bf[j] = B[wn + j * 8 + (lane >> 2)][(ks + (lane & 3)) ^ swz];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+}
+
+template <int WM, int WN, int MT, int NT, int STAGES, int KS>
+struct K2DCfg {
+  static constexpr int BM = WM * MT * 8, BN = WN * NT * 8, NCONS = WM * WN * KS, THREADS = 32 * (NCONS + 1);
+  static constexpr size_t ABYTES = sizeof(double) * BM * K2_BK;
+  static constexpr size_t PIPE = sizeof(double) * STAGES * (BM + BN) * K2_BK;
+  static constexpr size_t RED = sizeof(double) * (KS - 1) * BM * BN;
+  static constexpr size_t BAR_OFF = (PIPE > RED ? PIPE : RED);
+  static constexpr size_t SMEM = BAR_OFF + 16 * STAGES;
+};
+
+template <int WM, int WN, int MT, int NT, int S, int KS>
+__global__ void __launch_bounds__(32 * (WM * WN * KS + 1), 2)
+    patch_gemm_dense_kernel(LevelGeom g, const PatchClass* __restrict__ cls, const TileDesc* __restrict__ tiles,
+                            const double* __restrict__ invc, int lda, const double* __restrict__ rexp,
+                            double* __restrict__ Y, int ldy) {
+  using C = K2DCfg<WM, WN, MT, NT, S, KS>;
+  constexpr int BM = C::BM, BN = C::BN, NCONS = C::NCONS;
+  extern __shared__ __align__(128) double k2dsmem[];
+  double(*As)[BM][K2_BK] = reinterpret_cast<double(*)[BM][K2_BK]>(k2dsmem);
+  double(*Bs)[BN][K2_BK] = reinterpret_cast<double(*)[BN][K2_BK]>(k2dsmem + S * BM * K2_BK);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(k2dsmem) + C::BAR_OFF);
+  unsigned long long* empty = full + S;
+  __shared__ int plin[BN];
+  const TileDesc td = tiles[blockIdx.x];
+  const PatchClass pc = cls[td.cls];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cp = pc.cp;
+  const int nchunks = (cp + K2_BK - 1) / K2_BK;
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int t = tid; t < BN; t += C::THREADS) {
+    int pl = -1;
+    if (t < td.nn && td.n0 + t < pc.ncols) {
+      int rem = td.n0 + t, vs = 1;
+      pl = 0;
+      for (int a = 0; a < g.d; ++a) {
+        const int v = pc.vlo[a] + (rem % pc.cnt[a]) * pc.vst;
+        rem /= pc.cnt[a];
+        pl += v * vs;
+        vs *= (g.n[a] + 1);
+      }
+    }
+    plin[t] = pl;
+  }
+  __syncthreads();
+  const int kslice = warp / (WM * WN);
+  const int wt = warp % (WM * WN);
+  const int wm = (wt % WM) * (MT * 8), wn = (wt / WM) * (NT * 8);
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (warp == NCONS) {
+    if (lane == 0) {   // producer: A (static) and B (expanded residual of the previous kernel) per chunk
+      const double* Ab = invc + pc.inv_off + (long long)td.m0 * K2_BK;
+      const long long achunk = (long long)lda * K2_BK;
+      const double* Bb = rexp + pc.rexp_off + (long long)td.n0 * K2_BK;
+      const long long bchunk = (long long)pc.ncols * K2_BK;
+      const unsigned bbytes = (unsigned)(td.nn * K2_BK * sizeof(double));
+      pdl_wait();
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int st = ch % S;
+        if (ch >= S) mbar_wait(&empty[st], (unsigned)(((ch / S) - 1) & 1));
+        mbar_expect_tx(&full[st], (unsigned)C::ABYTES + bbytes);
+        bulk_copy(&As[st][0][0], Ab + ch * achunk, (unsigned)C::ABYTES, &full[st]);
+        bulk_copy(&Bs[st][0][0], Bb + ch * bchunk, bbytes, &full[st]);
+      }
+    }
+  } else {
+    const int swz = ((lane >> 2) & 3) << 2;
+    const int nj = td.nn > wn ? min(NT, (td.nn - wn + 7) / 8) : 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int st = ch % S;
+      mbar_wait(&full[st], (unsigned)((ch / S) & 1));
+      if (nj == NT) k2d_mma<MT, NT, NT, KS>(acc, As[st], Bs[st], wm, wn, kslice, lane, swz);
+      else if (nj == NT - 1) k2d_mma<MT, NT, (NT > 1 ? NT - 1 : 1), KS>(acc, As[st], Bs[st], wm, wn, kslice, lane, swz);
+      else if (nj == NT - 2) k2d_mma<MT, NT, (NT > 2 ? NT - 2 : 1), KS>(acc, As[st], Bs[st], wm, wn, kslice, lane, swz);
+      else if (nj == NT - 3) k2d_mma<MT, NT, (NT > 3 ? NT - 3 : 1), KS>(acc, As[st], Bs[st], wm, wn, kslice, lane, swz);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  __syncthreads();   // all chunks consumed: the pipe buffer can take the split-K partial sums
+  if (warp == NCONS) return;
+  if (KS > 1) {
+    double* red = k2dsmem;
+    if (kslice > 0) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            red[((kslice - 1) * BM + wm + i * 8 + (lane >> 2)) * BN + wn + j * 8 + 2 * (lane & 3) + e] = acc[i][j][e];
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * NCONS) : "memory");
+    if (kslice > 0) return;
+    for (int sl = 1; sl < KS; ++sl)
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            acc[i][j][e] += red[((sl - 1) * BM + wm + i * 8 + (lane >> 2)) * BN + wn + j * 8 + 2 * (lane & 3) + e];
+  }
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = td.m0 + wm + i * 8 + (lane >> 2);
+        const int nn = wn + j * 8 + 2 * (lane & 3) + e;
+        if (row < cp && plin[nn] >= 0) Y[(long long)plin[nn] * ldy + row] = acc[i][j][e];
+      }
+}
+
+#define K2D_BIG 2, 2, 7, 2, 5, 2    // 112 x 32, 8 consumer warps (2-way split-K) + producer
+#define K2D_WIDE 2, 4, 7, 2, 4, 1   // 112 x 64, 8 consumer warps + producer
+
+template <int WM, int WN, int MT, int NT, int S, int KS>
+static cudaError_t launch_k2d(const LevelGeom& g, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
+                              const double* invc, int lda, const double* rexp, double* Y, int ldy, cudaStream_t s) {
+  using C = K2DCfg<WM, WN, MT, NT, S, KS>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(patch_gemm_dense_kernel<WM, WN, MT, NT, S, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
+    attr = true;
+  }
+  return launch_pdl(patch_gemm_dense_kernel<WM, WN, MT, NT, S, KS>, dim3(ntiles), dim3(C::THREADS), C::SMEM, s, g,
+                    cls_dev, tiles, invc, lda, rexp, Y, ldy);
+}
+
+// variant 2 (big tiles) or 6 (wide tiles) of the dense K2
+cudaError_t launch_patch_gemm_dense(const LevelGeom& g, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
+                                    int ntiles, const double* invc, int lda, const double* rexp, double* Y, int ldy,
+                                    cudaStream_t s) {
+  if (variant == 6) return launch_k2d<K2D_WIDE>(g, cls_dev, tiles, ntiles, invc, lda, rexp, Y, ldy, s);
+  return launch_k2d<K2D_BIG>(g, cls_dev, tiles, ntiles, invc, lda, rexp, Y, ldy, s);
+}
+
+int k2d_slots(int variant) {
+  int nb = 0;
+  cudaError_t e;
+  if (variant == 6) {
+    using C = K2DCfg<K2D_WIDE>;
+    cudaFuncSetAttribute(patch_gemm_dense_kernel<K2D_WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_dense_kernel<K2D_WIDE>, C::THREADS, C::SMEM);
+  } else {
+    using C = K2DCfg<K2D_BIG>;
+    cudaFuncSetAttribute(patch_gemm_dense_kernel<K2D_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_dense_kernel<K2D_BIG>, C::THREADS, C::SMEM);
+  }
+  if (e != cudaSuccess || nb <= 0) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  return nb * 148;
+}
+
 // K2L: latency variant of K2 for small levels (few patches; the V-cycle there is a chain of latency-bound kernels).
 // CTA = 8*MT rows x 8 patch columns of one class.  No shared-memory pipeline: warp w takes the 16-wide K chunks
 // w, w + nw, ..; every lane loads its m8n8k4 A fragments straight from the chunk-major inverse (L2) and its B
