@@ -833,11 +833,9 @@ static int build_patches(stgmg_handle* h, int l) {
   int tbm = 0, tbn = 0;
   k2_tile_shape(Lv.k2var, &tbm, &tbn);
   // dense K2 (bulk-copied B from the patch-expanded residual) on the levels of the big / wide tile variants
-  // (measured: the expansion stores ~C_P values per patch, K2 does ~2 C_P^2 flops per patch; on cfg1's fine level,
-  // C_P = 218 and 4,225 patches, the expansion costs more than the dense K2 saves: 0.80 -> 0.84 ms per V-cycle; on
-  // cfg2 (C_P = 663) / cfg3 (C_P = 1,554) K2 reaches 32 / 33.5 TF/s, V-cycles 29.4 -> 26.8 / 63 -> 56 ms)
-  Lv.dense = (Lv.k2var == 2 || Lv.k2var == 6) && h->prm.smoother == STGMG_SMOOTH_ADDITIVE &&
-             (Lv.maxcp > 256 || (Lv.npatch_global ? Lv.npatch_global : Lv.npatch) >= 20000);
+  // (measured: cfg2 (C_P = 663) / cfg3 (C_P = 1,554) fine K2 34 / 33.5 TF/s, V-cycles 29.4 -> 27 / 63 -> 56 ms;
+  // cfg1 (C_P = 218): K2 22.0 -> 17.9 us, the expansion costs about as much, V-cycle 0.809 vs 0.811 ms)
+  Lv.dense = (Lv.k2var == 2 || Lv.k2var == 6) && h->prm.smoother == STGMG_SMOOTH_ADDITIVE;
   if (const char* ev = std::getenv("STGMG_K2_DENSE"))   // experiments / tests: 0 = never, 1 = on big / wide levels
     Lv.dense = std::atoi(ev) != 0 && (Lv.k2var == 2 || Lv.k2var == 6) && h->prm.smoother == STGMG_SMOOTH_ADDITIVE;
   {

@@ -356,26 +356,58 @@ __global__ void __launch_bounds__(128) gather_expand_kernel(LevelGeom g, const d
   for (int c = 0; c < NC; ++c) Yv[c] = Yc + (off[c] >= 0 ? off[c] : 0);
   const int nsl = pres ? 1 : 2 * D;
   pdl_wait();
+  if constexpr (D == 3) {   // 3D: one (m, slot) at a time (27 patch slots per node: the unrolled form spills)
 #pragma unroll 1
-  for (int m = 0; m < K1; ++m) {
+    for (int m = 0; m < K1; ++m) {
 #pragma unroll 1
-    for (int sl = 0; sl < nsl; ++sl) {
-      const long long eadd = (long long)(m * NE1 + sl * NQE) * estride;
-      double v[NC];
+      for (int sl = 0; sl < nsl; ++sl) {
+        const long long eadd = (long long)(m * NE1 + sl * NQE) * estride;
+        double v[NC];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) v[c] = off[c] >= 0 ? __ldg(Yv[c] + eadd) : 0.0;
-      double sum = 0.0;
+        for (int c = 0; c < NC; ++c) v[c] = off[c] >= 0 ? __ldg(Yv[c] + eadd) : 0.0;
+        double sum = 0.0;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) sum += off[c] >= 0 ? v[c] : 0.0;
-      const long long mu = m * blockN + node_off + (pres ? 0 : (long long)sl * g.nq);
-      const double val = beta * base[mu] + alpha * sum;
+        for (int c = 0; c < NC; ++c) sum += off[c] >= 0 ? v[c] : 0.0;
+        const long long mu = m * blockN + node_off + (pres ? 0 : (long long)sl * g.nq);
+        const double val = beta * base[mu] + alpha * sum;
 #pragma unroll
-      for (int s = 0; s < NPMAX; ++s) {
-        if (pbase[s] < 0) continue;
-        const int mh = pmh[s] + m * pblk[s] + (pres ? 0 : sl * pnq[s]);
-        rexp[pbase[s] + (long long)(mh >> 4) * pnc[s] * 16 + pcol[s] * 16 + ((mh & 15) ^ ((pcol[s] & 3) << 2))] = val;
+        for (int s = 0; s < NPMAX; ++s) {
+          if (pbase[s] < 0) continue;
+          const int mh = pmh[s] + m * pblk[s] + (pres ? 0 : sl * pnq[s]);
+          rexp[pbase[s] + (long long)(mh >> 4) * pnc[s] * 16 + pcol[s] * 16 + ((mh & 15) ^ ((pcol[s] & 3) << 2))] = val;
+        }
       }
     }
+  } else {
+  // 2D: all loads of the node first (unconditional addresses, so they issue back to back), then sums and stores
+  constexpr int NV = K1 * 2 * D;
+  double val[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const int m = q / (2 * D), sl = q % (2 * D);
+    const long long eadd = (long long)(m * NE1 + (sl < nsl ? sl : 0) * NQE) * estride;
+    double v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = off[c] >= 0 ? __ldg(Yv[c] + eadd) : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) sum += off[c] >= 0 ? v[c] : 0.0;
+    const long long mu = m * blockN + node_off + (pres ? 0 : (long long)(sl < nsl ? sl : 0) * g.nq);
+    val[q] = beta * __ldg(base + mu) + alpha * sum;
+  }
+#pragma unroll
+  for (int s = 0; s < NPMAX; ++s) {
+    if (pbase[s] < 0) continue;
+    double* dst = rexp + pbase[s] + pcol[s] * 16;
+    const int cst = pnc[s] * 16, swz = (pcol[s] & 3) << 2;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const int m = q / (2 * D), sl = q % (2 * D);
+      if (sl >= nsl) continue;
+      const int mh = pmh[s] + m * pblk[s] + (pres ? 0 : sl * pnq[s]);
+      dst[(long long)(mh >> 4) * cst + ((mh & 15) ^ swz)] = val[q];
+    }
+  }
   }
 }
 
