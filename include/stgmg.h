@@ -52,6 +52,7 @@ enum { STGMG_TOL_REL = 0 /* ||r|| <= tol ||b|| (BASELINE) */, STGMG_TOL_ABS = 1 
 enum { STGMG_SMOOTH_ADDITIVE = 0 /* Alg. 1 with averaging, P:L488-524 (default) */,
        STGMG_SMOOTH_COLORED_MULT = 1 /* Eq:VankaOP0 with successive overwriting, patches
                                         ordered by vertex colour (v mod 4 per axis); single GPU only */ };
+enum { STGMG_LOAD_MANUFACTURED = 0, STGMG_LOAD_BEAM_TRACTION = 1 };   /* stgmg_slab_load */
 enum { STGMG_COMM_NCCL = 0 /* nccl_comm is an ncclComm_t */,
        STGMG_COMM_LOOPBACK = 1 /* nccl_comm is an in-process hub (N emulated ranks on one GPU; tests) */ };
 
@@ -136,6 +137,19 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
 /* Same as stgmg_solve with HOST buffers: copies rhs host->device and x both ways inside the call. */
 int stgmg_solve_host(stgmg_handle* h, const double* rhs_host, double* x_host, double tol, int tol_mode,
                      int restart, int maxit, stgmg_stats* stats);
+
+/* SURVEY §8(f) N1, on-device load assembly: load = L_n of the slab (t_n, t_n + tau] in the slab layout — at Radau
+ * node b, U slot (chi rows) theta_b F_gamma(t_{n,b}), P slot (psi rows) theta_b G_gamma(t_{n,b}), V slot 0, with
+ * t_{n,b} = t_n + tau/2 (t_hat_b + 1) (Def:LG P:L215-228).  kind STGMG_LOAD_MANUFACTURED: the body loads
+ * of the BASELINE manufactured solution u_i = S sin(2 pi t), p = S cos(2 pi t), S = prod sin(pi x_a) (configs 0/1/3;
+ * reading A8), (r+2)^d Gauss points per cell (reading A10); STGMG_LOAD_BEAM_TRACTION: + sin(pi t/2) int_{x=hi}
+ * chi_{d-1} (config 4, reading A23).  Homogeneous Dirichlet data only (readings A26, A31).  load: caller-owned device
+ * vector of stgmg_local_size(fine); F_n = stgmg_slab_rhs(load, X_{n-1}). */
+int stgmg_slab_load(stgmg_handle* h, int kind, double t_n, double* load);
+
+/* x = 0 except its LAST Radau block = nodal interpolation of (v(t0), u(t0), p(t0)) of the manufactured
+ * solution (reading A20; zero for STGMG_LOAD_BEAM_TRACTION), i.e. the X_0 that stgmg_slab_rhs reads for slab 1. */
+int stgmg_initial_state(stgmg_handle* h, int kind, double t0, double* x);
 
 /* Slab RHS: rhs = load + J X_prev, where X_prev is the previous slab's full vector (its last
  * Radau block is the state at t_{n-1}) and J puts chi_b(-1) M_rho U, chi_b(-1) M_rho V,

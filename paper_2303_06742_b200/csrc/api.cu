@@ -370,6 +370,7 @@ struct stgmg_handle {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   OpConsts* c_dev = nullptr;    // operator constants (device copy, read by the 2D cell kernel)
   OpConsts* cj_dev = nullptr;   // slab-RHS variant: T'_ba = chi_b(-1) delta_{a,k}, theta = 0 (K8)
+  LoadConsts* lc_dev = nullptr; // on-device load assembly / initial data
   double* Yc = nullptr;         // element results of the 2D cell kernel (largest level)
   double* Ycell = nullptr;      // element results of the 3D element GEMM, patch-major (largest level)
   // multi-GPU
@@ -1615,6 +1616,37 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     CK(dalloc(h.get(), &h->cj_dev, 1));
     CKE(cudaMemcpy(h->c_dev, &h->c, sizeof(OpConsts), cudaMemcpyHostToDevice));
     CKE(cudaMemcpy(h->cj_dev, &cj, sizeof(OpConsts), cudaMemcpyHostToDevice));
+    {   // load-assembly constants: (r+2)-point Gauss rule, bases, GLL nodes, Radau nodes, data
+      LoadConsts lc;
+      std::memset(&lc, 0, sizeof(lc));
+      std::vector<double> xg, wg;
+      gauss01(r + 2, xg, wg);
+      const auto nq = gll01(r), npn = gll01(r - 1);
+      for (int q = 0; q < r + 2; ++q) {
+        lc.xg[q] = xg[q];
+        lc.wg[q] = wg[q];
+        for (int j = 0; j <= r; ++j) lc.Bq[q][j] = lag(nq, j, xg[q]);
+        for (int j = 0; j < r; ++j) lc.Bp[q][j] = lag(npn, j, xg[q]);
+      }
+      for (int s = 0; s < 2; ++s)
+        for (int j = 0; j <= r; ++j) lc.Eq[s][j] = lag(nq, j, (double)s);
+      for (int j = 0; j <= r; ++j) lc.gllq[j] = nq[j];
+      for (int j = 0; j < r; ++j) lc.gllp[j] = npn[j];
+      std::vector<double> tr, wr;
+      radau(k, tr, wr);
+      for (int b = 0; b <= k; ++b) {
+        lc.that[b] = tr[b];
+        lc.theta[b] = h->c.theta[b];
+      }
+      const LevelData& F = h->lev[levels - 1];
+      for (int a0 = 0; a0 < 3; ++a0) lc.lo[a0] = mesh->lo[a0] + (a0 == 0 ? F.w0 * F.g.h[0] : 0.0);
+      lc.rho = params->rho; lc.alpha = params->alpha; lc.c0 = params->c0; lc.lam = params->lambda; lc.mu = params->mu;
+      for (int i = 0; i < 9; ++i) lc.K[i] = params->K[i];
+      lc.r = r;
+      lc.xhi_cell = (F.w0 + F.g.n[0] == (F.gnx ? F.gnx : F.g.n[0])) ? F.g.n[0] - 1 : -1;
+      CK(dalloc(h.get(), &h->lc_dev, 1));
+      CKE(cudaMemcpy(h->lc_dev, &lc, sizeof(LoadConsts), cudaMemcpyHostToDevice));
+    }
     if (d == 2) CK(dalloc(h.get(), &h->Yc, (size_t)(cell_count(h->lev[levels - 1].g) * elem_dofs(h.get()))));
     if (d == 3) {
       long long nv = 1;
@@ -1735,6 +1767,33 @@ int stgmg_vcycle(stgmg_handle* h, const double* b, double* x) {
   if (!h || !b || !x) { set_error("bad argument"); return STGMG_EINVAL; }
   h->launches = 0;
   CK(vcycle_dev(h, b, x));
+  return sync_if_own(h);
+}
+
+int stgmg_slab_load(stgmg_handle* h, int kind, double t_n, double* load) {
+  if (!h || !load || (kind != STGMG_LOAD_MANUFACTURED && kind != STGMG_LOAD_BEAM_TRACTION)) {
+    set_error("bad argument");
+    return STGMG_EINVAL;
+  }
+  const LevelGeom& g = h->lev[h->L - 1].g;
+  double* yc = h->d == 2 ? h->Yc : h->Ycell;   // element-result scratch (cell-major layout), fine level
+  h->launches = 0;
+  cudaError_t e = launch_load_cells(h->d, h->r, h->k1, g, h->lc_dev, kind, t_n, h->prm.tau, yc, h->s);
+  if (e == cudaErrorNotSupported) { set_error("(d, r, k) combination not compiled"); return STGMG_ENOTSUP; }
+  CKE(e);
+  CKE(launch_op_gather(g, h->r, h->k1, yc, nullptr, load, 1.0, 0.0, 1, 0, 0, h->s, 0));
+  h->launches += 2;
+  return sync_if_own(h);
+}
+
+int stgmg_initial_state(stgmg_handle* h, int kind, double t0, double* x) {
+  if (!h || !x || (kind != STGMG_LOAD_MANUFACTURED && kind != STGMG_LOAD_BEAM_TRACTION)) {
+    set_error("bad argument");
+    return STGMG_EINVAL;
+  }
+  const LevelGeom& g = h->lev[h->L - 1].g;
+  CKE(launch_initial_state(h->d, h->k1, g, h->lc_dev, kind, t0, x, h->s));
+  h->launches = 1;
   return sync_if_own(h);
 }
 

@@ -30,6 +30,20 @@ struct OpConsts {
   double K[9];                 // row-major d x d (stride 3)
 };
 
+// Constants of the on-device load assembly and initial data (csrc/loads.cu).
+struct LoadConsts {
+  double xg[kMaxR1 + 2], wg[kMaxR1 + 2];     // (r+2)-point Gauss rule on [0,1] (reading A10)
+  double Bq[kMaxR1 + 2][kMaxR1];             // Q_r Lagrange basis (GLL nodes) at those points: Bq[q][j]
+  double Bp[kMaxR1 + 2][kMaxR1];             // Q_{r-1}
+  double Eq[2][kMaxR1];                      // Q_r basis at 0 / 1
+  double gllq[kMaxR1], gllp[kMaxR1];         // GLL nodes of Q_r / Q_{r-1} on [0,1] (reading A9)
+  double that[kMaxK1], theta[kMaxK1];        // right Radau nodes on [-1,1], theta_b = tau w_b / 2
+  double lo[3];                              // physical origin of this rank's (window) fine level
+  double rho, alpha, c0, lam, mu, K[9];
+  int r, xhi_cell;                           // local index of the cell at x = hi (-1: not on this rank)
+};
+
+
 // Geometry of one structured level (box split into n[a] cells per axis).
 struct LevelGeom {
   int d;
@@ -133,6 +147,10 @@ int k2d_slots(int variant);
 // K1e: residual written in patch-expanded, class chunk-major swizzled form (B operand of the dense K2).
 cudaError_t launch_gather_expand(const LevelGeom& g, int r, int k1, const double* Yc, const double* base, double alpha,
                                  double beta, int ldpm, const PatchClass* cls, double* rexp, cudaStream_t s);
+cudaError_t launch_load_cells(int d, int r, int k1, const LevelGeom& g, const LoadConsts* lc, int kind, double tn,
+                              double tau, double* Yc, cudaStream_t s);
+cudaError_t launch_initial_state(int d, int k1, const LevelGeom& g, const LoadConsts* lc, int kind, double t0, double* x,
+                                 cudaStream_t s);
 // K3: d <- (zero ? 0 : d) + omega * (sum_P Y_P[mu_hat]) / p_mu   (pull form, lexicographic patch order).
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
                                  int zero_init, double* dvec, cudaStream_t s);

@@ -14,6 +14,7 @@ TOL_REL, TOL_ABS = 0, 1
 BC_DIRICHLET, BC_NEUMANN = 0, 1
 HF_MEASURE, HF_EDGE = 0, 1
 SMOOTH_ADDITIVE, SMOOTH_COLORED_MULT = 0, 1
+LOAD_MANUFACTURED, LOAD_BEAM_TRACTION = 0, 1
 
 
 class Mesh(ctypes.Structure):
@@ -61,6 +62,8 @@ SIGNATURES = {
     "stgmg_solve_host": (ctypes.c_int, [_P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(Stats)]),
     "stgmg_slab_rhs": (ctypes.c_int, [_P, _P, _P, _P]),
+    "stgmg_slab_load": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _P]),
+    "stgmg_initial_state": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _P]),
     "stgmg_destroy": (ctypes.c_int, [_P]),
     "stgmg_last_error": (ctypes.c_char_p, []),
     "stgmg_info": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
@@ -287,6 +290,14 @@ class Solver:
     def slab_rhs(self, load, x_prev, rhs):
         lp = _ptr(load) if load is not None else None
         _check(self.lib.stgmg_slab_rhs(self.h, lp, _ptr(x_prev), _ptr(rhs)), "stgmg_slab_rhs")
+
+    def slab_load(self, kind, t_n, load):
+        """L_n of the slab (t_n, t_n + tau] assembled on the device (LOAD_MANUFACTURED / LOAD_BEAM_TRACTION)."""
+        _check(self.lib.stgmg_slab_load(self.h, int(kind), float(t_n), _ptr(load)), "stgmg_slab_load")
+
+    def initial_state(self, kind, t0, x):
+        """x = 0 except the last Radau block = interpolated initial data (reading A20)."""
+        _check(self.lib.stgmg_initial_state(self.h, int(kind), float(t0), _ptr(x)), "stgmg_initial_state")
 
     def level_work(self, level=None):
         lev = self.levels - 1 if level is None else level

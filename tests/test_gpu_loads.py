@@ -1,0 +1,121 @@
+"""on-device load assembly and initial data vs the oracle (-m gpu).
+
+The oracle assembles the loads from symbolic (sympy) derivatives of the exact solution with its own quadrature
+code (oracle/loads.py); the device evaluates the closed forms (csrc/loads.cu).  Tolerance 1e-12 relative: both
+integrate the same smooth integrands with the same (r+2)^d Gauss rule (reading A10), so only the summation order
+and the libm-vs-closed-form evaluation of sin/cos differ."""
+import numpy as np
+import pytest
+
+from stgmg_inputs import config
+from tests.gpu_common import small_config, oracle_hierarchy, oracle_params, cfg_key, to_gpu, to_np
+from tests.test_gpu_parity import physical_rhs
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("cfg0", config(0)), ("cfg1s", small_config(1)), ("cfg3s", small_config(3)), ("cfg4s", small_config(4))]
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
+def pair(request):
+    import torch
+    from paper_2303_06742_b200 import Solver
+    cfg = dict(request.param[1])
+    cfg["load"] = "beam" if cfg["dim"] == 3 and cfg["bc_u"][1] == 1 else "manufactured"
+    s = Solver(cfg)
+    H = oracle_hierarchy(cfg_key(cfg))
+    yield cfg, s, H
+    s.close()
+    torch.cuda.synchronize()
+
+
+def kind_of(cfg):
+    from paper_2303_06742_b200.stgmg import LOAD_MANUFACTURED, LOAD_BEAM_TRACTION
+    return LOAD_BEAM_TRACTION if cfg["load"] == "beam" else LOAD_MANUFACTURED
+
+
+def test_first_slab_rhs(pair):
+    """F_1 = L_1 + J X_0 assembled entirely on the device equals the oracle's F_1 (initial data + loads)."""
+    import torch
+    cfg, s, H = pair
+    N = H.fine.N
+    X0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+    L = torch.zeros_like(X0)
+    F = torch.zeros_like(X0)
+    s.initial_state(kind_of(cfg), 0.0, X0)
+    s.slab_load(kind_of(cfg), 0.0, L)
+    s.slab_rhs(L, X0, F)
+    torch.cuda.synchronize()
+    Fo = physical_rhs(cfg, H)
+    assert rel(to_np(F), Fo) < 1e-12, rel(to_np(F), Fo)
+
+
+def test_load_later_slab(pair):
+    """L_n at t_n = 3 tau (zero previous state): device vs oracle load vectors at the Radau nodes."""
+    import math
+    import torch
+    from oracle.loads import manufactured_baseline, load_vectors, slab_rhs, traction_face_vector
+    cfg, s, H = pair
+    lev, op = H.fine, H.ops[-1]
+    tn = 3 * cfg["tau"]
+    t_nodes = tn + 0.5 * cfg["tau"] * (op.t_hat + 1.0)
+    S = op.assemble_spatial()
+    Z = np.zeros(lev.R), np.zeros(lev.R), np.zeros(lev.S)
+    if cfg["load"] == "manufactured":
+        sol = manufactured_baseline(lev.d, oracle_params(cfg))
+        FG = [load_vectors(lev, sol, t) for t in t_nodes]
+        Lo = slab_rhs(lev, S, op.chi_m1, op.th, *Z, [f for f, g in FG], [g for f, g in FG])
+    else:
+        Fl = [traction_face_vector(lev, 1, lev.d - 1, math.sin(math.pi * t / 2)) for t in t_nodes]
+        Lo = slab_rhs(lev, S, op.chi_m1, op.th, *Z, Fl, None)
+    L = torch.zeros(lev.N, dtype=torch.float64, device="cuda")
+    s.slab_load(kind_of(cfg), tn, L)
+    torch.cuda.synchronize()
+    assert rel(to_np(L), Lo) < 1e-12, rel(to_np(L), Lo)
+
+
+def test_marching_three_slabs_on_device(pair):
+    """O12 marching: X_0, then three slabs F_n = L_n + J X_{n-1}, solve — all on the device — vs the oracle
+    marching the same three slabs (north_star solution tolerance per slab, accumulated)."""
+    import torch
+    from oracle.gmres import fgmres
+    from oracle.loads import manufactured_baseline, load_vectors, slab_rhs, end_state, interpolate_initial
+    from oracle.loads import traction_face_vector
+    import math
+    cfg, s, H = pair
+    if cfg["dim"] == 3 and cfg["cells"][0] > 8:
+        pytest.skip("3D marching covered by cfg3s")
+    lev, op = H.fine, H.ops[-1]
+    S = op.assemble_spatial()
+    kind = kind_of(cfg)
+    N = lev.N
+    X = torch.zeros(N, dtype=torch.float64, device="cuda")
+    L, F = torch.zeros_like(X), torch.zeros_like(X)
+    s.initial_state(kind, 0.0, X)
+    if cfg["load"] == "manufactured":
+        sol = manufactured_baseline(lev.d, oracle_params(cfg))
+        U, V, P = interpolate_initial(lev, sol, 0.0)
+    else:
+        U, V, P = np.zeros(lev.R), np.zeros(lev.R), np.zeros(lev.S)
+    for n in range(3):
+        tn = n * cfg["tau"]
+        s.slab_load(kind, tn, L)
+        s.slab_rhs(L, X, F)
+        X.zero_()
+        st = s.solve(F, X, tol=cfg["rtol"], restart=cfg["restart"])
+        t_nodes = tn + 0.5 * cfg["tau"] * (op.t_hat + 1.0)
+        if cfg["load"] == "manufactured":
+            FG = [load_vectors(lev, sol, t) for t in t_nodes]
+            Fo = slab_rhs(lev, S, op.chi_m1, op.th, U, V, P, [f for f, g in FG], [g for f, g in FG])
+        else:
+            Fl = [traction_face_vector(lev, 1, lev.d - 1, math.sin(math.pi * t / 2)) for t in t_nodes]
+            Fo = slab_rhs(lev, S, op.chi_m1, op.th, U, V, P, Fl, None)
+        Xo, info = fgmres(lambda v: H.A[-1] @ v, Fo, H.vcycle, tol=cfg["rtol"], restart=cfg["restart"])
+        assert st["converged"] and abs(st["iterations"] - info["iterations"]) <= 1
+        U, V, P = end_state(lev, Xo)
+    torch.cuda.synchronize()
+    assert rel(to_np(X), Xo) < 1e-7, rel(to_np(X), Xo)
