@@ -51,8 +51,9 @@ def all_cell_dofs(lev):
 class SlabOperator:
     """A_n on one level: T (x) calM + diag(theta) (x) calK."""
 
-    def __init__(self, lev, params, tau):
+    def __init__(self, lev, params, tau, ds=False):
         self.lev = lev
+        self.ds = ds   # Problem B.1 (DS) instead of Problem 3.1 (DSA), SURVEY N4
         self.params = full_params(params, lev.r)
         self.tau = float(tau)
         self.t_hat, self.w_hat, self.chi_m1, self.T = temporal_constants(lev.k)
@@ -73,7 +74,7 @@ class SlabOperator:
 
     def slab(self, key):
         if key not in self._slab:
-            self._slab[key] = slab_element_matrix(self.mats(key), self.T, self.th)
+            self._slab[key] = slab_element_matrix(self.mats(key), self.T, self.th, self.ds)
         return self._slab[key]
 
     def assemble(self):

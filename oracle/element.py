@@ -164,7 +164,7 @@ class ElementForms:
         return {"Mq": Mq, "Mp": Mp, "Mrho": Mrho, "Mc": Mc, "A": A, "C": C, "B": B}
 
 
-def slab_element_matrix(mats, T, th):
+def slab_element_matrix(mats, T, th, ds=False):
     """Element slab matrix in element DoF order (m, f in (V,U,P), c, node), P:L233-256 (Eq:DPQ_A0).
 
     Rows are the test slots (phi, chi, psi) at node b aligned with the columns (V, U, P) at node a
@@ -172,6 +172,8 @@ def slab_element_matrix(mats, T, th):
       [phi_b, V_a] = -theta_b d_ab M_rho   [phi_b, U_a] = T_ba M_rho
       [chi_b, V_a] = T_ba M_rho            [chi_b, U_a] = theta_b d_ab A   [chi_b, P_a] = theta_b d_ab C^T
       [psi_b, V_a] = -theta_b d_ab C       [psi_b, P_a] = T_ba M_c + theta_b d_ab B
+    ds=True: Problem B.1 (DS): the pressure equation keeps d_t u instead of v,
+    -Q_n(C(d_t u, psi)) - C(u^+(t_{n-1}), psi^+) = -sum_a T_ba C U_a, i.e. [psi_b, U_a] = -T_ba C, [psi_b, V_a] = 0.
     """
     Mr, Mc, A, C, B = mats["Mrho"], mats["Mc"], mats["A"], mats["C"], mats["B"]
     nv, ns = Mr.shape[0], Mc.shape[0]
@@ -185,11 +187,14 @@ def slab_element_matrix(mats, T, th):
             blk[sV, sU] = T[b, a] * Mr
             blk[sU, sV] = T[b, a] * Mr
             blk[sP, sP] = T[b, a] * Mc
+            if ds:
+                blk[sP, sU] = -T[b, a] * C
             if a == b:
                 blk[sV, sV] = -th[b] * Mr
                 blk[sU, sU] = th[b] * A
                 blk[sU, sP] = th[b] * C.T
-                blk[sP, sV] = -th[b] * C
+                if not ds:
+                    blk[sP, sV] = -th[b] * C
                 blk[sP, sP] += th[b] * B
             E[b * nb:(b + 1) * nb, a * nb:(a + 1) * nb] = blk
     return E

@@ -42,12 +42,12 @@ def _field_errors(lev, quad, sol, U, V, P, t):
     return np.array([e_gu, e_v, e_p])
 
 
-def march_errors(lev, params, sol, t0, T_end, n_slabs, nt=None, linf_M=0):
+def march_errors(lev, params, sol, t0, T_end, n_slabs, nt=None, linf_M=0, ds=False):
     """March n_slabs slabs of length (T_end - t0)/n_slabs with direct solves; return the error norms.
 
     Returns dict with 'L2' (3,), 'linf_tn' (3,), and 'Linf' (3,) if linf_M > 0."""
     tau = (T_end - t0) / n_slabs
-    op = SlabOperator(lev, params, tau)
+    op = SlabOperator(lev, params, tau, ds)
     A = op.assemble().tocsc()
     lu = spla.splu(A)
     spatial = op.assemble_spatial()
@@ -71,7 +71,7 @@ def march_errors(lev, params, sol, t0, T_end, n_slabs, nt=None, linf_M=0):
             F, G = load_vectors(lev, sol, t_nodes[b], quad)
             Fl.append(F)
             Gl.append(G)
-        rhs = slab_rhs(lev, spatial, op.chi_m1, op.th, U, V, P, Fl, Gl)
+        rhs = slab_rhs(lev, spatial, op.chi_m1, op.th, U, V, P, Fl, Gl, ds)
         X = lu.solve(rhs)
         blocks = [(X[m * lev.block + lev.R: m * lev.block + 2 * lev.R],
                    X[m * lev.block: m * lev.block + lev.R],

@@ -164,12 +164,16 @@ def traction_face_vector(lev, face, comp, amplitude=1.0):
     return F
 
 
-def slab_rhs(lev, spatial, chi_m1, th, U_prev, V_prev, P_prev, Floads, Gloads):
-    """Assemble F_n in ABI layout.  Floads[b], Gloads[b]: spatial loads at t_{n,b} (None = 0)."""
+def slab_rhs(lev, spatial, chi_m1, th, U_prev, V_prev, P_prev, Floads, Gloads, ds=False):
+    """Assemble F_n in ABI layout.  Floads[b], Gloads[b]: spatial loads at t_{n,b} (None = 0).
+    ds=True (Problem B.1): the jump term of the pressure equation adds -chi_b(-1) C U^{n-1} to the
+    psi-row (the u^- part of -C([u]_{n-1}, psi^+))."""
     Rv = np.zeros(lev.N)
     MU = spatial["Mrho"] @ U_prev
     MV = spatial["Mrho"] @ V_prev
     MP = spatial["Mc"] @ P_prev
+    if ds:
+        MP = MP - spatial["C"] @ U_prev
     for b in range(lev.k + 1):
         o = b * lev.block
         Rv[o: o + lev.R] = chi_m1[b] * MU

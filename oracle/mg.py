@@ -15,9 +15,9 @@ from .vanka import Patches, VankaSmoother, equilibrated_inverse
 
 class Hierarchy:
     def __init__(self, d, cells, lo, hi, r, k, nlevels, params, tau, bc_u=None, bc_p=None,
-                 omega=0.7, jmax=4, share_classes=True, colored=False):
+                 omega=0.7, jmax=4, share_classes=True, colored=False, ds=False):
         self.levels = hierarchy(d, cells, lo, hi, r, k, nlevels, bc_u, bc_p)
-        self.ops = [SlabOperator(lv, params, tau) for lv in self.levels]
+        self.ops = [SlabOperator(lv, params, tau, ds) for lv in self.levels]
         self.A = [op.assemble() for op in self.ops]
         self.P = [None] + [prolongation(self.levels[l - 1], self.levels[l]) for l in range(1, nlevels)]
         self.jmax = jmax

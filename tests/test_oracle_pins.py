@@ -481,3 +481,50 @@ def test_N2_multiplicative_gmg_converges(cfg0):
     xs = spla.spsolve(Hm.A[-1].tocsc(), b)
     assert info["iterations"] <= 30
     assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
+
+
+# ---------------------------------------------------------------- N4: Problem B.1 (DS) -----------------------
+def test_N4_ds_equals_dsa_on_steady_states():
+    """Problem B.1 couples d_t u (not v) into the pressure equation, via -sum_a T_ba C U_a on the left and
+    -chi_b(-1) C U^{n-1} on the right.  For a state steady in time (V = 0, U_a = U^{n-1} = U0, P_a = P^{n-1} = P0)
+    d_t u = v = 0 in both formulations, so F_n - A_n X must be the same for DS and DSA: the row sums of T equal
+    chi(-1) (App. A.2), which makes the DS coupling cancel exactly; a wrong sign or slot breaks it."""
+    lev = Level(2, [4, 4], [0, 0], [1, 1], 2, 1)
+    rng = np.random.default_rng(21)
+    U0, P0 = rng.standard_normal(lev.R), rng.standard_normal(lev.S)
+    V0 = np.zeros(lev.R)
+    X = np.zeros(lev.N)
+    for m in range(lev.k + 1):
+        o = m * lev.block
+        X[o + lev.R: o + 2 * lev.R] = U0
+        X[o + 2 * lev.R: o + lev.block] = P0
+    res = []
+    for ds in (False, True):
+        op = SlabOperator(lev, P0_params(), 0.01, ds)
+        S = op.assemble_spatial()
+        F = slab_rhs(lev, S, op.chi_m1, op.th, U0, V0, P0, None, None, ds)
+        res.append(F - op.assemble() @ X)
+    assert np.abs(res[0] - res[1]).max() < 1e-12 * np.abs(res[0]).max()
+    # and the DS operator really differs from DSA on a non-steady state
+    opd, opa = SlabOperator(lev, P0_params(), 0.01, True), SlabOperator(lev, P0_params(), 0.01, False)
+    Y = rng.standard_normal(lev.N)
+    assert np.abs(opd.assemble() @ Y - opa.assemble() @ Y).max() > 1e-6
+
+
+def P0_params():
+    return dict(P0)
+
+
+def test_N4_ds_eoc_baseline_family():
+    """P6 for Problem B.1: the DS discretisation converges with the same order ~2 ('identical convergence
+    behaviour' of both formulations), and its errors stay within a factor 2 of the DSA errors."""
+    errs, errs_a = [], []
+    for lvl in range(3):
+        n = 4 * 2 ** lvl
+        lev = Level(2, [n, n], [0, 0], [1, 1], 2, 1)
+        errs.append(march_errors(lev, P0, manufactured_baseline(2, P0), 0.0, 0.2, 2 * 2 ** lvl, ds=True)["L2"])
+        errs_a.append(march_errors(lev, P0, manufactured_baseline(2, P0), 0.0, 0.2, 2 * 2 ** lvl)["L2"])
+    errs, errs_a = np.array(errs), np.array(errs_a)
+    eoc = np.log2(errs[:-1] / errs[1:])
+    assert np.all(eoc[-1][[0, 2]] > 1.7) and np.all(eoc[-1] < 4.0)
+    assert np.all(errs[-1] < 2 * errs_a[-1]) and np.all(errs_a[-1] < 2 * errs[-1])
