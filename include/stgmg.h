@@ -52,6 +52,9 @@ enum { STGMG_TOL_REL = 0 /* ||r|| <= tol ||b|| (BASELINE) */, STGMG_TOL_ABS = 1 
 enum { STGMG_SMOOTH_ADDITIVE = 0 /* Alg. 1 with averaging, P:L488-524 (default) */,
        STGMG_SMOOTH_COLORED_MULT = 1 /* Eq:VankaOP0 with successive overwriting, patches
                                         ordered by vertex colour (v mod 4 per axis); single GPU only */ };
+enum { STGMG_FORM_DSA = 0 /* Problem 3.1 (Eq:DPQ_A0): p-equation couples v (default) */,
+       STGMG_FORM_DS = 1 /* Problem B.1: p-equation couples d_t u through T, slab RHS
+                            adds -chi_b(-1) C U^{n-1} (stgmg_slab_rhs) */ };
 enum { STGMG_LOAD_MANUFACTURED = 0, STGMG_LOAD_BEAM_TRACTION = 1 };   /* stgmg_slab_load */
 enum { STGMG_COMM_NCCL = 0 /* nccl_comm is an ncclComm_t */,
        STGMG_COMM_LOOPBACK = 1 /* nccl_comm is an in-process hub (N emulated ranks on one GPU; tests) */ };
@@ -84,6 +87,7 @@ typedef struct {
   int rank, nranks;                  /* x-slab domain decomposition over nranks GPUs */
   void* stream;                      /* cudaStream_t for all work; NULL = default stream */
   int comm_kind;                     /* STGMG_COMM_NCCL | STGMG_COMM_LOOPBACK */
+  int formulation;                   /* STGMG_FORM_DSA (Problem 3.1, default) | STGMG_FORM_DS (Problem B.1) */
 } stgmg_params;
 
 typedef struct {

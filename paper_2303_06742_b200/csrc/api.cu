@@ -180,6 +180,7 @@ static OpConsts make_consts(int d, int r, int k, const stgmg_params& p) {
   for (int b = 0; b <= k; ++b)
     for (int a = 0; a <= k; ++a) c.T[b][a] = w[b] * dlag(t, a, t[b]) + c.chim1[a] * c.chim1[b];
   c.rho = p.rho; c.alpha = p.alpha; c.c0 = p.c0; c.lam = p.lambda; c.mu = p.mu;
+  c.ds = p.formulation == STGMG_FORM_DS ? 1.0 : 0.0;
   c.gamma_a = p.gamma_a < 0 ? 5.0e4 * r * (r + 1) : p.gamma_a;
   c.gamma_b = p.gamma_b < 0 ? 0.5 * r * (r - 1) : p.gamma_b;
   for (int i = 0; i < 9; ++i) c.K[i] = 0.0;
@@ -1486,6 +1487,10 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       return STGMG_EINVAL;
     }
   const int nranks = params->nranks > 1 ? params->nranks : 1;
+  if (params->formulation != STGMG_FORM_DSA && params->formulation != STGMG_FORM_DS) {
+    set_error("unknown formulation");
+    return STGMG_EINVAL;
+  }
   if (params->smoother != STGMG_SMOOTH_ADDITIVE && params->smoother != STGMG_SMOOTH_COLORED_MULT) {
     set_error("unknown smoother");
     return STGMG_EINVAL;

@@ -267,17 +267,38 @@ __global__ void __launch_bounds__(OP2D_CPB * 4) op2d_cell_kernel(LevelGeom g, co
     for (int j = 0; j < NP; ++j) pn[j] = XP(b, j);
     tp2<NP1, NG, NG>(pn, px, &c.Dp[0][0], &c.Bp[0][0]);
     tp2<NP1, NG, NG>(pn, py, &c.Bp[0][0], &c.Dp[0][0]);
+    // velocity coupled into the p-equation: V_b (DSA, Problem 3.1) or sum_a T_ba U_a (DS, Problem B.1: d_t u)
+    const bool ds = c.ds != 0.0;
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) nod[j] = XQ(b, 0, j);
+    for (int j = 0; j < NQ; ++j) {
+      double s = 0.0;
+      if (ds) {
+#pragma unroll
+        for (int a = 0; a < K1; ++a) s = fma(c.T[b][a], XQ(a, 2, j), s);
+      } else {
+        s = XQ(b, 0, j);
+      }
+      nod[j] = s;
+    }
     tp2<NQ1, NG, NG>(nod, dv, &c.Dm[0][0], &c.B[0][0]);
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) nod[j] = XQ(b, 1, j);
+    for (int j = 0; j < NQ; ++j) {
+      double s = 0.0;
+      if (ds) {
+#pragma unroll
+        for (int a = 0; a < K1; ++a) s = fma(c.T[b][a], XQ(a, 3, j), s);
+      } else {
+        s = XQ(b, 1, j);
+      }
+      nod[j] = s;
+    }
     tp2<NQ1, NG, NG>(nod, tmp, &c.B[0][0], &c.Dm[0][0]);
+    const double cth = ds ? 1.0 : th;   // coefficient of the velocity coupling
 #pragma unroll
     for (int q = 0; q < NGP; ++q) {
       const double w = jac * c.wg[q % NG] * c.wg[q / NG];
       const double div = dv[q] * hx + tmp[q] * hy;
-      pval[q] = (c.c0 * pval[q] + th * c.alpha * div) * w;
+      pval[q] = (c.c0 * pval[q] + cth * c.alpha * div) * w;
       const double gx = px[q] * hx, gy = py[q] * hy;
       const double kx = c.K[0] * gx + c.K[1] * gy, ky = c.K[3] * gx + c.K[4] * gy;
       px[q] = th * kx * w * hx;
@@ -312,13 +333,24 @@ __global__ void __launch_bounds__(OP2D_CPB * 4) op2d_cell_kernel(LevelGeom g, co
       if (fa == 0) tp2<NP1, 1, NF>(pn, fP, Vp, Wp); else tp2<NP1, NF, 1>(pn, fP, Vp, Wp);
 #pragma unroll
       for (int q = 0; q < NF; ++q) psiv[q] = psig0[q] = psig1[q] = 0.0;
-      if (du) {   // -theta alpha <V.n, psi> (Def:C on G_D^u)
+      if (du) {   // -theta alpha <V.n, psi> (Def:C on G_D^u); DS: -alpha <(sum_a T_ba U_a).n, psi>
+        const bool ds = c.ds != 0.0;
         double nod[NQ], Vn[NF];
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) nod[j] = XQ(b, fa, j);
-        if (fa == 0) tp2<NQ1, 1, NF>(nod, Vn, Vq, Wq); else tp2<NQ1, NF, 1>(nod, Vn, Vq, Wq);
+        for (int j = 0; j < NQ; ++j) {
+          double s = 0.0;
+          if (ds) {
 #pragma unroll
-        for (int q = 0; q < NF; ++q) psiv[q] += -c.alpha * Vn[q] * nrm * th * area * c.wg[q];
+            for (int a = 0; a < K1; ++a) s = fma(c.T[b][a], XQ(a, 2 + fa, j), s);
+          } else {
+            s = XQ(b, fa, j);
+          }
+          nod[j] = s;
+        }
+        if (fa == 0) tp2<NQ1, 1, NF>(nod, Vn, Vq, Wq); else tp2<NQ1, NF, 1>(nod, Vn, Vq, Wq);
+        const double cth = ds ? 1.0 : th;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) psiv[q] += -c.alpha * Vn[q] * nrm * cth * area * c.wg[q];
       }
       if (dp) {   // B_gamma Nitsche terms (Def:B, Def:bgam)
         double gx[NF], gy[NF];

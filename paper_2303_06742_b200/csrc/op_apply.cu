@@ -208,7 +208,14 @@ __global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, const OpCons
       Xphi[i] = sphi;
       Xchi[i] = schi;
       Ub[i] = xe[b * T::NE1 + D * T::NQ + i];
-      Vb[i] = xe[b * T::NE1 + i];
+      if (c.ds != 0.0) {   // DS (Problem B.1): the p-equation couples d_t u = sum_a T_ba U_a instead of V_b
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < K1; ++a) s = fma(c.T[b][a], xe[a * T::NE1 + D * T::NQ + i], s);
+        Vb[i] = s;
+      } else {
+        Vb[i] = xe[b * T::NE1 + i];
+      }
     }
     for (int i = lane; i < T::NP; i += 32) {
       double s = 0.0;
@@ -263,7 +270,7 @@ __global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, const OpCons
         q_chi[i * T::NGP + q] *= c.rho * w;
       }
       // psi value coefficient: (c0 Xpsi + theta alpha div V) JxW ; psi gradient: theta K grad P JxW / h_j
-      q_psi[q] = (c.c0 * q_psi[q] + th * c.alpha * divV[q]) * w;
+      q_psi[q] = (c.c0 * q_psi[q] + (c.ds != 0.0 ? 1.0 : th) * c.alpha * divV[q]) * w;
       double gp[3];
       for (int j = 0; j < D; ++j) gp[j] = gP[j * T::NGP + q];
       for (int i = 0; i < D; ++i) {
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, const OpCons
               fgU[(i * D + l) * NF + q] = -th * Gc * w * hinv[l];
             }
           }
-          psi_val += -th * c.alpha * vn * w;
+          psi_val += -(c.ds != 0.0 ? 1.0 : th) * c.alpha * vn * w;
         }
         if (dp) {
           double gpn = 0.0;

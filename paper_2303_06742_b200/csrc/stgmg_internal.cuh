@@ -28,6 +28,7 @@ struct OpConsts {
   double chim1[kMaxK1];        // chi_b(-1)
   double rho, alpha, c0, lam, mu, gamma_a, gamma_b;
   double K[9];                 // row-major d x d (stride 3)
+  double ds;                   // 1: Problem B.1 (DS) — psi rows couple sum_a T_ba U_a instead of theta_b V_b (N4)
 };
 
 // Constants of the on-device load assembly and initial data (csrc/loads.cu).

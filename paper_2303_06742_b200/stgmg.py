@@ -15,6 +15,7 @@ BC_DIRICHLET, BC_NEUMANN = 0, 1
 HF_MEASURE, HF_EDGE = 0, 1
 SMOOTH_ADDITIVE, SMOOTH_COLORED_MULT = 0, 1
 LOAD_MANUFACTURED, LOAD_BEAM_TRACTION = 0, 1
+FORM_DSA, FORM_DS = 0, 1
 
 
 class Mesh(ctypes.Structure):
@@ -32,7 +33,8 @@ class Params(ctypes.Structure):
                 ("tau", ctypes.c_double), ("gamma_a", ctypes.c_double), ("gamma_b", ctypes.c_double),
                 ("hF_mode", ctypes.c_int), ("omega", ctypes.c_double), ("jmax", ctypes.c_int),
                 ("smoother", ctypes.c_int), ("nccl_comm", ctypes.c_void_p), ("rank", ctypes.c_int),
-                ("nranks", ctypes.c_int), ("stream", ctypes.c_void_p), ("comm_kind", ctypes.c_int)]
+                ("nranks", ctypes.c_int), ("stream", ctypes.c_void_p), ("comm_kind", ctypes.c_int),
+                ("formulation", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -184,7 +186,7 @@ class Solver:
     loopback hub with comm_kind=COMM_LOOPBACK); vectors are then the rank's window vectors (stgmg_local_size)."""
 
     def __init__(self, cfg, stream=None, tau=None, omega=0.7, jmax=4, hF_mode=HF_MEASURE, levels=None,
-                 rank=0, nranks=1, comm=None, comm_kind=COMM_NCCL, smoother=0):
+                 rank=0, nranks=1, comm=None, comm_kind=COMM_NCCL, smoother=0, formulation=0):
         import torch
         if not torch.cuda.is_available():
             raise StgmgError("no CUDA device: the stgmg product path has no CPU fallback")
@@ -207,6 +209,7 @@ class Solver:
         p.omega = omega
         p.jmax = jmax
         p.smoother = int(smoother)   # SMOOTH_ADDITIVE (Alg. 1) | SMOOTH_COLORED_MULT
+        p.formulation = int(formulation)   # FORM_DSA (Problem 3.1) | FORM_DS (Problem B.1)
         p.nccl_comm = comm
         p.rank, p.nranks = int(rank), int(nranks)
         p.comm_kind = int(comm_kind)
