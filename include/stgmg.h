@@ -155,6 +155,11 @@ int stgmg_slab_load(stgmg_handle* h, int kind, double t_n, double* load);
  * solution (reading A20; zero for STGMG_LOAD_BEAM_TRACTION), i.e. the X_0 that stgmg_slab_rhs reads for slab 1. */
 int stgmg_initial_state(stgmg_handle* h, int kind, double t0, double* x);
 
+/* SURVEY N1 / P7 (Eq:ExUniDS_3): discrete energy at t_n of the slab solution x (its last Radau block
+ * (V, U, P)): *energy = A_gamma(U, U) + <rho V, V> + <c0 P, P> (host scalar; owned DoFs summed over the ranks).
+ * With zero loads it is non-increasing from slab to slab. */
+int stgmg_energy(stgmg_handle* h, const double* x, double* energy);
+
 /* Slab RHS: rhs = load + J X_prev, where X_prev is the previous slab's full vector (its last
  * Radau block is the state at t_{n-1}) and J puts chi_b(-1) M_rho U, chi_b(-1) M_rho V,
  * chi_b(-1) M_c P into the V, U, P slots of node b.  load: the theta_b-scaled load part (may be NULL). */

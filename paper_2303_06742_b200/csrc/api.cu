@@ -39,6 +39,7 @@ cudaError_t launch_csr_spmv(int nrows, int lpr, const int* rp, const int* ci, co
                             const double* base, double* y, double alpha, double beta, cudaStream_t s);
 cudaError_t launch_avg_table(int d, int N, const int* tab, const double* Y, double omega, int zero_init, double* dvec,
                              cudaStream_t s);
+cudaError_t launch_energy_place(const LevelGeom& g, int k1, const double* x, double* y, int mode, cudaStream_t s);
 cudaError_t launch_extract_elem(const double* Ycb, long long ycstride, int ne, int ntypes, const long long* rep,
                                 const int* mdofs, double* E, int lda, cudaStream_t s);
 cudaError_t launch_op2d_cells(int r, int k1, const LevelGeom& g, const OpConsts* cdev, const double* x, double* Yc,
@@ -372,6 +373,7 @@ struct stgmg_handle {
   OpConsts* c_dev = nullptr;    // operator constants (device copy, read by the 2D cell kernel)
   OpConsts* cj_dev = nullptr;   // slab-RHS variant: T'_ba = chi_b(-1) delta_{a,k}, theta = 0 (K8)
   LoadConsts* lc_dev = nullptr; // on-device load assembly / initial data
+  OpConsts* ce_dev = nullptr;   // discrete energy (N1, P7): [0] T = 0, theta_k = 1 ; [1] T_kk = 1, theta = 0
   double* Yc = nullptr;         // element results of the 2D cell kernel (largest level)
   double* Ycell = nullptr;      // element results of the 3D element GEMM, patch-major (largest level)
   // multi-GPU
@@ -1621,6 +1623,20 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     CK(dalloc(h.get(), &h->cj_dev, 1));
     CKE(cudaMemcpy(h->c_dev, &h->c, sizeof(OpConsts), cudaMemcpyHostToDevice));
     CKE(cudaMemcpy(h->cj_dev, &cj, sizeof(OpConsts), cudaMemcpyHostToDevice));
+    {   // energy constants: ce[0] picks theta_k (A_gamma U in the chi rows), ce[1] picks T_kk (mass rows)
+      OpConsts ce[2] = {h->c, h->c};
+      for (int b = 0; b < kMaxK1; ++b) {
+        ce[0].theta[b] = (b == h->k1 - 1) ? 1.0 : 0.0;
+        ce[1].theta[b] = 0.0;
+        for (int a2 = 0; a2 < kMaxK1; ++a2) {
+          ce[0].T[b][a2] = 0.0;
+          ce[1].T[b][a2] = (a2 == h->k1 - 1 && b == h->k1 - 1) ? 1.0 : 0.0;
+        }
+      }
+      ce[0].ds = ce[1].ds = 0.0;
+      CK(dalloc(h.get(), &h->ce_dev, 2));
+      CKE(cudaMemcpy(h->ce_dev, ce, 2 * sizeof(OpConsts), cudaMemcpyHostToDevice));
+    }
     {   // load-assembly constants: (r+2)-point Gauss rule, bases, GLL nodes, Radau nodes, data
       LoadConsts lc;
       std::memset(&lc, 0, sizeof(lc));
@@ -1826,6 +1842,34 @@ static int dot(stgmg_handle* h, double* w, const double* vprev, const double* hp
       h->launches += 1;
     }
   }
+  return 0;
+}
+
+// Discrete energy at t_n of a slab solution (P7, Eq:ExUniDS_3 P:L300-306):
+//   E = A_gamma(U, U) + <rho V, V> + <c0 P, P>,  (V, U, P) = the last Radau block of x (t_{n,k+1} = t_n).
+// Two operator applies with selector constants on placed copies of that block, two owned-DoF inner products.
+int stgmg_energy(stgmg_handle* h, const double* x, double* energy) {
+  if (!h || !x || !energy) { set_error("bad argument"); return STGMG_EINVAL; }
+  const int Lf = h->L - 1;
+  const LevelGeom& g = h->lev[Lf].g;
+  double *Y = h->w, *O = h->rv, *Zt = h->stage_rhs;
+  h->launches = 0;
+  // A_gamma(U, U): input (0, U, 0) in the last block, T = 0, theta_k = 1 -> chi rows = A_gamma U
+  CKE(launch_energy_place(g, h->k1, x, Y, 0, h->s));
+  CK(exchange(h, Lf, Y));
+  CK(apply_geom(h, g, h->ce_dev, Y, O, nullptr, 1.0, 0.0));
+  CK(dot(h, O, nullptr, nullptr, Y, h->scal + 8, false));
+  // <rho V, V> + <c0 P, P>: input (V, 0, P), T_kk = 1, theta = 0 -> chi rows = M_rho V, psi rows = M_c P; test
+  // vector (0, V, P) aligns V with the chi rows
+  CKE(launch_energy_place(g, h->k1, x, Y, 1, h->s));
+  CK(exchange(h, Lf, Y));
+  CK(apply_geom(h, g, h->ce_dev + 1, Y, O, nullptr, 1.0, 0.0));
+  CKE(launch_energy_place(g, h->k1, x, Zt, 2, h->s));
+  CK(dot(h, O, nullptr, nullptr, Zt, h->scal + 9, false));
+  h->launches += 3;
+  CKE(cudaMemcpyAsync(h->pinned + 8, h->scal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
+  CKE(cudaStreamSynchronize(h->s));
+  *energy = h->pinned[8] + h->pinned[9];
   return 0;
 }
 

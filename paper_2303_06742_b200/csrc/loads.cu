@@ -185,6 +185,29 @@ __global__ void initial_state_kernel(LevelGeom g, const LoadConsts* __restrict__
   x[mu] = val;
 }
 
+// Energy helpers: y = 0 except the last Radau block built from x's last block (V, U, P) as
+//   mode 0: (0, U, 0)   mode 1: (V, 0, P)   mode 2: (0, V, P)
+__global__ void energy_place_kernel(LevelGeom g, int k1, const double* __restrict__ x, double* __restrict__ y, int mode) {
+  const long long mu = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (mu >= g.N) return;
+  pdl_wait();
+  const int m = (int)(mu / g.block);
+  const long long rem = mu - (long long)m * g.block;
+  double v = 0.0;
+  if (m == k1 - 1) {
+    const long long o = (long long)m * g.block;
+    const int slot = rem < g.R ? 0 : (rem < 2 * g.R ? 1 : 2);   // 0 = V, 1 = U, 2 = P
+    if (mode == 0) v = slot == 1 ? x[mu] : 0.0;
+    else if (mode == 1) v = slot == 1 ? 0.0 : x[mu];
+    else v = slot == 1 ? x[o + (rem - g.R)] : (slot == 2 ? x[mu] : 0.0);
+  }
+  y[mu] = v;
+}
+
+cudaError_t launch_energy_place(const LevelGeom& g, int k1, const double* x, double* y, int mode, cudaStream_t s) {
+  return launch_pdl(energy_place_kernel, dim3((unsigned)((g.N + 255) / 256)), dim3(256), 0, s, g, k1, x, y, mode);
+}
+
 cudaError_t launch_load_cells(int d, int r, int k1, const LevelGeom& g, const LoadConsts* lc, int kind, double tn,
                               double tau, double* Yc, cudaStream_t s) {
   const long long ncell = (long long)g.n[0] * g.n[1] * (d == 3 ? g.n[2] : 1);

@@ -66,6 +66,7 @@ SIGNATURES = {
     "stgmg_slab_rhs": (ctypes.c_int, [_P, _P, _P, _P]),
     "stgmg_slab_load": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _P]),
     "stgmg_initial_state": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _P]),
+    "stgmg_energy": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_double)]),
     "stgmg_destroy": (ctypes.c_int, [_P]),
     "stgmg_last_error": (ctypes.c_char_p, []),
     "stgmg_info": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
@@ -301,6 +302,12 @@ class Solver:
     def initial_state(self, kind, t0, x):
         """x = 0 except the last Radau block = interpolated initial data (reading A20)."""
         _check(self.lib.stgmg_initial_state(self.h, int(kind), float(t0), _ptr(x)), "stgmg_initial_state")
+
+    def energy(self, x):
+        """A_gamma(U,U) + <rho V,V> + <c0 P,P> of the last Radau block of x (host float)."""
+        e = ctypes.c_double()
+        _check(self.lib.stgmg_energy(self.h, _ptr(x), ctypes.byref(e)), "stgmg_energy")
+        return e.value
 
     def level_work(self, level=None):
         lev = self.levels - 1 if level is None else level

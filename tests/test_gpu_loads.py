@@ -119,3 +119,31 @@ def test_marching_three_slabs_on_device(pair):
         U, V, P = end_state(lev, Xo)
     torch.cuda.synchronize()
     assert rel(to_np(X), Xo) < 1e-7, rel(to_np(X), Xo)
+
+
+def test_energy_matches_oracle_and_decays(pair):
+    """N1 / P7: the device energy of a slab vector equals U.A U + V.M_rho V + P.M_c P of the oracle's assembled
+    spatial matrices (1e-12), and with zero loads it does not increase from slab to slab (Eq:ExUniDS_3)."""
+    import torch
+    from oracle.loads import end_state
+    cfg, s, H = pair
+    lev, op = H.fine, H.ops[-1]
+    S = op.assemble_spatial()
+    rng = np.random.default_rng(77)
+    X = rng.standard_normal(lev.N)
+    U, V, P = end_state(lev, X)
+    Eo = U @ (S["A"] @ U) + V @ (S["Mrho"] @ V) + P @ (S["Mc"] @ P)
+    Eg = s.energy(to_gpu(X))
+    assert abs(Eg - Eo) <= 1e-12 * abs(Eo), (Eg, Eo)
+    Xg = to_gpu(X)
+    F, Y = torch.zeros_like(Xg), torch.zeros_like(Xg)
+    E_prev = Eg
+    for _ in range(4):
+        s.slab_rhs(None, Xg, F)
+        Y.zero_()
+        st = s.solve(F, Y, tol=1e-12, restart=cfg["restart"])
+        assert st["converged"]
+        E = s.energy(Y)
+        assert E <= E_prev * (1 + 1e-9), (E, E_prev)
+        E_prev = E
+        Xg.copy_(Y)
