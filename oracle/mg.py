@@ -15,14 +15,14 @@ from .vanka import Patches, VankaSmoother, equilibrated_inverse
 
 class Hierarchy:
     def __init__(self, d, cells, lo, hi, r, k, nlevels, params, tau, bc_u=None, bc_p=None,
-                 omega=0.7, jmax=4, share_classes=True, colored=False, ds=False):
+                 omega=0.7, jmax=4, share_classes=True, colored=False, ds=False, cell_patches=False):
         self.levels = hierarchy(d, cells, lo, hi, r, k, nlevels, bc_u, bc_p)
         self.ops = [SlabOperator(lv, params, tau, ds) for lv in self.levels]
         self.A = [op.assemble() for op in self.ops]
         self.P = [None] + [prolongation(self.levels[l - 1], self.levels[l]) for l in range(1, nlevels)]
         self.jmax = jmax
         self.colored = colored   # N2(i): multiplicative colour-ordered smoother instead of Alg. 1
-        self.smoothers = [None] + [VankaSmoother(self.A[l], Patches(self.levels[l]), omega, share_classes)
+        self.smoothers = [None] + [VankaSmoother(self.A[l], Patches(self.levels[l], cell_patches), omega, share_classes)
                                    for l in range(1, nlevels)]
         self.coarse_inv = equilibrated_inverse(self.A[0].toarray())
 

@@ -52,18 +52,37 @@ def equilibrated_inverse(A):
     return inv * s[:, None] * s[None, :]
 
 
-class Patches:
-    """Vertex patches of one level with their DoF index sets Z(P) in local order."""
+def axis_class_cell(c, n):
+    """Per-axis class of a cell for element-wise Vanka (N2(ii)): {0}, {1..n-2}, {n-1} (n >= 3), every cell its own
+    class for n < 3.  A_K = A_l[Z(K), Z(K)] also sums the neighbours' element matrices on K's boundary DoFs, but a
+    Nitsche face term of a boundary neighbour couples only DoFs ON that face, which a cell one away does not own, so
+    one class per side suffices (pinned bitwise up to assembly order in test_oracle_pins.py)."""
+    if n < 3:
+        return c
+    return 0 if c == 0 else (2 if c == n - 1 else 1)
 
-    def __init__(self, lev):
+
+class Patches:
+    """Vertex patches (Eq:DefPlm) of one level with their DoF index sets Z(P) in local order.
+    cells=True: one patch per CELL instead (element-wise Vanka, SURVEY N2(ii), the alternative P:L529-531 rejects);
+    ``verts`` then holds cell + 1 per axis, so that the patch cell range below is the single cell."""
+
+    def __init__(self, lev, cells=False):
         self.lev = lev
         d, r = lev.d, lev.r
-        self.verts = [tuple(reversed(t)) for t in itertools.product(*[range(n + 1) for n in reversed(lev.n)])]
+        self.cells = cells
+        if cells:
+            self.verts = [tuple(c + 1 for c in reversed(t))
+                          for t in itertools.product(*[range(n) for n in reversed(lev.n)])]
+        else:
+            self.verts = [tuple(reversed(t)) for t in itertools.product(*[range(n + 1) for n in reversed(lev.n)])]
         self.dofs = []
         self.keys = []
         for v in self.verts:
             lo_c = [max(v[a] - 1, 0) for a in range(d)]
             hi_c = [min(v[a], lev.n[a] - 1) for a in range(d)]       # inclusive cell range
+            if cells:
+                hi_c = list(lo_c)
             qbox = [np.arange(r * lo_c[a], r * (hi_c[a] + 1) + 1) for a in range(d)]
             pbox = [np.arange((r - 1) * lo_c[a], (r - 1) * (hi_c[a] + 1) + 1) for a in range(d)]
             qn = self._lex(qbox, lev.q_strides)
@@ -76,7 +95,10 @@ class Patches:
                     idx.append(lev.offset(m, FIELD_U, c) + qn)
                 idx.append(lev.offset(m, FIELD_P) + pn)
             self.dofs.append(np.concatenate(idx))
-            self.keys.append(tuple(axis_class(v[a], lev.n[a]) for a in range(d)))
+            if cells:
+                self.keys.append(tuple(axis_class_cell(v[a] - 1, lev.n[a]) for a in range(d)))
+            else:
+                self.keys.append(tuple(axis_class(v[a], lev.n[a]) for a in range(d)))
         self.classes = sorted(set(self.keys))
         self.members = {c: [i for i, kk in enumerate(self.keys) if kk == c] for c in self.classes}
         cnt = np.zeros(lev.N)

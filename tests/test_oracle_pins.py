@@ -528,3 +528,35 @@ def test_N4_ds_eoc_baseline_family():
     eoc = np.log2(errs[:-1] / errs[1:])
     assert np.all(eoc[-1][[0, 2]] > 1.7) and np.all(eoc[-1] < 4.0)
     assert np.all(errs[-1] < 2 * errs_a[-1]) and np.all(errs_a[-1] < 2 * errs[-1])
+
+
+# ---------------------------------------------------------------- N2(ii): element-wise Vanka -------------------
+@pytest.mark.parametrize("dim,cells", [(2, (7, 6)), (3, (4, 3, 5))])
+def test_N2ii_cell_class_sharing(dim, cells):
+    """Element-wise patches Z(K) (one cell): A_K = A_l[Z(K), Z(K)] is the same matrix for all cells of a per-axis
+    class {0}, {1..n-2}, {n-1} (mixed boundary conditions), up to the global assembly's summation order."""
+    d = dim
+    bcu = [0, 1, 0, 0, 1, 0][:2 * d]
+    bcp = [1, 0, 0, 1, 0, 0][:2 * d]
+    lev = Level(d, list(cells), [0] * d, [1] * d, 2, 1, bc_u=bcu, bc_p=bcp)
+    par = dict(P0) if d == 2 else dict(P0, K=[0.01, 0, 0, 0, 0.01, 0, 0, 0, 0.01])
+    A = SlabOperator(lev, par, 0.01).assemble()
+    pa = Patches(lev, cells=True)
+    assert len(pa.verts) == int(np.prod(cells)) and len(pa.classes) == 3 ** d
+    for c in pa.classes:
+        mem = pa.members[c]
+        A0 = pa.extract(A, mem[0])
+        for i in mem[1:]:
+            assert np.abs(pa.extract(A, i) - A0).max() <= 1e-15 * np.abs(A0).max()
+
+
+def test_N2ii_cell_multiplicities_and_fixed_point(cfg0):
+    """p_mu = number of cells containing mu (2D interior Q2: vertex 4, edge 2, cell-interior 1); b = A d is a fixed
+    point of the element-wise sweep."""
+    lev = cfg0.fine
+    A = cfg0.A[-1]
+    sm = VankaSmoother(A, Patches(lev, cells=True))
+    q = lambda i, j: sm.P.p[lev.offset(0, FIELD_U, 0) + i + j * lev.q_shape[0]]
+    assert (q(4, 4), q(5, 4), q(5, 5)) == (4, 2, 1)
+    d = np.random.default_rng(31).standard_normal(lev.N)
+    assert np.abs(sm.sweep(A @ d, d) - d).max() < 1e-12 * np.abs(d).max()
