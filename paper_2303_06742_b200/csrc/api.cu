@@ -549,7 +549,9 @@ static int prolong_level(stgmg_handle* h, int l, const double* dc, double* df) {
 
 static int average_level(stgmg_handle* h, int l, bool zero, double* d) {
   LevelData& L = h->lev[l];
-  if (L.k3tab)
+  if (h->prm.smoother == STGMG_SMOOTH_ELEMENT)
+    CKE(launch_avg_cells(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero ? 1 : 0, d, h->s));
+  else if (L.k3tab)
     CKE(launch_avg_table(h->d, (int)L.g.N, L.k3tab, L.Y, h->prm.omega, zero ? 1 : 0, d, h->s));
   else
     CKE(launch_vanka_average(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero ? 1 : 0, d, h->s));
@@ -736,8 +738,20 @@ static int build_patches(stgmg_handle* h, int l) {
   struct AxCls { int vlo, cnt, vmini, cells; };
   std::vector<AxCls> ax[3];
   int nmini[3] = {1, 1, 1};
+  const bool cellp = h->prm.smoother == STGMG_SMOOTH_ELEMENT;   // element-wise Vanka
   for (int a = 0; a < d; ++a) {
     const int n = g.n[a];
+    if (cellp) {   // one patch per cell, "vertex" = cell + 1; per-axis classes {0}, {1..n-2}, {n-1}
+      nmini[a] = std::min(n, 3);
+      if (n < 3) {
+        for (int c = 0; c < n; ++c) ax[a].push_back({c + 1, 1, c + 1, 1});
+      } else {
+        ax[a].push_back({1, 1, 1, 1});
+        ax[a].push_back({2, n - 2, 2, 1});
+        ax[a].push_back({n, 1, 3, 1});
+      }
+      continue;
+    }
     nmini[a] = std::min(n, 4);
     if (n < 4) {
       for (int v = 0; v <= n; ++v) ax[a].push_back({v, 1, v, (v > 0 ? 1 : 0) + (v < n ? 1 : 0)});
@@ -1411,7 +1425,7 @@ static int build_small(stgmg_handle* h, int l) {
   // transfer CSR and averaging tables: a few int32 per DoF, cheaper than the node-mapped index math up to ~10 x thr
   if (ng <= 10 * thr) {
     CK(build_small_transfer(h, l));
-    CK(build_small_k3(h, l));
+    if (h->prm.smoother == STGMG_SMOOTH_ADDITIVE) CK(build_small_k3(h, l));   // vertex-patch averaging table
   }
   return 0;
 }
@@ -1493,12 +1507,13 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     set_error("unknown formulation");
     return STGMG_EINVAL;
   }
-  if (params->smoother != STGMG_SMOOTH_ADDITIVE && params->smoother != STGMG_SMOOTH_COLORED_MULT) {
+  if (params->smoother != STGMG_SMOOTH_ADDITIVE && params->smoother != STGMG_SMOOTH_COLORED_MULT &&
+      params->smoother != STGMG_SMOOTH_ELEMENT) {
     set_error("unknown smoother");
     return STGMG_EINVAL;
   }
-  if (params->smoother == STGMG_SMOOTH_COLORED_MULT && nranks > 1) {
-    set_error("the multiplicative colour-ordered smoother is single-GPU only");
+  if (params->smoother != STGMG_SMOOTH_ADDITIVE && nranks > 1) {
+    set_error("the smoother variants (colour-ordered multiplicative, element-wise) are single-GPU only");
     return STGMG_ENOTSUP;
   }
   if (nranks > 1 && (params->rank < 0 || params->rank >= nranks || params->nccl_comm == nullptr)) {

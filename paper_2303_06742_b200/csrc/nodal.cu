@@ -220,6 +220,75 @@ __global__ void __launch_bounds__(128) gather_nodal_kernel(LevelGeom g, const do
   }
 }
 
+// ------------------------------------------------------------------------------------------------ K3c -------
+// Averaging update of the element-wise Vanka smoother: patches are the cells, stored like the 3D
+// element results (Y[plin(K + 1)][e(K, mu)]), so d <- d + omega * (sum_{cells K containing mu} y_K) / p_mu with
+// p_mu = number of cells containing mu, cells in lexicographic order (reading A17 form).
+template <int D, int R, int K1>
+__global__ void __launch_bounds__(128) avg_cells_kernel(LevelGeom g, const double* __restrict__ Y, int ldy,
+                                                        double omega, int zero_init, double* __restrict__ dvec) {
+  constexpr int NQE = D == 3 ? (R + 1) * (R + 1) * (R + 1) : (R + 1) * (R + 1);
+  constexpr int NPE = D == 3 ? R * R * R : R * R;
+  constexpr int NE1 = 2 * D * NQE + NPE;
+  constexpr int NC = 1 << D;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nq = (int)g.nq, np = (int)g.np;
+  if (t >= nq + np) return;
+  const bool pres = t >= nq;
+  const int node = pres ? t - nq : t;
+  int idx[3];
+  node_coords<D>(node, pres ? g.pn : g.qn, idx);
+  int nc[3] = {1, 1, 1}, cc[3][2], li[3][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) { cc[a][0] = cc[a][1] = 0; li[a][0] = li[a][1] = 0; }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int i = idx[a];
+    int c1, l1;
+    if (pres) { c1 = i / (R - 1); l1 = i - c1 * (R - 1); } else { c1 = i / R; l1 = i - c1 * R; }
+    const int deg = pres ? R - 1 : R;
+    int k = 0;
+    if (l1 == 0 && c1 > 0) { cc[a][k] = c1 - 1; li[a][k] = deg; ++k; }
+    if (c1 < g.n[a]) { cc[a][k] = c1; li[a][k] = l1; ++k; }
+    nc[a] = k;
+  }
+  const int n1 = pres ? R : R + 1;
+  int off[NC], p = 1;
+#pragma unroll
+  for (int a = 0; a < D; ++a) p *= nc[a];
+#pragma unroll
+  for (int s = 0; s < NC; ++s) {
+    const int j[3] = {s & 1, (s >> 1) & 1, (s >> 2) & 1};
+    bool ok = true;
+    int plin = 0, vs = 1, loc = 0, ls = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      ok = ok && j[a] < nc[a];
+      plin += (cc[a][j[a]] + 1) * vs;
+      vs *= g.n[a] + 1;
+      loc += li[a][j[a]] * ls;
+      ls *= n1;
+    }
+    off[s] = ok ? plin * ldy + loc + (pres ? 2 * D * NQE : 0) : -1;
+  }
+  const double wp = omega / (double)p;
+  const long long blockN = g.block;
+  const long long node_off = pres ? 2 * g.R + node : (long long)node;
+  const int nsl = pres ? 1 : 2 * D;
+  pdl_wait();
+  for (int m = 0; m < K1; ++m)
+    for (int sl = 0; sl < nsl; ++sl) {
+      const int eadd = m * NE1 + sl * NQE;
+      double z = 0.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (off[c] >= 0) z += __ldg(Y + off[c] + eadd);
+      const long long mu = m * blockN + node_off + (pres ? 0 : (long long)sl * g.nq);
+      const double upd = z * wp;
+      dvec[mu] = zero_init ? upd : dvec[mu] + upd;
+    }
+}
+
 // ------------------------------------------------------------------------------------------------ K1e -------
 // Residual in "patch-expanded" form for the dense K2 (large levels): r[mu] = beta * base[mu] + alpha * (sum of the
 // element results of the cells containing mu, lexicographic) exactly as gather_nodal computes it, then stored at
@@ -562,6 +631,14 @@ cudaError_t launch_op_gather(const LevelGeom& g, int r, int k1, const double* Yc
   STGMG_DRK(g.d, r, k1,
             return launch_pdl(gather_nodal_kernel<D_, R_, K_>, dim3(node_blocks(g), (unsigned)batch), dim3(128), 0, s,
                               g, Yc, base, y, alpha, beta, stride, ycstride, ldpm));
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_avg_cells(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega, int zero_init,
+                             double* dvec, cudaStream_t s) {
+  STGMG_DRK(g.d, r, k1,
+            return launch_pdl(avg_cells_kernel<D_, R_, K_>, dim3(node_blocks(g)), dim3(128), 0, s, g, Y, ldy, omega,
+                              zero_init, dvec));
   return cudaErrorNotSupported;
 }
 

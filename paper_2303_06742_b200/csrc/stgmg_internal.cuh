@@ -152,6 +152,9 @@ cudaError_t launch_load_cells(int d, int r, int k1, const LevelGeom& g, const Lo
                               double tau, double* Yc, cudaStream_t s);
 cudaError_t launch_initial_state(int d, int k1, const LevelGeom& g, const LoadConsts* lc, int kind, double t0, double* x,
                                  cudaStream_t s);
+// K3 of the element-wise Vanka smoother: cells as patches, Y[plin(K + 1)][element-local index].
+cudaError_t launch_avg_cells(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega, int zero_init,
+                             double* dvec, cudaStream_t s);
 // K3: d <- (zero ? 0 : d) + omega * (sum_P Y_P[mu_hat]) / p_mu   (pull form, lexicographic patch order).
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
                                  int zero_init, double* dvec, cudaStream_t s);
