@@ -15,13 +15,15 @@ from .vanka import Patches, VankaSmoother, equilibrated_inverse
 
 class Hierarchy:
     def __init__(self, d, cells, lo, hi, r, k, nlevels, params, tau, bc_u=None, bc_p=None,
-                 omega=0.7, jmax=4, share_classes=True, colored=False, ds=False, cell_patches=False):
+                 omega=0.7, jmax=4, share_classes=True, colored=False, ds=False, cell_patches=False,
+                 overwrite=False):
         self.levels = hierarchy(d, cells, lo, hi, r, k, nlevels, bc_u, bc_p)
         self.ops = [SlabOperator(lv, params, tau, ds) for lv in self.levels]
         self.A = [op.assemble() for op in self.ops]
         self.P = [None] + [prolongation(self.levels[l - 1], self.levels[l]) for l in range(1, nlevels)]
         self.jmax = jmax
         self.colored = colored   # N2(i): multiplicative colour-ordered smoother instead of Alg. 1
+        self.overwrite = overwrite   # N2(iii): Alg. 1 without averaging
         self.smoothers = [None] + [VankaSmoother(self.A[l], Patches(self.levels[l], cell_patches), omega, share_classes)
                                    for l in range(1, nlevels)]
         self.coarse_inv = equilibrated_inverse(self.A[0].toarray())
@@ -37,8 +39,8 @@ class Hierarchy:
         if l == 0:
             return self.coarse_inv @ b
         sm = self.smoothers[l]
-        d = sm.smooth(b, None, self.jmax, self.colored)
+        d = sm.smooth(b, None, self.jmax, self.colored, self.overwrite)
         r = b - self.A[l] @ d
         dc = self.vcycle(self.P[l].T @ r, l - 1)
         d = d + self.P[l] @ dc
-        return sm.smooth(b, d, self.jmax, self.colored)
+        return sm.smooth(b, d, self.jmax, self.colored, self.overwrite)

@@ -170,6 +170,31 @@ class VankaSmoother:
         np.add.at(z, self.P.flat_idx, d[self.P.flat_idx] + self.omega * y)
         return z / self.P.p
 
+    # ---------------------------------------------------------------- overwrite variant (N2(iii))
+    def sweep_overwrite(self, b, d):
+        """Alg. 1 without averaging (P:L527-529 names it as what averaging replaces): lines 7-9 become
+        z[dof(P, mu_hat)] = S_P(d)[mu_hat] (overwrite, no counter) and d = z, so every DoF keeps the update of the LAST
+        patch (lexicographic vertex order) that contains it.  Vectorised: the last writer of each DoF."""
+        r = b - self.A @ d
+        y = self.patch_updates(r)
+        last = np.full(len(d), -1, dtype=np.int64)
+        last[self.P.flat_idx] = np.arange(len(self.P.flat_idx))   # numpy keeps the last assignment per index
+        z = d.copy()
+        hit = last >= 0
+        z[hit] = d[hit] + self.omega * y[last[hit]]
+        return z
+
+    def sweep_overwrite_literal(self, b, d):
+        """The same, written as the literal patch loop (pin of ``sweep_overwrite``)."""
+        r = b - self.A @ d
+        z = d.copy()
+        for i in range(len(self.P.dofs)):
+            Z = self.P.dofs[i]
+            yP = self.inv[i] @ r[Z]
+            for j, mu in enumerate(Z):
+                z[mu] = d[mu] + self.omega * yP[j]
+        return z
+
     # ---------------------------------------------------------------- multiplicative variant (N2(i))
     NCOL = 4   # colours per axis: same-colour patches share no cell
 
@@ -202,9 +227,14 @@ class VankaSmoother:
                 d[z] = d[z] + self.omega * (self.inv[i] @ (b - self.A @ d)[z])
         return d
 
-    def smooth(self, b, d=None, steps=4, colored=False):
+    def smooth(self, b, d=None, steps=4, colored=False, overwrite=False):
         """Alg. 1: d initialised with 0 (pre-smoothing) or continued (post-smoothing, reading A13)."""
         d = np.zeros_like(b) if d is None else d.copy()
         for _ in range(steps):
-            d = self.sweep_colored(b, d) if colored else self.sweep(b, d)
+            if colored:
+                d = self.sweep_colored(b, d)
+            elif overwrite:
+                d = self.sweep_overwrite(b, d)
+            else:
+                d = self.sweep(b, d)
         return d

@@ -560,3 +560,16 @@ def test_N2ii_cell_multiplicities_and_fixed_point(cfg0):
     assert (q(4, 4), q(5, 4), q(5, 5)) == (4, 2, 1)
     d = np.random.default_rng(31).standard_normal(lev.N)
     assert np.abs(sm.sweep(A @ d, d) - d).max() < 1e-12 * np.abs(d).max()
+
+
+# ---------------------------------------------------------------- N2(iii): overwrite without averaging ----------
+def test_N2iii_overwrite_equals_literal_loop_and_fixed_point(cfg0):
+    """The vectorised last-writer form equals the literal overwriting patch loop; b = A d stays a fixed point; and it
+    differs from the averaged sweep (DoFs shared by patches take one patch's update, not the mean)."""
+    sm = cfg0.smoothers[1]
+    rng = np.random.default_rng(41)
+    b, d = rng.standard_normal(cfg0.fine.N), rng.standard_normal(cfg0.fine.N)
+    s1, s2 = sm.sweep_overwrite(b, d), sm.sweep_overwrite_literal(b, d)
+    assert np.abs(s1 - s2).max() == 0.0
+    assert np.abs(sm.sweep_overwrite(cfg0.A[1] @ d, d) - d).max() < 1e-12 * np.abs(d).max()
+    assert np.abs(s1 - sm.sweep(b, d)).max() > 1e-3 * np.abs(s1).max()
