@@ -40,9 +40,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of the decomposition")
-    ap.add_argument("--smoother", default="additive", choices=["additive", "colored", "element"],
+    ap.add_argument("--smoother", default="additive", choices=["additive", "colored", "element", "overwrite"],
                     help="additive = Alg. 1 (paper, default); colored = multiplicative colour-ordered Vanka (N2(i)); "
-                         "element = element-wise Vanka (N2(ii))")
+                         "element = element-wise Vanka (N2(ii)); overwrite = Alg. 1 without averaging (N2(iii))")
     return ap.parse_args()
 
 
@@ -194,7 +194,7 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     dd = ws > 1 and not args.replicas
-    smoother = {"additive": 0, "colored": 1, "element": 2}[args.smoother]
+    smoother = {"additive": 0, "colored": 1, "element": 2, "overwrite": 3}[args.smoother]
     comm = None
     t_setup = time.perf_counter()
     if dd:

@@ -53,7 +53,9 @@ enum { STGMG_SMOOTH_ADDITIVE = 0 /* Alg. 1 with averaging, P:L488-524 (default) 
        STGMG_SMOOTH_COLORED_MULT = 1 /* Eq:VankaOP0 with successive overwriting, patches
                                         ordered by vertex colour (v mod 4 per axis); single GPU only */,
        STGMG_SMOOTH_ELEMENT = 2 /* Alg. 1 on one patch per CELL (element-wise Vanka, the variant the
-                                   Remark after alg:smoother P:L529-531 rejects); single GPU only */ };
+                                   Remark after alg:smoother P:L529-531 rejects); single GPU only */,
+       STGMG_SMOOTH_OVERWRITE = 3 /* Alg. 1 without averaging, every DoF keeps the update of the last
+                                     patch (lexicographic) containing it; single GPU only */ };
 enum { STGMG_FORM_DSA = 0 /* Problem 3.1 (Eq:DPQ_A0): p-equation couples v (default) */,
        STGMG_FORM_DS = 1 /* Problem B.1: p-equation couples d_t u through T, slab RHS
                             adds -chi_b(-1) C U^{n-1} (stgmg_slab_rhs) */ };
@@ -84,7 +86,7 @@ typedef struct {
   int hF_mode;                       /* STGMG_HF_MEASURE (default) | STGMG_HF_EDGE */
   double omega;                      /* Vanka under-relaxation, 0.7; <= 0 -> 0.7 */
   int jmax;                          /* smoothing steps per level, 4; <= 0 -> 4 */
-  int smoother;                      /* STGMG_SMOOTH_ADDITIVE (default) | _COLORED_MULT | _ELEMENT */
+  int smoother;                      /* STGMG_SMOOTH_ADDITIVE (default) | _COLORED_MULT | _ELEMENT | _OVERWRITE */
   void* nccl_comm;                   /* multi-GPU: ncclComm_t (STGMG_COMM_NCCL) or loopback hub; NULL if nranks = 1 */
   int rank, nranks;                  /* x-slab domain decomposition over nranks GPUs */
   void* stream;                      /* cudaStream_t for all work; NULL = default stream */

@@ -38,7 +38,7 @@ cudaError_t launch_noop(int blocks, cudaStream_t s);
 cudaError_t launch_csr_spmv(int nrows, int lpr, const int* rp, const int* ci, const double* v, const double* x,
                             const double* base, double* y, double alpha, double beta, cudaStream_t s);
 cudaError_t launch_avg_table(int d, int N, const int* tab, const double* Y, double omega, int zero_init, double* dvec,
-                             cudaStream_t s);
+                             cudaStream_t s, int overwrite = 0);
 cudaError_t launch_energy_place(const LevelGeom& g, int k1, const double* x, double* y, int mode, cudaStream_t s);
 cudaError_t launch_extract_elem(const double* Ycb, long long ycstride, int ne, int ntypes, const long long* rep,
                                 const int* mdofs, double* E, int lda, cudaStream_t s);
@@ -549,12 +549,13 @@ static int prolong_level(stgmg_handle* h, int l, const double* dc, double* df) {
 
 static int average_level(stgmg_handle* h, int l, bool zero, double* d) {
   LevelData& L = h->lev[l];
+  const int ow = h->prm.smoother == STGMG_SMOOTH_OVERWRITE ? 1 : 0;   // N2(iii): no averaging
   if (h->prm.smoother == STGMG_SMOOTH_ELEMENT)
     CKE(launch_avg_cells(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero ? 1 : 0, d, h->s));
   else if (L.k3tab)
-    CKE(launch_avg_table(h->d, (int)L.g.N, L.k3tab, L.Y, h->prm.omega, zero ? 1 : 0, d, h->s));
+    CKE(launch_avg_table(h->d, (int)L.g.N, L.k3tab, L.Y, h->prm.omega, zero ? 1 : 0, d, h->s, ow));
   else
-    CKE(launch_vanka_average(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero ? 1 : 0, d, h->s));
+    CKE(launch_vanka_average(L.g, h->r, h->k1, L.Y, L.ldy, h->prm.omega, zero ? 1 : 0, d, h->s, ow));
   h->launches += 1;
   return 0;
 }
@@ -853,7 +854,8 @@ static int build_patches(stgmg_handle* h, int l) {
   // dense K2 (bulk-copied B from the patch-expanded residual) on the levels of the big / wide tile variants
   // (measured: cfg2 (C_P = 663) / cfg3 (C_P = 1,554) fine K2 34 / 33.5 TF/s, V-cycles 29.4 -> 27 / 63 -> 56 ms;
   // cfg1 (C_P = 218): K2 22.0 -> 17.9 us, the expansion costs about as much, V-cycle 0.809 vs 0.811 ms)
-  Lv.dense = (Lv.k2var == 2 || Lv.k2var == 6) && h->prm.smoother == STGMG_SMOOTH_ADDITIVE;
+  Lv.dense = (Lv.k2var == 2 || Lv.k2var == 6) &&
+             (h->prm.smoother == STGMG_SMOOTH_ADDITIVE || h->prm.smoother == STGMG_SMOOTH_OVERWRITE);
   if (const char* ev = std::getenv("STGMG_K2_DENSE"))   // experiments / tests: 0 = never, 1 = on big / wide levels
     Lv.dense = std::atoi(ev) != 0 && (Lv.k2var == 2 || Lv.k2var == 6) && h->prm.smoother == STGMG_SMOOTH_ADDITIVE;
   {
@@ -1425,7 +1427,8 @@ static int build_small(stgmg_handle* h, int l) {
   // transfer CSR and averaging tables: a few int32 per DoF, cheaper than the node-mapped index math up to ~10 x thr
   if (ng <= 10 * thr) {
     CK(build_small_transfer(h, l));
-    if (h->prm.smoother == STGMG_SMOOTH_ADDITIVE) CK(build_small_k3(h, l));   // vertex-patch averaging table
+    if (h->prm.smoother == STGMG_SMOOTH_ADDITIVE || h->prm.smoother == STGMG_SMOOTH_OVERWRITE)
+      CK(build_small_k3(h, l));   // vertex-patch averaging table
   }
   return 0;
 }
@@ -1508,7 +1511,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     return STGMG_EINVAL;
   }
   if (params->smoother != STGMG_SMOOTH_ADDITIVE && params->smoother != STGMG_SMOOTH_COLORED_MULT &&
-      params->smoother != STGMG_SMOOTH_ELEMENT) {
+      params->smoother != STGMG_SMOOTH_ELEMENT && params->smoother != STGMG_SMOOTH_OVERWRITE) {
     set_error("unknown smoother");
     return STGMG_EINVAL;
   }

@@ -29,7 +29,8 @@ __device__ __forceinline__ void node_coords(int node, const int* nn, int* idx) {
 // ------------------------------------------------------------------------------------------------ K3 --------
 template <int D, int R, int K1>
 __global__ void __launch_bounds__(128) avg_nodal_kernel(LevelGeom g, const double* __restrict__ Y, int ldy,
-                                                        double omega, int zero_init, double* __restrict__ dvec) {
+                                                        double omega, int zero_init, double* __restrict__ dvec,
+                                                        int overwrite) {
   pdl_trigger();
   constexpr int NPMAX = D == 3 ? 27 : 9;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -98,7 +99,8 @@ __global__ void __launch_bounds__(128) avg_nodal_kernel(LevelGeom g, const doubl
 #pragma unroll
   for (int s = 0; s < NPMAX; ++s) Yv[s] = Y + (off[s] >= 0 ? off[s] : 0);   // absent patch: any valid address
   const int nsl = pres ? 1 : 2 * D;
-  const double wp = omega / (double)p;   // omega / p_mu (reading A17: d + omega * (sum_P y_P) / p_mu)
+  // omega / p_mu (reading A17: d + omega * (sum_P y_P) / p_mu); N2(iii) overwrite: the last patch's y, p = 1
+  const double wp = overwrite ? omega : omega / (double)p;
   pdl_wait();
   // loads first (unconditional, so that they issue back to back), then the fixed-order sums
   constexpr int SLB = D == 3 ? 1 : 2 * D;   // slots loaded per batch (register budget)
@@ -122,8 +124,13 @@ __global__ void __launch_bounds__(128) avg_nodal_kernel(LevelGeom g, const doubl
       for (int j = 0; j < SLB; ++j) {
         if (sl0 + j >= nsl) break;
         double z = 0.0;
+        if (overwrite) {
 #pragma unroll
-        for (int s = 0; s < NPMAX; ++s) z += off[s] >= 0 ? v[j][s] : 0.0;
+          for (int s = 0; s < NPMAX; ++s) z = off[s] >= 0 ? v[j][s] : z;   // last patch (lexicographic) wins
+        } else {
+#pragma unroll
+          for (int s = 0; s < NPMAX; ++s) z += off[s] >= 0 ? v[j][s] : 0.0;
+        }
         const long long mu = m * blockN + node_off + (pres ? 0 : (long long)(sl0 + j) * g.nq);
         const double upd = z * wp;
         dvec[mu] = zero_init ? upd : dold[j] + upd;
@@ -618,10 +625,10 @@ static inline unsigned node_blocks(const LevelGeom& g) { return (unsigned)((g.nq
   } while (0)
 
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
-                                 int zero_init, double* dvec, cudaStream_t s) {
+                                 int zero_init, double* dvec, cudaStream_t s, int overwrite) {
   STGMG_DRK(g.d, r, k1,
             return launch_pdl(avg_nodal_kernel<D_, R_, K_>, dim3(node_blocks(g)), dim3(128), 0, s, g, Y, ldy, omega,
-                              zero_init, dvec));
+                              zero_init, dvec, overwrite));
   return cudaErrorNotSupported;
 }
 

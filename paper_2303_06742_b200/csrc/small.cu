@@ -49,7 +49,8 @@ cudaError_t launch_csr_spmv(int nrows, int lpr, const int* rp, const int* ci, co
 // tab[s * N + mu] = offset of y_P[mu_hat] in Y for the s-th patch containing mu (lexicographic), -1 past the last
 template <int NS>
 __global__ void __launch_bounds__(128) avg_table_kernel(int N, const int* __restrict__ tab, const double* __restrict__ Y,
-                                                        double omega, int zero_init, double* __restrict__ dvec) {
+                                                        double omega, int zero_init, double* __restrict__ dvec,
+                                                        int overwrite) {
   const int mu = blockIdx.x * blockDim.x + threadIdx.x;
   if (mu >= N) return;
   int off[NS];
@@ -64,18 +65,20 @@ __global__ void __launch_bounds__(128) avg_table_kernel(int N, const int* __rest
   int p = 0;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-    z += off[s] >= 0 ? v[s] : 0.0;
+    if (overwrite) z = off[s] >= 0 ? v[s] : z;   // N2(iii): the last patch's update
+    else z += off[s] >= 0 ? v[s] : 0.0;
     p += off[s] >= 0 ? 1 : 0;
   }
-  const double upd = z * (omega / (double)p);
+  const double upd = z * (overwrite ? omega : omega / (double)p);
   dvec[mu] = zero_init ? upd : dold + upd;
 }
 
 cudaError_t launch_avg_table(int d, int N, const int* tab, const double* Y, double omega, int zero_init, double* dvec,
-                             cudaStream_t s) {
+                             cudaStream_t s, int overwrite) {
   const unsigned grid = (unsigned)((N + 127) / 128);
-  if (d == 3) return launch_pdl(avg_table_kernel<27>, dim3(grid), dim3(128), 0, s, N, tab, Y, omega, zero_init, dvec);
-  return launch_pdl(avg_table_kernel<9>, dim3(grid), dim3(128), 0, s, N, tab, Y, omega, zero_init, dvec);
+  if (d == 3)
+    return launch_pdl(avg_table_kernel<27>, dim3(grid), dim3(128), 0, s, N, tab, Y, omega, zero_init, dvec, overwrite);
+  return launch_pdl(avg_table_kernel<9>, dim3(grid), dim3(128), 0, s, N, tab, Y, omega, zero_init, dvec, overwrite);
 }
 
 }  // namespace stgmg

@@ -157,7 +157,7 @@ cudaError_t launch_avg_cells(const LevelGeom& g, int r, int k1, const double* Y,
                              double* dvec, cudaStream_t s);
 // K3: d <- (zero ? 0 : d) + omega * (sum_P Y_P[mu_hat]) / p_mu   (pull form, lexicographic patch order).
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
-                                 int zero_init, double* dvec, cudaStream_t s);
+                                 int zero_init, double* dvec, cudaStream_t s, int overwrite = 0);
 // K4 (setup): gather A_P of each class from the dense mini-level matrix; equilibrated Gauss–Jordan inverse.
 cudaError_t launch_extract_patch(const LevelGeom& mini, int r, int k1, const double* Adense, long long ldA,
                                  const int* vrep, int nclass, const int* cps, const long long* rel_offs,

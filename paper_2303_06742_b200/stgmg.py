@@ -13,7 +13,7 @@ STGMG_OK, STGMG_NOT_CONVERGED = 0, 1
 TOL_REL, TOL_ABS = 0, 1
 BC_DIRICHLET, BC_NEUMANN = 0, 1
 HF_MEASURE, HF_EDGE = 0, 1
-SMOOTH_ADDITIVE, SMOOTH_COLORED_MULT, SMOOTH_ELEMENT = 0, 1, 2
+SMOOTH_ADDITIVE, SMOOTH_COLORED_MULT, SMOOTH_ELEMENT, SMOOTH_OVERWRITE = 0, 1, 2, 3
 LOAD_MANUFACTURED, LOAD_BEAM_TRACTION = 0, 1
 FORM_DSA, FORM_DS = 0, 1
 
