@@ -281,6 +281,13 @@ def run_ours(args):
 
     # roofline of the dominant kernel: K2 patch GEMM on the fine level (FP64 DMMA), timed alone
     work = s.level_work()
+    # whole-solve FP64 tensor work: 2 J_max patch-solve sweeps per smoothed level per V-cycle (one V-cycle per GMRES
+    # iteration), the dominant flops of the solve (95-99 %)
+    vc_flops = sum(2 * 4 * s.level_work(l)["k2_flops"] for l in range(1, cfg["levels"]))   # this rank's
+    job_flops = torch.tensor([vc_flops * its], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(job_flops, op=torch.distributed.ReduceOp.SUM)
+    solve_tflops = float(job_flops.item()) / t_max_s / 1e12
     k2_ms = s.time_kernel(0, reps=50)
     k2_achieved = work["k2_flops"] / (k2_ms * 1e-3) / 1e12
     vc_ms = s.time_kernel(3, reps=20)
@@ -343,6 +350,10 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": work["k2_bytes"],
                          "peak_source": "FP64 DMMA m8n8k4 microbenchmark on this pool (profiles/fp64_peak_r01.json); "
                                         "MEASURED_PEAKS.json has no fp64 entry"},
+            "solve_fp64": {"flops_per_vcycle": vc_flops, "achieved_tflops": solve_tflops,
+                           "frac_of_dmma_peak": solve_tflops / (FP64_PEAK_TFLOPS * ws),
+                           "note": "patch-solve (K2) flops of the whole slab solves / timed solve time; K1/K3/K5/K7 "
+                                   "flops (<5 %) not counted"},
             "clocks": clk,
             "e2e": {"value": e2e_val, "unit": "MDoF*iter/s", "h2d_bytes_per_step": 16 * N * ws,
                     "d2h_bytes_per_step": 8 * N * ws},
