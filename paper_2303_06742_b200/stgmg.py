@@ -144,6 +144,33 @@ def make_mesh(cfg):
     return m
 
 
+def setup_args(cfg, tau=None, omega=0.7, jmax=4, hF_mode=HF_MEASURE, rank=0, nranks=1, comm=None,
+               comm_kind=COMM_NCCL, smoother=0, formulation=0):
+    """(stgmg_mesh, stgmg_order, stgmg_params) of a configuration dict (stream left NULL)."""
+    m = make_mesh(cfg)
+    o = Order(int(cfg["r"]), int(cfg["k"]))
+    p = Params()
+    pr = cfg["params"]
+    p.rho, p.alpha, p.c0, p.lambda_, p.mu = pr["rho"], pr["alpha"], pr["c0"], pr["lam"], pr["mu"]
+    K = list(pr["K"])
+    if len(K) == 4:
+        K = [K[0], K[1], 0, K[2], K[3], 0, 0, 0, 0]
+    for i in range(9):
+        p.K[i] = float(K[i])
+    p.tau = float(tau if tau is not None else cfg["tau"])
+    p.gamma_a = float(pr.get("gamma_a", -1.0) or -1.0)
+    p.gamma_b = float(pr.get("gamma_b", -1.0) or -1.0)
+    p.hF_mode = hF_mode
+    p.omega = omega
+    p.jmax = jmax
+    p.smoother = int(smoother)         # SMOOTH_ADDITIVE (Alg. 1) | _COLORED_MULT | _ELEMENT | _OVERWRITE (N2)
+    p.formulation = int(formulation)   # FORM_DSA (Problem 3.1) | FORM_DS (Problem B.1, SURVEY N4)
+    p.nccl_comm = comm
+    p.rank, p.nranks = int(rank), int(nranks)
+    p.comm_kind = int(comm_kind)
+    return m, o, p
+
+
 def partition_plan(cfg, level, rank, nranks):
     """Host-only partition of a level (no GPU): dict(split, gnx, w0, c0, c1, nx_window)."""
     lib = load_library()
@@ -193,27 +220,7 @@ class Solver:
             raise StgmgError("no CUDA device: the stgmg product path has no CPU fallback")
         self.lib = load_library()
         self.cfg = cfg
-        m = make_mesh(cfg)
-        o = Order(int(cfg["r"]), int(cfg["k"]))
-        p = Params()
-        pr = cfg["params"]
-        p.rho, p.alpha, p.c0, p.lambda_, p.mu = pr["rho"], pr["alpha"], pr["c0"], pr["lam"], pr["mu"]
-        K = list(pr["K"])
-        if len(K) == 4:
-            K = [K[0], K[1], 0, K[2], K[3], 0, 0, 0, 0]
-        for i in range(9):
-            p.K[i] = float(K[i])
-        p.tau = float(tau if tau is not None else cfg["tau"])
-        p.gamma_a = float(pr.get("gamma_a", -1.0) or -1.0)
-        p.gamma_b = float(pr.get("gamma_b", -1.0) or -1.0)
-        p.hF_mode = hF_mode
-        p.omega = omega
-        p.jmax = jmax
-        p.smoother = int(smoother)   # SMOOTH_ADDITIVE (Alg. 1) | SMOOTH_COLORED_MULT
-        p.formulation = int(formulation)   # FORM_DSA (Problem 3.1) | FORM_DS (Problem B.1)
-        p.nccl_comm = comm
-        p.rank, p.nranks = int(rank), int(nranks)
-        p.comm_kind = int(comm_kind)
+        m, o, p = setup_args(cfg, tau, omega, jmax, hF_mode, rank, nranks, comm, comm_kind, smoother, formulation)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         p.stream = ctypes.c_void_p(self.stream.cuda_stream)
         self.levels = int(levels or cfg["levels"])

@@ -53,3 +53,53 @@ def test_solver_requires_gpu_no_fallback():
     except StgmgError:
         return
     raise AssertionError("Solver constructed without a GPU")
+
+
+def _setup_rc(mutate, levels=None):
+    """stgmg_setup on a mutated config-0 argument set: (return code, last error).  Argument validation happens
+    before any CUDA call, so invalid input is rejected on a machine without a GPU (include/stgmg.h: EINVAL)."""
+    from paper_2303_06742_b200.stgmg import load_library, setup_args
+    from stgmg_inputs import config
+    lib = load_library()
+    cfg = config(0)
+    m, o, p = setup_args(cfg)
+    lv = cfg["levels"] if levels is None else levels
+    mutate(m, o, p)
+    h = ctypes.c_void_p()
+    rc = lib.stgmg_setup(ctypes.byref(m), lv, ctypes.byref(o), ctypes.byref(p), ctypes.byref(h))
+    return rc, lib.stgmg_last_error().decode()
+
+
+def _set(obj, **kw):
+    for k, v in kw.items():
+        setattr(obj, k, v)
+
+
+import pytest  # noqa: E402
+
+INVALID = {
+    "r<2 (P:L148 Taylor-Hood needs r>=2)": lambda m, o, p: _set(o, r=1),
+    "k<0": lambda m, o, p: _set(o, k=-1),
+    "cells not divisible by 2^(levels-1)": lambda m, o, p: m.cells.__setitem__(0, 5),
+    "rho<=0 (P:L52)": lambda m, o, p: _set(p, rho=0.0),
+    "c0<=0 (P:L52)": lambda m, o, p: _set(p, c0=-1.0),
+    "tau<=0": lambda m, o, p: _set(p, tau=0.0),
+    "K not symmetric (Eq:PosDefK)": lambda m, o, p: p.K.__setitem__(1, 0.5),
+    "K not positive definite (Eq:PosDefK)": lambda m, o, p: p.K.__setitem__(4, -1.0),
+    "dim 4": lambda m, o, p: _set(m, dim=4),
+    "unknown smoother": lambda m, o, p: _set(p, smoother=9),
+    "unknown formulation": lambda m, o, p: _set(p, formulation=7),
+    "multi-rank without communicator": lambda m, o, p: _set(p, nranks=2, rank=0, nccl_comm=None),
+}
+
+
+@pytest.mark.parametrize("case", sorted(INVALID))
+def test_setup_rejects_invalid_arguments(case):
+    rc, msg = _setup_rc(INVALID[case])
+    assert rc == -1, (case, rc, msg)      # STGMG_EINVAL
+    assert msg
+
+
+def test_setup_rejects_bad_level_count():
+    assert _setup_rc(lambda m, o, p: None, levels=0)[0] == -1
+    assert _setup_rc(lambda m, o, p: None, levels=17)[0] == -1
