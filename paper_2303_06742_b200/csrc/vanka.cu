@@ -547,7 +547,7 @@ int k2d_slots(int variant) {
 // w, w + nw, ..; every lane loads its m8n8k4 A fragments straight from the chunk-major inverse (L2) and its B
 // fragment element from r (through the class gather table), so the critical path is two dependent loads plus the
 // DMMAs of one or two chunks.  The nw partial products are added in warp order (fixed) through shared memory.
-template <int MT>
+template <int MT, int NT>
 __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r, const PatchClass* __restrict__ cls,
                                                              const TileDesc* __restrict__ tiles,
                                                              const int* __restrict__ relidx,
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r,
                                                              const double* __restrict__ rvec, double* __restrict__ Y,
                                                              int ldy) {
   pdl_trigger();
-  extern __shared__ double lred[];   // [nw][MT][2][32]
+  extern __shared__ double lred[];   // [nw][MT][NT][2][32]
   const TileDesc td = tiles[blockIdx.x];
   const PatchClass pc = cls[td.cls];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -574,47 +574,64 @@ __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r,
       vs *= (g.n[a] + 1);
     }
   };
-  const int nl = lane >> 2;                        // this lane's B column (m8n8k4 .col fragment: k = lane & 3)
-  const bool cvalid = nl < td.nn && td.n0 + nl < pc.ncols;
-  int bq = 0, bp = 0, pl = 0;
-  if (cvalid) col_base(td.n0 + nl, bq, bp, pl);
+  // this lane's B columns j*8 + lane/4 (m8n8k4 .col fragment: k = lane & 3)
+  bool cvalid[NT];
+  int bq[NT], bp[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int nl = j * 8 + (lane >> 2);
+    cvalid[j] = nl < td.nn && td.n0 + nl < pc.ncols;
+    int pl = 0;
+    bq[j] = bp[j] = 0;
+    if (cvalid[j]) col_base(td.n0 + nl, bq[j], bp[j], pl);
+  }
   const int swz = ((lane >> 2) & 3) << 2;
   const double* Ab = invc + pc.inv_off + (long long)(td.m0 + (lane >> 2)) * K2_BK;
   const int* rel = relidx + pc.rel_off;
-  double acc[MT][2];
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   pdl_wait();
   for (int ch = warp; ch < nch; ch += nw) {
-    double a[4][MT], b[4];
+    double a[4][MT], b[4][NT];
     int code[4];
     const double* Ac = Ab + (long long)ch * lda * K2_BK;
 #pragma unroll
     for (int st = 0; st < 4; ++st) {
       const int k = ch * K2_BK + st * 4 + (lane & 3);
-      code[st] = (cvalid && k < cp) ? __ldg(rel + k) : -1;
+      code[st] = k < cp ? __ldg(rel + k) : -1;
 #pragma unroll
       for (int i = 0; i < MT; ++i) a[st][i] = __ldg(Ac + i * 8 * K2_BK + ((st * 4 + (lane & 3)) ^ swz));
     }
 #pragma unroll
     for (int st = 0; st < 4; ++st)
-      b[st] = code[st] >= 0 ? __ldg(rvec + (code[st] >> 1) + ((code[st] & 1) ? bp : bq)) : 0.0;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        b[st][j] = (cvalid[j] && code[st] >= 0)
+                       ? __ldg(rvec + (code[st] >> 1) + ((code[st] & 1) ? bp[j] : bq[j]))
+                       : 0.0;
 #pragma unroll
     for (int st = 0; st < 4; ++st)
 #pragma unroll
-      for (int i = 0; i < MT; ++i) dmma884(acc[i][0], acc[i][1], a[st][i], b[st]);
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[st][i], b[st][j]);
   }
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) lred[((warp * MT + i) * 2 + e) * 32 + lane] = acc[i][e];
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) lred[(((warp * MT + i) * NT + j) * 2 + e) * 32 + lane] = acc[i][j][e];
   __syncthreads();
-  for (int t = threadIdx.x; t < MT * 2 * 32; t += blockDim.x) {
-    const int ln = t & 31, e = (t >> 5) & 1, i = t >> 6;
+  for (int t = threadIdx.x; t < MT * NT * 2 * 32; t += blockDim.x) {
+    const int ln = t & 31, e = (t >> 5) & 1, j = (t >> 6) % NT, i = (t >> 6) / NT;
     double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += lred[((w * MT + i) * 2 + e) * 32 + ln];
+    for (int w = 0; w < nw; ++w) s += lred[(((w * MT + i) * NT + j) * 2 + e) * 32 + ln];
     const int row = td.m0 + i * 8 + (ln >> 2);
-    const int n = 2 * (ln & 3) + e;
+    const int n = j * 8 + 2 * (ln & 3) + e;
     if (row < cp && n < td.nn && td.n0 + n < pc.ncols) {
       int q, p, plo;
       col_base(td.n0 + n, q, p, plo);
@@ -623,30 +640,39 @@ __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r,
   }
 }
 
-constexpr int K2L_MT = 4;   // 32 x 8 tiles
+constexpr int K2L_MT = 4;   // 32-row tiles
 
-static int k2l_warps(int lda) { return std::max(1, std::min(16, lda / K2_BK)); }
+template <int NT>
+static int k2l_warps(int lda) { return std::max(1, std::min(16 / NT, lda / K2_BK)); }
 
+template <int NT>
+static size_t k2l_smem(int nw) { return sizeof(double) * nw * K2L_MT * NT * 2 * 32; }
+
+template <int NT>
 static cudaError_t launch_k2l(const LevelGeom& g, int r, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
                               const int* relidx, const double* invc, int lda, const double* rvec, double* Y, int ldy,
                               cudaStream_t s) {
-  const int nw = k2l_warps(lda);
-  const size_t smem = sizeof(double) * nw * K2L_MT * 2 * 32;
-  return launch_pdl(patch_gemm_lat_kernel<K2L_MT>, dim3(ntiles), dim3(32 * nw), smem, s, g, r, cls_dev, tiles, relidx,
-                    invc, lda, rvec, Y, ldy);
+  const int nw = k2l_warps<NT>(lda);
+  return launch_pdl(patch_gemm_lat_kernel<K2L_MT, NT>, dim3(ntiles), dim3(32 * nw), k2l_smem<NT>(nw), s, g, r,
+                    cls_dev, tiles, relidx, invc, lda, rvec, Y, ldy);
 }
 
-// resident CTA slots of the whole GPU for a variant launched with clusters of cn CTAs
-int k2_slots(int variant, int cn) {
-  if (variant == 4) {
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_lat_kernel<K2L_MT>, 512,
-                                                      sizeof(double) * 16 * K2L_MT * 2 * 32) != cudaSuccess || nb <= 0) {
-      cudaGetLastError();
-      nb = 1;
-    }
-    return nb * 148;
+template <int NT>
+static int k2l_slots() {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_lat_kernel<K2L_MT, NT>, 32 * (16 / NT),
+                                                    k2l_smem<NT>(16 / NT)) != cudaSuccess || nb <= 0) {
+    cudaGetLastError();
+    nb = 1;
   }
+  return nb * 148;
+}
+
+// resident CTA slots of the whole GPU for a tile variant
+int k2_slots(int variant, int cn) {
+  if (variant == 4) return k2l_slots<1>();
+  if (variant == 7) return k2l_slots<2>();
+  if (variant == 8) return k2l_slots<4>();
   if (variant == 5) return k2_occ<K2_BIGK1>(cn);
   if (variant == 6) return k2_occ<K2_WIDE>(cn);
   if (variant == 3) return k2_occ<K2_TALL>(cn);
@@ -661,6 +687,8 @@ void k2_tile_shape(int variant, int* bm, int* bn) {
   using M = K2Cfg<K2_MED>;
   using Sm = K2Cfg<K2_SMALL>;
   if (variant == 4) { *bm = 8 * K2L_MT; *bn = 8; }
+  else if (variant == 7) { *bm = 8 * K2L_MT; *bn = 16; }
+  else if (variant == 8) { *bm = 8 * K2L_MT; *bn = 32; }
   else if (variant == 5) { *bm = K2Cfg<K2_BIGK1>::BM; *bn = K2Cfg<K2_BIGK1>::BN; }
   else if (variant == 6) { *bm = K2Cfg<K2_WIDE>::BM; *bn = K2Cfg<K2_WIDE>::BN; }
   else if (variant == 3) { *bm = T::BM; *bn = T::BN; }
@@ -675,6 +703,8 @@ int k2_pick_variant(long long npatch, int maxcp) {
   if (const char* ev = std::getenv("STGMG_K2L_MAX")) { if (npatch < std::atoll(ev)) return 4; }
   else if (npatch < 200 && maxcp <= 700) return 4;   // latency variant on the smallest 2D levels (25 / 81 patches);
                                                      // 3D coarse levels stream ~1 GB of inverses: pipelined is faster
+  if (npatch < 2000 && maxcp <= 256) return 7;   // K2L 32 x 16 (cfg1 level 4: 16.4 -> 14.3 us, level 3: 8.0 -> 7.4 us;
+                                                  // slower on cfg2's C_P = 663)
   if (npatch >= 20000) return 6;      // wide 112 x 64 (cfg2 fine 25.6 -> 27.6 TF/s, cfg3 fine 27.1 -> 27.3)
   if (npatch >= 2000) return 2;
   if (npatch >= 1000) return maxcp > 256 ? 2 : 1;   // cfg2 level 4 (C_P 663): big 56 us vs medium 90 us
@@ -684,7 +714,9 @@ int k2_pick_variant(long long npatch, int maxcp) {
 cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
                               int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
                               double* Y, int ldy, int cn, cudaStream_t s) {
-  if (variant == 4) return launch_k2l(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
+  if (variant == 4) return launch_k2l<1>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
+  if (variant == 7) return launch_k2l<2>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
+  if (variant == 8) return launch_k2l<4>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
   if (variant == 5) return launch_k2<K2_BIGK1>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
   if (variant == 6) return launch_k2<K2_WIDE>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
   if (variant == 3) return launch_k2<K2_TALL>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
