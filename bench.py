@@ -197,12 +197,30 @@ def run_ours(args):
     smoother = {"additive": 0, "colored": 1, "element": 2, "overwrite": 3}[args.smoother]
     comm = None
     t_setup = time.perf_counter()
+    dd_error = None
     if dd:
         # the library's own NCCL communicator: rank 0 draws the id, torch.distributed broadcasts it (stgmg.h)
-        uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
-        torch.distributed.broadcast(uid, 0)
-        comm = nccl_comm_create(bytes(uid.cpu().tolist()), ws, rank)
-        s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm, smoother=smoother)
+        try:
+            uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
+            torch.distributed.broadcast(uid, 0)
+            comm = nccl_comm_create(bytes(uid.cpu().tolist()), ws, rank)
+            s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm, smoother=smoother)
+        except Exception as e:   # every rank fails the same way: report it and run replicas instead
+            dd_error = "%s: %s" % (type(e).__name__, e)
+            ok = torch.tensor([0.0], device=dev)
+        else:
+            ok = torch.tensor([1.0], device=dev)
+        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+        if ok.item() < 1.0:
+            if dd_error is None:
+                s.close()
+                dd_error = "another rank failed to set up the decomposition"
+            if comm is not None:
+                nccl_comm_destroy(comm)
+                comm = None
+            dd = False
+            print("bench: x-slab decomposition unavailable (%s); running %d replicas" % (dd_error, ws), file=sys.stderr)
+            s = Solver(cfg, stream=stream, smoother=smoother)
     else:
         s = Solver(cfg, stream=stream, smoother=smoother)
     t_setup = time.perf_counter() - t_setup
@@ -338,7 +356,9 @@ def run_ours(args):
                        "gmres_iterations_total": its, "final_rel_residual_max": max(resid),
                        "l2": "flushed between timed steps (256 MB write, untimed)",
                        "parallelism": ("x-slab decomposition over %d GPUs (NCCL halo exchange)" % ws) if dd else
-                                      ("%d replicas" % ws if ws > 1 else "single GPU"), "setup_s": t_setup,
+                                      (("%d replicas" % ws + (" (decomposition unavailable: %s)" % dd_error
+                                                              if dd_error else "")) if ws > 1 else "single GPU"),
+                       "setup_s": t_setup,
                        "s_per_slab": t_max_s / args.steps,
                        "vcycle_ms": vc_ms, "k1_fine_apply_ms": k1_ms,
                        "k1_fine_hbm_gbs": work["k1_bytes"] / (k1_ms * 1e-3) / 1e9},
