@@ -164,6 +164,34 @@ def traction_face_vector(lev, face, comp, amplitude=1.0):
     return F
 
 
+def goal_quantities(lev, X, face):
+    """Goal quantities of Eq:DefGQ on a whole box face at t_n (last Radau block of X):
+    b_u = int_face u . n do, b_p = int_face p do, with the (r+2)^{d-1} Gauss rule on the face cells."""
+    d, r = lev.d, lev.r
+    a, s = face // 2, face % 2
+    U, V, P = end_state(lev, X)
+    nrm = 1.0 if s == 1 else -1.0
+    Fu = traction_face_vector(lev, face, a, 1.0)            # int_face chi_a for every Q_r basis function
+    bu = nrm * (Fu @ U)
+    # pressure: int_face xi_s over the Q_{r-1} basis
+    xg, wg = gauss_legendre01(r + 2)
+    pts = [xg] * d
+    pts[a] = np.array([float(s)])
+    wts = [wg] * d
+    wts[a] = np.array([1.0])
+    php, _ = _tensor_eval(d, gauss_lobatto_nodes01(r - 1), pts, lev.h)
+    w = _tensor_weights(wts, float(np.prod(lev.h)) / lev.h[a])
+    loc = php @ w
+    D, cells = all_cell_dofs(lev)
+    sel = cells[:, a] == (0 if s == 0 else lev.n[a] - 1)
+    nql, npl = (r + 1) ** d, r ** d
+    pn = D[sel][:, 2 * d * nql: 2 * d * nql + npl] - lev.offset(0, FIELD_P)
+    Fp = np.zeros(lev.S)
+    np.add.at(Fp, pn, loc[None, :])
+    bp = Fp @ P
+    return bu, bp
+
+
 def slab_rhs(lev, spatial, chi_m1, th, U_prev, V_prev, P_prev, Floads, Gloads, ds=False):
     """Assemble F_n in ABI layout.  Floads[b], Gloads[b]: spatial loads at t_{n,b} (None = 0).
     ds=True (Problem B.1): the jump term of the pressure equation adds -chi_b(-1) C U^{n-1} to the

@@ -573,3 +573,25 @@ def test_N2iii_overwrite_equals_literal_loop_and_fixed_point(cfg0):
     assert np.abs(s1 - s2).max() == 0.0
     assert np.abs(sm.sweep_overwrite(cfg0.A[1] @ d, d) - d).max() < 1e-12 * np.abs(d).max()
     assert np.abs(s1 - sm.sweep(b, d)).max() > 1e-3 * np.abs(s1).max()
+
+
+# ---------------------------------------------------------------- N1: goal quantities (Eq:DefGQ) ---------------
+def test_N1_goal_quantities_exact_for_fe_functions():
+    """b_u = int_face u.n, b_p = int_face p on box faces are exact for interpolants of polynomials in the FE spaces:
+    u = (1 + x + 2y, 3 - y), p = 2 + x y on [0,2] x [0,1] (closed-form face integrals)."""
+    from oracle.loads import goal_quantities
+    lev = Level(2, [4, 3], [0, 0], [2, 1], 2, 1)
+    xq = lev.node_coords(2, gauss_lobatto_nodes01(2))
+    xp = lev.node_coords(1, gauss_lobatto_nodes01(1))
+    X = np.zeros(lev.N)
+    o = lev.k * lev.block
+    X[o + lev.R: o + lev.R + lev.nq] = 1 + xq[:, 0] + 2 * xq[:, 1]      # U_x
+    X[o + lev.R + lev.nq: o + 2 * lev.R] = 3 - xq[:, 1]                 # U_y
+    X[o + 2 * lev.R: o + lev.block] = 2 + xp[:, 0] * xp[:, 1]           # P
+    want = {0: (-2.0, 2.0),            # x = 0: n = -e_x, int (1 + 2y) dy = 2 ; int 2 dy = 2
+            1: (4.0, 3.0),             # x = 2: int (3 + 2y) dy = 4 ; int (2 + 2y) dy = 3
+            2: (-6.0, 4.0),            # y = 0: n = -e_y, int 3 dx = 6 ; int 2 dx = 4
+            3: (4.0, 6.0)}             # y = 1: int 2 dx = 4 ; int (2 + x) dx = 6
+    for face, (bu, bp) in want.items():
+        gu, gp = goal_quantities(lev, X, face)
+        assert abs(gu - bu) < 1e-12 and abs(gp - bp) < 1e-12, (face, gu, gp)
