@@ -164,6 +164,11 @@ int stgmg_initial_state(stgmg_handle* h, int kind, double t0, double* x);
  * With zero loads it is non-increasing from slab to slab. */
 int stgmg_energy(stgmg_handle* h, const double* x, double* energy);
 
+/* SURVEY N1, goal quantities of Eq:DefGQ on a whole box face (0..2d-1 = x-, x+, y-, y+, z-, z+) at t_n:
+ * *b_u = int_face u . n do and *b_p = int_face p do of the last Radau block of x ((r+2)^{d-1} Gauss points per face
+ * cell; host scalars; owned face cells summed over the ranks).  EINVAL for a face index outside 0..2d-1. */
+int stgmg_goal_quantities(stgmg_handle* h, const double* x, int face, double* b_u, double* b_p);
+
 /* Slab RHS: rhs = load + J X_prev, where X_prev is the previous slab's full vector (its last
  * Radau block is the state at t_{n-1}) and J puts chi_b(-1) M_rho U, chi_b(-1) M_rho V,
  * chi_b(-1) M_c P into the V, U, P slots of node b.  load: the theta_b-scaled load part (may be NULL). */

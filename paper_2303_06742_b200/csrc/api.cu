@@ -40,6 +40,9 @@ cudaError_t launch_csr_spmv(int nrows, int lpr, const int* rp, const int* ci, co
 cudaError_t launch_avg_table(int d, int N, const int* tab, const double* Y, double omega, int zero_init, double* dvec,
                              cudaStream_t s, int overwrite = 0);
 cudaError_t launch_energy_place(const LevelGeom& g, int k1, const double* x, double* y, int mode, cudaStream_t s);
+cudaError_t launch_face_integrals(int d, int r, int k1, const LevelGeom& g, const LoadConsts* lc, const double* x,
+                                  int face, int c0, int c1, double* part, int nface_cells, double* out,
+                                  cudaStream_t s);
 cudaError_t launch_extract_elem(const double* Ycb, long long ycstride, int ne, int ntypes, const long long* rep,
                                 const int* mdofs, double* E, int lda, cudaStream_t s);
 cudaError_t launch_op2d_cells(int r, int k1, const LevelGeom& g, const OpConsts* cdev, const double* x, double* Yc,
@@ -1834,6 +1837,43 @@ int stgmg_initial_state(stgmg_handle* h, int kind, double t0, double* x) {
   CKE(launch_initial_state(h->d, h->k1, g, h->lc_dev, kind, t0, x, h->s));
   h->launches = 1;
   return sync_if_own(h);
+}
+
+// Goal quantities (Eq:DefGQ): b_u = int_face u . n do, b_p = int_face p do at t_n (last Radau
+// block of x) over a whole box face; owned face cells of this rank, summed over the ranks.
+int stgmg_goal_quantities(stgmg_handle* h, const double* x, int face, double* bu, double* bp) {
+  if (!h || !x || !bu || !bp || face < 0 || face >= 2 * h->d) { set_error("bad argument"); return STGMG_EINVAL; }
+  const LevelData& F = h->lev[h->L - 1];
+  const LevelGeom& g = F.g;
+  const int a = face >> 1, side = face & 1;
+  const int gnx = F.gnx ? F.gnx : g.n[0];
+  const int c0 = F.part ? F.c0 : 0, c1 = F.part ? F.c1 : g.n[0];
+  long long ncells = 1;
+  for (int b = 0; b < h->d; ++b)
+    if (b != a) ncells *= (b == 0 ? (c1 - c0) : g.n[b]);
+  if (a == 0) {   // an x face lives on the rank that owns the first / last global cell column
+    const bool here = side ? (F.w0 + c1 == gnx) : (F.w0 + c0 == 0);
+    if (!here) ncells = 0;
+  }
+  h->launches = 0;
+  if (ncells > 0) {
+    cudaError_t e = launch_face_integrals(h->d, h->r, h->k1, g, h->lc_dev, x, face, c0, c1, h->w, (int)ncells,
+                                          h->scal + 10, h->s);
+    if (e == cudaErrorNotSupported) { set_error("(d, r) combination not compiled"); return STGMG_ENOTSUP; }
+    CKE(e);
+    h->launches += 2;
+  } else {
+    CKE(cudaMemsetAsync(h->scal + 10, 0, 2 * sizeof(double), h->s));
+  }
+  if (h->nranks > 1) {
+    const int rc = h->tr->allreduce_sum(h->scal + 10, 2, h->s);
+    if (rc) return rc;
+  }
+  CKE(cudaMemcpyAsync(h->pinned + 10, h->scal + 10, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
+  CKE(cudaStreamSynchronize(h->s));
+  *bu = h->pinned[10];
+  *bp = h->pinned[11];
+  return 0;
 }
 
 int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, double* rhs) {

@@ -208,6 +208,116 @@ cudaError_t launch_energy_place(const LevelGeom& g, int k1, const double* x, dou
   return launch_pdl(energy_place_kernel, dim3((unsigned)((g.N + 255) / 256)), dim3(256), 0, s, g, k1, x, y, mode);
 }
 
+// Goal quantities (Eq:DefGQ): per face cell, the (r+2)^{d-1}-point face integrals of
+// u . n and p of the last Radau block (t_n); partial sums per cell, then one fixed-order reduction (deterministic).
+template <int D, int R>
+__global__ void face_integrals_kernel(LevelGeom g, const LoadConsts* __restrict__ lc, const double* __restrict__ x,
+                                      int k1, int face, int c0, int c1, double* __restrict__ part) {
+  constexpr int NQ1 = R + 2, NF = D == 3 ? NQ1 * NQ1 : NQ1;
+  const int a = face >> 1, side = face & 1;
+  // face cells: the other axes run over all cells (x restricted to the owned range [c0, c1) when a != 0)
+  int n1 = 1, n2 = 1, ax1 = 0, ax2 = 0;
+  {
+    int k = 0;
+    for (int b = 0; b < D; ++b)
+      if (b != a) {
+        if (k == 0) { ax1 = b; n1 = (b == 0 ? c1 - c0 : g.n[b]); } else { ax2 = b; n2 = g.n[b]; }
+        ++k;
+      }
+  }
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n1 * n2) return;
+  pdl_wait();
+  const LoadConsts& c = *lc;
+  int cell[3] = {0, 0, 0};
+  cell[a] = side ? g.n[a] - 1 : 0;
+  cell[ax1] = t % n1 + (ax1 == 0 ? c0 : 0);
+  if (D == 3) cell[ax2] = t / n1;
+  const double nrm = side ? 1.0 : -1.0;
+  const long long o = (long long)(k1 - 1) * g.block;
+  double bu = 0.0, bp = 0.0;
+  for (int q = 0; q < NF; ++q) {
+    const int qa[3] = {q % NQ1, q / NQ1, 0};
+    double w = g.vol / g.h[a];
+    int qq = 0;
+    int qi[3] = {0, 0, 0};   // quadrature index along each in-face axis
+    for (int b = 0; b < D; ++b) {
+      if (b == a) continue;
+      w *= c.wg[qa[qq]];
+      qi[b] = qa[qq++];
+    }
+    double u = 0.0, p = 0.0;
+    // Q_r nodes of the cell
+    for (int j = 0; j < (D == 3 ? (R + 1) * (R + 1) * (R + 1) : (R + 1) * (R + 1)); ++j) {
+      int rem = j;
+      long long node = 0;
+      double phi = 1.0;
+      for (int b = 0; b < D; ++b) {
+        const int jb = rem % (R + 1);
+        rem /= (R + 1);
+        node += (long long)(R * cell[b] + jb) * g.qs[b];
+        phi *= b == a ? c.Eq[side][jb] : c.Bq[qi[b]][jb];
+      }
+      u += phi * x[o + g.R + (long long)a * g.nq + node];
+    }
+    for (int j = 0; j < (D == 3 ? R * R * R : R * R); ++j) {
+      int rem = j;
+      long long node = 0;
+      double phi = 1.0;
+      for (int b = 0; b < D; ++b) {
+        const int jb = rem % R;
+        rem /= R;
+        node += (long long)((R - 1) * cell[b] + jb) * g.ps[b];
+        // Q_{r-1} basis at the face point: endpoint value = Lagrange value at 0 / 1 (GLL nodes include both ends)
+        phi *= b == a ? ((side ? (jb == R - 1) : (jb == 0)) ? 1.0 : 0.0) : c.Bp[qi[b]][jb];
+      }
+      p += phi * x[o + 2 * g.R + node];
+    }
+    bu += w * nrm * u;
+    bp += w * p;
+  }
+  part[2 * t] = bu;
+  part[2 * t + 1] = bp;
+}
+
+// out[0..1] = sum over the n partial pairs, fixed order (one block, strided partial sums + fixed tree)
+__global__ void sum_pairs_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double s0[256], s1[256];
+  pdl_wait();
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+  s0[threadIdx.x] = a;
+  s1[threadIdx.x] = b;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      s0[threadIdx.x] += s0[threadIdx.x + st];
+      s1[threadIdx.x] += s1[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s0[0];
+    out[1] = s1[0];
+  }
+}
+
+cudaError_t launch_face_integrals(int d, int r, int k1, const LevelGeom& g, const LoadConsts* lc, const double* x,
+                                  int face, int c0, int c1, double* part, int nface_cells, double* out,
+                                  cudaStream_t s) {
+  const unsigned grid = (unsigned)((nface_cells + 127) / 128);
+  cudaError_t e = cudaErrorNotSupported;
+  if (d == 2 && r == 2) e = launch_pdl(face_integrals_kernel<2, 2>, dim3(grid), dim3(128), 0, s, g, lc, x, k1, face, c0, c1, part);
+  if (d == 2 && r == 3) e = launch_pdl(face_integrals_kernel<2, 3>, dim3(grid), dim3(128), 0, s, g, lc, x, k1, face, c0, c1, part);
+  if (d == 3 && r == 2) e = launch_pdl(face_integrals_kernel<3, 2>, dim3(grid), dim3(128), 0, s, g, lc, x, k1, face, c0, c1, part);
+  if (d == 3 && r == 3) e = launch_pdl(face_integrals_kernel<3, 3>, dim3(grid), dim3(128), 0, s, g, lc, x, k1, face, c0, c1, part);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(sum_pairs_kernel, dim3(1), dim3(256), 0, s, (const double*)part, nface_cells, out);
+}
+
 cudaError_t launch_load_cells(int d, int r, int k1, const LevelGeom& g, const LoadConsts* lc, int kind, double tn,
                               double tau, double* Yc, cudaStream_t s) {
   const long long ncell = (long long)g.n[0] * g.n[1] * (d == 3 ? g.n[2] : 1);

@@ -67,6 +67,8 @@ SIGNATURES = {
     "stgmg_slab_load": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _P]),
     "stgmg_initial_state": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _P]),
     "stgmg_energy": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_double)]),
+    "stgmg_goal_quantities": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                             ctypes.POINTER(ctypes.c_double)]),
     "stgmg_destroy": (ctypes.c_int, [_P]),
     "stgmg_last_error": (ctypes.c_char_p, []),
     "stgmg_info": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
@@ -315,6 +317,13 @@ class Solver:
         e = ctypes.c_double()
         _check(self.lib.stgmg_energy(self.h, _ptr(x), ctypes.byref(e)), "stgmg_energy")
         return e.value
+
+    def goal_quantities(self, x, face):
+        """SURVEY N1 / Eq:DefGQ: (b_u, b_p) = (int_face u.n, int_face p) of the last Radau block of x."""
+        bu, bp = ctypes.c_double(), ctypes.c_double()
+        _check(self.lib.stgmg_goal_quantities(self.h, _ptr(x), int(face), ctypes.byref(bu), ctypes.byref(bp)),
+               "stgmg_goal_quantities")
+        return bu.value, bp.value
 
     def level_work(self, level=None):
         lev = self.levels - 1 if level is None else level

@@ -147,3 +147,18 @@ def test_energy_matches_oracle_and_decays(pair):
         assert E <= E_prev * (1 + 1e-9), (E, E_prev)
         E_prev = E
         Xg.copy_(Y)
+
+
+def test_goal_quantities_vs_oracle(pair):
+    """N1 / Eq:DefGQ: b_u = int_face u.n and b_p = int_face p of the last Radau block on every box face, device vs
+    the oracle's face quadrature (pinned exact on FE polynomials), 1e-12 relative."""
+    from oracle.loads import goal_quantities
+    cfg, s, H = pair
+    lev = H.fine
+    X = np.random.default_rng(88).standard_normal(lev.N)
+    Xg = to_gpu(X)
+    for face in range(2 * lev.d):
+        gu, gp = s.goal_quantities(Xg, face)
+        ou, op = goal_quantities(lev, X, face)
+        assert abs(gu - ou) <= 1e-12 * max(1.0, abs(ou)), (face, gu, ou)
+        assert abs(gp - op) <= 1e-12 * max(1.0, abs(op)), (face, gp, op)
