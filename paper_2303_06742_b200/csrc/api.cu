@@ -304,7 +304,7 @@ using namespace stgmg;
 struct LevelData {
   LevelGeom g;
   double *b = nullptr, *d = nullptr, *r = nullptr, *Y = nullptr;
-  int ldy = 0, lda = 0, maxcp = 0, ntiles = 0, k2var = 0, cn = 1;
+  int ldy = 0, lda = 0, maxcp = 0, ntiles = 0, k2var = 0;
   long long npatch = 0;
   std::vector<PatchClass> cls;
   PatchClass* cls_dev = nullptr;
@@ -316,7 +316,7 @@ struct LevelData {
   std::vector<PatchClass> ecls;
   PatchClass* ecls_dev = nullptr;
   TileDesc* etiles_dev = nullptr;
-  int entiles = 0, elda = 0, ek2var = 0, ecn = 1;
+  int entiles = 0, elda = 0, ek2var = 0;
   int* erelidx_dev = nullptr;
   double* E_dev = nullptr;
   // x-slab domain decomposition; a replicated level has part = false, w0 = 0, gnx = n[0]
@@ -479,7 +479,7 @@ static int apply_level(stgmg_handle* h, int l, const double* x, double* y, const
   LevelData& Lv = h->lev[l];
   const int ne = (int)elem_dofs(h);
   CKE(launch_patch_gemm(Lv.g, h->r, Lv.ek2var, Lv.ecls_dev, Lv.etiles_dev, Lv.entiles, Lv.erelidx_dev, Lv.E_dev,
-                        Lv.elda, x, h->Ycell, ne, Lv.ecn, h->s));
+                        Lv.elda, x, h->Ycell, ne, h->s));
   CKE(launch_op_gather(Lv.g, h->r, h->k1, h->Ycell, base, y, alpha, beta, 1, 0, 0, h->s, ne));
   h->launches += 2;
   return 0;
@@ -578,7 +578,7 @@ static int sweep_colored(stgmg_handle* h, int l, const double* b, double* d, boo
     }
     first = false;
     CKE(launch_patch_gemm(L.g, h->r, C.k2var, C.cls_dev, C.tiles_dev, C.ntiles, L.relidx_dev, L.inv_dev, L.lda, rin,
-                          L.Y, L.ldy, 1, h->s));
+                          L.Y, L.ldy, h->s));
     CKE(launch_colour_update(L.g, h->r, C.cls_dev, C.items_dev, C.nitems, L.relidx_dev, L.Y, L.ldy, h->prm.omega, d,
                              h->s));
     h->launches += 2;
@@ -601,7 +601,7 @@ static int residual_expand(stgmg_handle* h, int l, const double* b, const double
   } else {
     const int ne = (int)elem_dofs(h);
     CKE(launch_patch_gemm(L.g, h->r, L.ek2var, L.ecls_dev, L.etiles_dev, L.entiles, L.erelidx_dev, L.E_dev, L.elda, d,
-                          h->Ycell, ne, L.ecn, h->s));
+                          h->Ycell, ne, h->s));
     CKE(launch_gather_expand(L.g, h->r, h->k1, h->Ycell, b, -1.0, 1.0, ne, L.cls_dev, L.Rexp, h->s));
   }
   h->launches += 2;
@@ -625,7 +625,7 @@ static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_s
     rin = L.r;
   }
   CKE(launch_patch_gemm(L.g, h->r, L.k2var, L.cls_dev, L.tiles_dev, L.ntiles, L.relidx_dev, L.inv_dev, L.lda, rin, L.Y,
-                        L.ldy, L.cn, h->s));
+                        L.ldy, h->s));
   h->launches += 1;
   CK(average_level(h, l, zero_start, d));
   return exchange(h, l, d);
@@ -723,15 +723,6 @@ std::vector<TileDesc> stgmg::balanced_tiles(const std::vector<int>& cp, const st
                          "avg=%.3g\n",
                  bm, bn, cn, slots, t0, target, out.size(), wmax_tile, out.empty() ? 0.0 : wsum / (double)out.size());
   return out;
-}
-
-// Cluster size of a level's grouped GEMM.  Multicasting A over clusters of 2 / 4 CTAs was measured slower on B200 in
-// every case (cfg1 fine 22 -> 42 us, cfg3 fine 5.6 -> 6.8 ms): K2 is not L2-bandwidth bound and the per-chunk
-// cluster barrier costs more than the A traffic it saves.  Default 1; STGMG_K2_CN=2|4 enables it for experiments.
-static int k2_cluster(long long ncols_total) {
-  (void)ncols_total;
-  if (const char* ev = std::getenv("STGMG_K2_CN")) return std::max(1, std::min(4, std::atoi(ev)));
-  return 1;
 }
 
 static int build_patches(stgmg_handle* h, int l) {
@@ -872,8 +863,7 @@ static int build_patches(stgmg_handle* h, int l) {
   {
     std::vector<int> cpv, ncv;
     for (const auto& c : Lv.cls) { cpv.push_back(c.cp); ncv.push_back(c.ncols); }
-    Lv.cn = k2_cluster(Lv.npatch_global ? Lv.npatch_global : Lv.npatch);
-    tiles = balanced_tiles(cpv, ncv, tbm, tbn, Lv.dense ? k2d_slots(Lv.k2var) : k2_slots(Lv.k2var, Lv.cn), Lv.cn);
+    tiles = balanced_tiles(cpv, ncv, tbm, tbn, Lv.dense ? k2d_slots(Lv.k2var) : k2_slots(Lv.k2var), 1);
   }
   Lv.ntiles = (int)tiles.size();
   if (Lv.dense) {
@@ -919,7 +909,7 @@ static int build_patches(stgmg_handle* h, int l) {
       C.k2var = k2_pick_variant((long long)items.size(), Lv.maxcp);
       int cbm = 0, cbn = 0;
       k2_tile_shape(C.k2var, &cbm, &cbn);
-      std::vector<TileDesc> ct = balanced_tiles(cpv, ncv, cbm, cbn, k2_slots(C.k2var, 1), 1);
+      std::vector<TileDesc> ct = balanced_tiles(cpv, ncv, cbm, cbn, k2_slots(C.k2var), 1);
       C.ntiles = (int)ct.size();
       CK(upload(h, &C.cls_dev, sub));
       CK(upload(h, &C.tiles_dev, ct));
@@ -1064,8 +1054,7 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
     std::vector<TileDesc> tiles;
     std::vector<int> cpv, ncv;
     for (const auto& c : Lv.ecls) { cpv.push_back(c.cp); ncv.push_back(c.ncols); }
-    Lv.ecn = k2_cluster(Lv.ncell_global ? Lv.ncell_global : cell_count(g));
-    tiles = balanced_tiles(cpv, ncv, tbm, tbn, k2_slots(Lv.ek2var, Lv.ecn), Lv.ecn);
+    tiles = balanced_tiles(cpv, ncv, tbm, tbn, k2_slots(Lv.ek2var), 1);
     Lv.entiles = (int)tiles.size();
     CK(upload(h, &Lv.ecls_dev, Lv.ecls));
     CK(upload(h, &Lv.etiles_dev, tiles));
@@ -2057,7 +2046,7 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
                                     Lv.Y, Lv.ldy, h->s));
       else
         CKE(launch_patch_gemm(Lv.g, h->r, Lv.k2var, Lv.cls_dev, Lv.tiles_dev, Lv.ntiles, Lv.relidx_dev, Lv.inv_dev,
-                              Lv.lda, Lv.r, Lv.Y, Lv.ldy, Lv.cn, h->s));
+                              Lv.lda, Lv.r, Lv.Y, Lv.ldy, h->s));
     } else if (kind == 1) {
       CK(apply_level(h, level, Lv.d, Lv.r, nullptr, 1.0, 0.0));
     } else if (kind == 2) {

@@ -124,9 +124,9 @@ cudaError_t launch_op_apply(int d, int r, int k1, const LevelGeom& g, const OpCo
 // K2: Y[patch][mu_hat] = Ainv_class * R_P r for all patches (grouped DMMA GEMM); variant = tile shape.
 int k2_pick_variant(long long npatch, int maxcp);
 void k2_tile_shape(int variant, int* bm, int* bn);
-int k2_slots(int variant, int cn);   // resident CTA slots on the GPU for a variant launched in clusters of cn
+int k2_slots(int variant);   // resident CTA slots on the GPU for a tile variant
 // Tiles of a grouped GEMM balanced over the resident CTA slots: cp[c] x ncols[c] per class, BM x (<= BN) tiles;
-// consecutive groups of cn tiles share (class, row block) (one thread-block cluster, A multicast).
+// consecutive groups of cn tiles share (class, row block) (cn = 1 everywhere since the A multicast was dropped).
 std::vector<TileDesc> balanced_tiles(const std::vector<int>& cp, const std::vector<int>& ncols, int bm, int bn,
                                      int slots, int cn);
 // A matrices of the grouped GEMM: row-major lda x lda -> chunk-major swizzled (dst needs nmat*lda*lda + slack).
@@ -134,7 +134,7 @@ cudaError_t launch_chunk_swizzle(const double* src, double* dst, int nmat, int l
 constexpr int kK2Slack = 224 * 16;   // doubles after the last chunk-major matrix (tile rows past lda)
 cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
                               int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
-                              double* Y, int ldy, int cn, cudaStream_t s);
+                              double* Y, int ldy, cudaStream_t s);
 // Multiplicative colour-ordered smoother: d[dof(P, mu_hat)] += omega * Y[P][mu_hat] for the patches
 // (sub-class, column) of one colour; same-colour patches are DoF-disjoint, so there are no conflicting writes.
 cudaError_t launch_colour_update(const LevelGeom& g, int r, const PatchClass* cls, const int2* items, int nitems,

@@ -18,16 +18,15 @@ namespace stgmg {
 // Grouped GEMM  Y[:, P] = Ainv_class * R_P r  on the FP64 tensor pipe (mma.sync m8n8k4 -> SASS DMMA.8x8x4).
 // A CTA computes a BM (patch-local rows mu_hat) x BN (patches of one class) tile; K runs in chunks of 16.
 //   A operand: the class inverse is stored chunk-major and bank-swizzled (see launch_chunk_swizzle), so the BM x 16
-//     slab of a chunk is ONE contiguous run of BM x 128 bytes.  The CTAs of a thread-block cluster (CN = 1, 2 or 4)
-//     share (class, row block) and differ only in their patch columns: each issues a 1/CN slice of every A chunk as a
-//     bulk async copy multicast to all CN CTAs (cp.async.bulk ... multicast::cluster, completion on an mbarrier), so
-//     the L2 -> SM traffic of A — the operand every tile re-reads — drops CN-fold.
+//     slab of a chunk is ONE contiguous run of BM x 128 bytes, fetched by a single bulk async copy (cp.async.bulk,
+//     completion counted on the stage's mbarrier).
 //   B operand: R_P r gathered element-wise with cp.async (zero fill beyond C_P / for absent columns).
-//   Pipeline: S stages; a cluster barrier (arrive after the local __syncthreads, wait after the chunk's DMMAs)
-//   guarantees that no CTA overwrites a stage another CTA is still reading.
-// Tile variants (WM x WN warps, each MT x NT m8n8 tiles, split-K KS): tall 224 x 32, big 112 x 32, medium 56 x 32,
-// small 32 x 8.  Split-K partial sums are added in a fixed order, every output element is computed by exactly one CTA
-// with the same k order whatever the tiling or cluster size: the result is bitwise reproducible.
+//   S-stage pipeline, one __syncthreads per chunk.  (Multicasting A over thread-block clusters and a
+//   warp-specialised variant of THIS gathered-B kernel were measured slower; the dense K2D below,
+//   whose B is pre-expanded, is the warp-specialised kernel.)
+// Tile variants (WM x WN warps, each MT x NT m8n8 tiles, split-K KS): big 112 x 32, wide 112 x 64, medium 56 x 32,
+// small 32 x 8, and the latency variants K2L below.  Split-K partial sums are added in a fixed order, every output
+// element is computed by exactly one CTA with the same k order whatever the tiling: bitwise reproducible.
 constexpr int K2_BK = 16;
 constexpr int K2_MAXCP = 2048;       // largest C_P whose gather table is staged in shared memory
 
@@ -59,24 +58,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
           smem_u32(b)),
       "r"(parity)
-      : "memory");
-}
-// relaxed arrive: every read of the stage being released has already returned (its values fed DMMAs before the
-// preceding __syncthreads), so no release fence (MEMBAR) is needed on the hot path
-__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ unsigned cluster_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-// bulk global -> shared copy of `bytes` (multiple of 16) to the same smem offset of every CTA in `mask`
-__device__ __forceinline__ void bulk_copy_mc(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
-                                             unsigned short mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
@@ -122,7 +103,7 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
                                                                   const int* __restrict__ relidx,
                                                                   const double* __restrict__ invc, int lda,
                                                                   const double* __restrict__ rvec,
-                                                                  double* __restrict__ Y, int ldy, int cn) {
+                                                                  double* __restrict__ Y, int ldy) {
   pdl_trigger();
   using C = K2Cfg<WM, WN, MT, NT, K2_STAGES, KS>;
   constexpr int BM = C::BM, BN = C::BN, NTH = C::THREADS, BSLD = C::BSLD, S = K2_STAGES;
@@ -135,29 +116,20 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
   const TileDesc td = tiles[blockIdx.x];
   const PatchClass pc = cls[td.cls];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned crank = cn > 1 ? cluster_rank() : 0u;
-  const unsigned short cmask = (unsigned short)((1u << cn) - 1u);
   const int cp = pc.cp;
   const int nchunks = (cp + K2_BK - 1) / K2_BK;
   // A chunk ch of this tile: rows [m0, m0 + BM) of chunk ch of the class's chunk-major inverse (lda rows per chunk)
   const double* Ab = invc + pc.inv_off + (long long)td.m0 * K2_BK;
   const long long achunk = (long long)lda * K2_BK;
-  constexpr unsigned SLICE_ROWS_1 = BM;   // rows per slice for cn = 1
-  const unsigned slice_rows = cn == 4 ? BM / 4 : (cn == 2 ? BM / 2 : SLICE_ROWS_1);
   auto issue_a = [&](int ch, int buf) {   // thread 0 only
     mbar_expect_tx(&full[buf], (unsigned)C::ABYTES);
-    const double* src = Ab + ch * achunk + (long long)crank * slice_rows * K2_BK;
-    double* dst = &As[buf][crank * slice_rows][0];
-    const unsigned bytes = slice_rows * K2_BK * (unsigned)sizeof(double);
-    if (cn > 1) bulk_copy_mc(dst, src, bytes, &full[buf], cmask);
-    else bulk_copy(dst, src, bytes, &full[buf]);
+    bulk_copy(&As[buf][0][0], Ab + ch * achunk, (unsigned)C::ABYTES, &full[buf]);
   };
   if (tid == 0) {
     for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (cn > 1) { cluster_arrive(); cluster_wait(); }   // every CTA's barriers exist before any multicast lands
   // the class inverse is static: its first chunks stream in while the previous kernel drains (PDL)
   if (tid == 0)
     for (int st = 0; st < S - 1; ++st)
@@ -223,14 +195,12 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
     mbar_wait(&full[buf], (unsigned)((ch / S) & 1));
     cp_async_wait<S - 2>();
     __syncthreads();
-    if (cn > 1) cluster_arrive();                 // this CTA is done with the stage of chunk ch - 1
     // warp-uniform branch on the number of non-empty 8-column blocks (predicated-off DMMAs still occupy the pipe)
     if (nj == NT) k2_mma_impl<MT, NT, NT, KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
     else if (nj == NT - 1) k2_mma_impl<MT, NT, (NT > 1 ? NT - 1 : 1), KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
     else if (nj == NT - 2) k2_mma_impl<MT, NT, (NT > 2 ? NT - 2 : 1), KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
     else if (nj == NT - 3) k2_mma_impl<MT, NT, (NT > 3 ? NT - 3 : 1), KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
     else if (nj == NT - 4) k2_mma_impl<MT, NT, (NT > 4 ? NT - 4 : 1), KS, BM, BSLD, BN>(acc, As[buf], Bs[buf], wm, wn, kslice, lane, swz);
-    if (cn > 1) cluster_wait();                   // every CTA is done with that stage: it may be refilled
     const int nx = ch + S - 1;                    // refill the stage consumed in iteration ch - 1
     if (nx < nchunks) {
       if (tid == 0) issue_a(nx, nx % S);
@@ -282,7 +252,6 @@ static void k2_set_attr() {
   if (!attr) {
     cudaFuncSetAttribute(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM);
-    cudaFuncSetAttribute(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     attr = true;
   }
 }
@@ -290,62 +259,29 @@ static void k2_set_attr() {
 template <int WM, int WN, int MT, int NT, int ST, int KS>
 static cudaError_t launch_k2(const LevelGeom& g, int r, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
                              const int* relidx, const double* invc, int lda, const double* rvec, double* Y, int ldy,
-                             int cn, cudaStream_t s) {
+                             cudaStream_t s) {
   using C = K2Cfg<WM, WN, MT, NT, ST, KS>;
   k2_set_attr<WM, WN, MT, NT, ST, KS>();
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ntiles);
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = cn;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = cn > 1 ? 2 : 1;   // no cluster attribute for cn = 1 (plain launch)
-  return cudaLaunchKernelEx(&cfg, patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, g, r, cls_dev, tiles, relidx, invc, lda,
-                            rvec, Y, ldy, cn);
+  return launch_pdl(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, dim3(ntiles), dim3(C::THREADS), C::SMEM, s, g, r, cls_dev,
+                    tiles, relidx, invc, lda, rvec, Y, ldy);
 }
 
-#define K2_TALL 4, 1, 7, 5, 4, 2    // 224 x 40, 8 warps (2-way split-K): the whole C_P <= 224 in one tile
 #define K2_BIG 2, 2, 7, 2, 5, 2     // 112 x 32, 8 warps (2-way split-K), 2 CTAs / SM
 #define K2_MED 1, 2, 7, 2, 4, 4     // 56 x 32, 8 warps (4-way split-K)
 #define K2_SMALL 2, 1, 2, 1, 4, 4   // 32 x 8, 8 warps (4-way split-K)
-#define K2_BIGK1 2, 2, 7, 2, 4, 1   // 112 x 32, 4 warps (no split-K), 3 CTAs / SM
 #define K2_WIDE 2, 4, 7, 2, 3, 1    // 112 x 64, 8 warps (no split-K), 2 CTAs / SM
 
 template <int WM, int WN, int MT, int NT, int ST, int KS>
-static int k2_occ(int cn) {
+static int k2_occ() {
   using C = K2Cfg<WM, WN, MT, NT, ST, KS>;
   k2_set_attr<WM, WN, MT, NT, ST, KS>();
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cn * 148);
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cn;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int nclusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&nclusters, patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, &cfg) != cudaSuccess ||
-      nclusters <= 0) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, C::THREADS,
+                                                    C::SMEM) != cudaSuccess || nb <= 0) {
     cudaGetLastError();
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, C::THREADS,
-                                                      C::SMEM) != cudaSuccess || nb <= 0) {
-      cudaGetLastError();
-      nb = 1;
-    }
-    return nb * 148;
+    nb = 1;
   }
-  return nclusters * cn;
+  return nb * 148;
 }
 
 // K2D: dense variant of K2 for large levels.  The residual arrives patch-expanded (gather_expand_kernel: class
@@ -669,36 +605,31 @@ static int k2l_slots() {
 }
 
 // resident CTA slots of the whole GPU for a tile variant
-int k2_slots(int variant, int cn) {
+int k2_slots(int variant) {
   if (variant == 4) return k2l_slots<1>();
   if (variant == 7) return k2l_slots<2>();
   if (variant == 8) return k2l_slots<4>();
-  if (variant == 5) return k2_occ<K2_BIGK1>(cn);
-  if (variant == 6) return k2_occ<K2_WIDE>(cn);
-  if (variant == 3) return k2_occ<K2_TALL>(cn);
-  if (variant == 2) return k2_occ<K2_BIG>(cn);
-  if (variant == 1) return k2_occ<K2_MED>(cn);
-  return k2_occ<K2_SMALL>(cn);
+  if (variant == 6) return k2_occ<K2_WIDE>();
+  if (variant == 2) return k2_occ<K2_BIG>();
+  if (variant == 1) return k2_occ<K2_MED>();
+  return k2_occ<K2_SMALL>();
 }
 
 void k2_tile_shape(int variant, int* bm, int* bn) {
-  using T = K2Cfg<K2_TALL>;
   using B = K2Cfg<K2_BIG>;
   using M = K2Cfg<K2_MED>;
   using Sm = K2Cfg<K2_SMALL>;
   if (variant == 4) { *bm = 8 * K2L_MT; *bn = 8; }
   else if (variant == 7) { *bm = 8 * K2L_MT; *bn = 16; }
   else if (variant == 8) { *bm = 8 * K2L_MT; *bn = 32; }
-  else if (variant == 5) { *bm = K2Cfg<K2_BIGK1>::BM; *bn = K2Cfg<K2_BIGK1>::BN; }
   else if (variant == 6) { *bm = K2Cfg<K2_WIDE>::BM; *bn = K2Cfg<K2_WIDE>::BN; }
-  else if (variant == 3) { *bm = T::BM; *bn = T::BN; }
   else if (variant == 2) { *bm = B::BM; *bn = B::BN; }
   else if (variant == 1) { *bm = M::BM; *bn = M::BN; }
   else { *bm = Sm::BM; *bn = Sm::BN; }
 }
 
-// Measured on B200 (cfg1 fine level, 4225 patches, C_P = 218): big 22 us, tall 29 us (one CTA per SM hides less
-// latency than two), so tall is not picked automatically (STGMG_K2_VARIANT=3 forces it on the fine level).
+// Variants: 0 small, 1 medium, 2 big, 6 wide (pipelined, gathered B; 2 / 6 run as the dense K2D where the level has
+// the expanded residual), 4 / 7 / 8 K2L with 8 / 16 / 32 columns.  Measured choices on B200 in the comments.
 int k2_pick_variant(long long npatch, int maxcp) {
   if (const char* ev = std::getenv("STGMG_K2L_MAX")) { if (npatch < std::atoll(ev)) return 4; }
   else if (npatch < 200 && maxcp <= 700) return 4;   // latency variant on the smallest 2D levels (25 / 81 patches);
@@ -713,16 +644,14 @@ int k2_pick_variant(long long npatch, int maxcp) {
 
 cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
                               int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
-                              double* Y, int ldy, int cn, cudaStream_t s) {
+                              double* Y, int ldy, cudaStream_t s) {
   if (variant == 4) return launch_k2l<1>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
   if (variant == 7) return launch_k2l<2>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
   if (variant == 8) return launch_k2l<4>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
-  if (variant == 5) return launch_k2<K2_BIGK1>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
-  if (variant == 6) return launch_k2<K2_WIDE>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
-  if (variant == 3) return launch_k2<K2_TALL>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
-  if (variant == 2) return launch_k2<K2_BIG>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
-  if (variant == 1) return launch_k2<K2_MED>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
-  return launch_k2<K2_SMALL>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, cn, s);
+  if (variant == 6) return launch_k2<K2_WIDE>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
+  if (variant == 2) return launch_k2<K2_BIG>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
+  if (variant == 1) return launch_k2<K2_MED>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
+  return launch_k2<K2_SMALL>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
 }
 
 // Row-major lda x lda matrices -> chunk-major, bank-swizzled layout read by K2:
