@@ -1,0 +1,111 @@
+"""Boundary behaviour of stgmg_solve / stgmg_solve_host on the GPU (-m gpu): determinism (no atomics: repeated calls
+are bitwise identical), host-buffer entry point = device entry point, absolute tolerance (STGMG_TOL_ABS),
+restarts (reading A4) and maxit / STGMG_NOT_CONVERGED, each against the oracle's FGMRES where it applies."""
+import numpy as np
+import pytest
+
+from stgmg_inputs import uniform_load, random_vector
+from tests.gpu_common import small_config, oracle_hierarchy, cfg_key, to_gpu, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pair():
+    import torch
+    from paper_2303_06742_b200 import Solver
+    cfg = small_config(1)
+    s = Solver(cfg)
+    H = oracle_hierarchy(cfg_key(cfg))
+    yield cfg, s, H
+    s.close()
+    torch.cuda.synchronize()
+
+
+def test_repeated_solves_are_bitwise_identical(pair):
+    import torch
+    cfg, s, H = pair
+    b = to_gpu(uniform_load(H.fine.N, 91))
+    xs, its = [], []
+    for _ in range(3):
+        x = torch.zeros(H.fine.N, dtype=torch.float64, device="cuda")
+        st = s.solve(b, x, tol=cfg["rtol"], restart=cfg["restart"])
+        torch.cuda.synchronize()
+        xs.append(to_np(x))
+        its.append(st["iterations"])
+    assert its[0] == its[1] == its[2]
+    assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[0], xs[2])
+    v1 = torch.zeros_like(b)
+    v2 = torch.zeros_like(b)
+    s.vcycle(b, v1)
+    s.vcycle(b, v2)
+    torch.cuda.synchronize()
+    assert torch.equal(v1, v2)
+
+
+def test_solve_host_equals_solve(pair):
+    import torch
+    cfg, s, H = pair
+    bn = uniform_load(H.fine.N, 92)
+    x = torch.zeros(H.fine.N, dtype=torch.float64, device="cuda")
+    st = s.solve(to_gpu(bn), x, tol=cfg["rtol"], restart=cfg["restart"])
+    torch.cuda.synchronize()
+    xh = np.zeros(H.fine.N)
+    sth = s.solve_host(np.ascontiguousarray(bn), xh, tol=cfg["rtol"], restart=cfg["restart"])
+    assert sth["iterations"] == st["iterations"]
+    assert np.array_equal(xh, to_np(x))
+
+
+def test_absolute_tolerance_and_restarts_match_oracle(pair):
+    """TOL_ABS stops on ||r|| <= tol; restart m = 2 forces restarts from the true residual (A4).  Both against
+    the oracle's FGMRES with the same settings: iterations +-1, solution 1e-8."""
+    import torch
+    from oracle.gmres import fgmres, TOL_ABS
+    from paper_2303_06742_b200.stgmg import TOL_ABS as GPU_TOL_ABS
+    cfg, s, H = pair
+    bn = uniform_load(H.fine.N, 93)
+    A = H.A[-1]
+    tabs = 3e-9 * np.linalg.norm(bn)       # an absolute target that no relative setting of the same run reproduces
+    for tol, mode, gmode, restart in [(tabs, TOL_ABS, GPU_TOL_ABS, 30), (1e-10, 0, 0, 2)]:
+        x = torch.zeros(H.fine.N, dtype=torch.float64, device="cuda")
+        st = s.solve(to_gpu(bn), x, tol=tol, tol_mode=gmode, restart=restart)
+        torch.cuda.synchronize()
+        xo, info = fgmres(lambda v: A @ v, bn, H.vcycle, tol=tol, tol_mode=mode, restart=restart)
+        assert st["converged"] and info["converged"]
+        assert abs(st["iterations"] - info["iterations"]) <= 1
+        xg = to_np(x)
+        assert np.linalg.norm(xg - xo) <= 1e-8 * np.linalg.norm(xo)
+        r = np.linalg.norm(bn - A @ xg)
+        if mode == TOL_ABS:
+            assert r <= tol * (1 + 1e-6)
+        if restart == 2:
+            assert st["restarts"] >= 1 and st["restarts"] == info["restarts"]
+
+
+def test_maxit_returns_not_converged_with_last_iterate(pair):
+    import torch
+    cfg, s, H = pair
+    bn = uniform_load(H.fine.N, 94)
+    x = torch.zeros(H.fine.N, dtype=torch.float64, device="cuda")
+    st = s.solve(to_gpu(bn), x, tol=1e-14, restart=30, maxit=1)
+    torch.cuda.synchronize()
+    assert not st["converged"] and st["iterations"] == 1
+    xg = to_np(x)
+    assert np.all(np.isfinite(xg)) and np.linalg.norm(xg) > 0
+    r = np.linalg.norm(bn - H.A[-1] @ xg) / np.linalg.norm(bn)
+    assert abs(r - st["rel_residual"]) <= 1e-10 and r < 1.0
+
+
+def test_nonzero_initial_guess_matches_oracle(pair):
+    """x on entry is the initial guess X^(0) (r_0 = b - A X^(0)); device vs oracle FGMRES from the same X^(0)."""
+    import torch
+    from oracle.gmres import fgmres
+    cfg, s, H = pair
+    bn = uniform_load(H.fine.N, 95)
+    x0 = random_vector(H.fine.N, 96, 1e-2)
+    x = to_gpu(x0)
+    st = s.solve(to_gpu(bn), x, tol=cfg["rtol"], restart=cfg["restart"])
+    torch.cuda.synchronize()
+    xo, info = fgmres(lambda v: H.A[-1] @ v, bn, H.vcycle, x0=x0, tol=cfg["rtol"], restart=cfg["restart"])
+    assert st["converged"] and abs(st["iterations"] - info["iterations"]) <= 1
+    assert np.linalg.norm(to_np(x) - xo) <= 1e-8 * np.linalg.norm(xo)
