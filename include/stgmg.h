@@ -200,7 +200,8 @@ int64_t stgmg_last_launch_count(const stgmg_handle* h);
 int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double* k2_bytes, double* k1_bytes);
 
 /* Times reps back-to-back launches of one hot-path kernel on level l with CUDA events on params.stream:
- * kind 0 = K2 patch GEMM, 1 = K1 operator apply (all colours), 2 = K3 averaging, 3 = whole V-cycle graph.
+ * kind 0 = K2 patch GEMM, 1 = K1 operator apply (all colours), 2 = K3 averaging, 3 = whole V-cycle graph,
+ * 4 / 5 = empty kernel on 1 / 148 CTAs, 6 = one smoothing sweep (level >= 1), 7 = restriction + prolongation.
  * Operates on the level's internal work buffers (their contents are overwritten). */
 int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms);
 

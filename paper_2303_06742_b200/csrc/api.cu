@@ -2037,7 +2037,10 @@ int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double*
 
 int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms) {
   if (!h || level < 0 || level >= h->L || reps < 1 || !avg_ms) { set_error("bad argument"); return STGMG_EINVAL; }
-  if ((kind == 0 || kind == 2) && level < 1) { set_error("smoother kernels need level >= 1"); return STGMG_EINVAL; }
+  if ((kind == 0 || kind == 2 || kind == 6 || kind == 7) && level < 1) {
+    set_error("smoother kernels need level >= 1");
+    return STGMG_EINVAL;
+  }
   LevelData& Lv = h->lev[level];
   auto one = [&]() -> int {
     if (kind == 0) {
@@ -2055,6 +2058,11 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
       CKE(launch_noop(1, h->s));
     } else if (kind == 5) {
       CKE(launch_noop(148, h->s));
+    } else if (kind == 6) {   // one post-smoothing sweep (residual, patch solves, averaging)
+      CK(sweep(h, level, Lv.b, Lv.d, false));
+    } else if (kind == 7) {   // restriction to and prolongation from level - 1
+      CK(restrict_level(h, level, Lv.r, h->lev[level - 1].b));
+      CK(prolong_level(h, level, h->lev[level - 1].d, Lv.d));
     } else if (h->vgraph) {
       CKE(cudaGraphLaunch(h->vgraph, h->s));
     } else {

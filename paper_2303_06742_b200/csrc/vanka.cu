@@ -375,8 +375,16 @@ __global__ void __launch_bounds__(32 * (WM * WN * KS + 1), 2)
       const double* Bb = rexp + pc.rexp_off + (long long)td.n0 * K2_BK;
       const long long bchunk = (long long)pc.ncols * K2_BK;
       const unsigned bbytes = (unsigned)(td.nn * K2_BK * sizeof(double));
+      // the class inverse is static: the first S chunks of A stream in while the previous kernel drains (PDL);
+      // each stage's barrier expects A + B bytes, so it completes only when B has landed too
+      const int pre = nchunks < S ? nchunks : S;
+      for (int ch = 0; ch < pre; ++ch) {
+        mbar_expect_tx(&full[ch], (unsigned)C::ABYTES + bbytes);
+        bulk_copy(&As[ch][0][0], Ab + ch * achunk, (unsigned)C::ABYTES, &full[ch]);
+      }
       pdl_wait();
-      for (int ch = 0; ch < nchunks; ++ch) {
+      for (int ch = 0; ch < pre; ++ch) bulk_copy(&Bs[ch][0][0], Bb + ch * bchunk, bbytes, &full[ch]);
+      for (int ch = pre; ch < nchunks; ++ch) {
         const int st = ch % S;
         if (ch >= S) mbar_wait(&empty[st], (unsigned)(((ch / S) - 1) & 1));
         mbar_expect_tx(&full[st], (unsigned)C::ABYTES + bbytes);
@@ -479,12 +487,21 @@ int k2d_slots(int variant) {
 }
 
 // K2L: latency variant of K2 for small levels (few patches; the V-cycle there is a chain of latency-bound kernels).
-// CTA = 8*MT rows x 8 patch columns of one class.  No shared-memory pipeline: warp w takes the 16-wide K chunks
+// CTA = 8*MT rows x 8*NT patch columns of one class.  No shared-memory pipeline: warp w takes the 16-wide K chunks
 // w, w + nw, ..; every lane loads its m8n8k4 A fragments straight from the chunk-major inverse (L2) and its B
-// fragment element from r (through the class gather table), so the critical path is two dependent loads plus the
-// DMMAs of one or two chunks.  The nw partial products are added in warp order (fixed) through shared memory.
+// fragment element from r (through the class gather table).  Within a chunk, lane q of a fragment row takes
+// k = 4q + s in the s-th m8n8k4 step (A and B alike), so its four A values are one contiguous, 32-byte aligned block of
+// the swizzled row (block q ^ (row mod 4)): ONE 256-bit load per row fragment (LDG.256) instead of four 64-bit loads
+// that touch a single sector of each of eight lines — the L1/L2 request rate, not the bytes, bounded the A stream.  The inverse and the gather table are static (setup),
+// so the A fragments and gather codes of a warp's first chunk, the codes of its second and the output vertex of
+// every column are fetched BEFORE the programmatic-dependent-launch wait, while the previous kernel drains; after
+// the wait the critical path is one L2 round trip (the B elements of both chunks and the second A chunk in flight
+// together), the DMMAs and the reduction.  The nw partial products are added in warp order (fixed) through shared
+// memory.
+constexpr int k2l_max_warps(int nt) { return nt == 1 ? 16 : nt == 2 ? 7 : 4; }
+
 template <int MT, int NT>
-__global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r, const PatchClass* __restrict__ cls,
+__global__ void __launch_bounds__(32 * k2l_max_warps(NT), NT == 1 ? 1 : 2) patch_gemm_lat_kernel(LevelGeom g, int r, const PatchClass* __restrict__ cls,
                                                              const TileDesc* __restrict__ tiles,
                                                              const int* __restrict__ relidx,
                                                              const double* __restrict__ invc, int lda,
@@ -492,6 +509,7 @@ __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r,
                                                              int ldy) {
   pdl_trigger();
   extern __shared__ double lred[];   // [nw][MT][NT][2][32]
+  __shared__ int splin[NT * 8];
   const TileDesc td = tiles[blockIdx.x];
   const PatchClass pc = cls[td.cls];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -510,6 +528,12 @@ __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r,
       vs *= (g.n[a] + 1);
     }
   };
+  if (threadIdx.x < NT * 8) {
+    const int n = threadIdx.x;
+    int q, p, pl = -1;
+    if (n < td.nn && td.n0 + n < pc.ncols) col_base(td.n0 + n, q, p, pl);
+    splin[n] = pl;
+  }
   // this lane's B columns j*8 + lane/4 (m8n8k4 .col fragment: k = lane & 3)
   bool cvalid[NT];
   int bq[NT], bp[NT];
@@ -521,39 +545,68 @@ __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r,
     bq[j] = bp[j] = 0;
     if (cvalid[j]) col_base(td.n0 + nl, bq[j], bp[j], pl);
   }
-  const int swz = ((lane >> 2) & 3) << 2;
   const double* Ab = invc + pc.inv_off + (long long)(td.m0 + (lane >> 2)) * K2_BK;
   const int* rel = relidx + pc.rel_off;
+  auto load_codes = [&](int ch, int (&code)[4]) {
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+      const int k = ch * K2_BK + (lane & 3) * 4 + st;
+      code[st] = (ch < nch && k < cp) ? __ldg(rel + k) : -1;
+    }
+  };
+  auto load_a = [&](int ch, double (&a)[4][MT]) {
+    const double* Ac = Ab + (long long)ch * lda * K2_BK + (((lane & 3) ^ ((lane >> 2) & 3)) << 2);
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n"
+                   : "=d"(a[0][i]), "=d"(a[1][i]), "=d"(a[2][i]), "=d"(a[3][i])
+                   : "l"(Ac + i * 8 * K2_BK));
+  };
+  auto load_b = [&](const int (&code)[4], double (&b)[4][NT]) {
+#pragma unroll
+    for (int st = 0; st < 4; ++st)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        b[st][j] = (cvalid[j] && code[st] >= 0) ? __ldg(rvec + (code[st] >> 1) + ((code[st] & 1) ? bp[j] : bq[j]))
+                                                : 0.0;
+  };
   double acc[MT][NT][2];
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  pdl_wait();
-  for (int ch = warp; ch < nch; ch += nw) {
-    double a[4][MT], b[4][NT];
-    int code[4];
-    const double* Ac = Ab + (long long)ch * lda * K2_BK;
-#pragma unroll
-    for (int st = 0; st < 4; ++st) {
-      const int k = ch * K2_BK + st * 4 + (lane & 3);
-      code[st] = k < cp ? __ldg(rel + k) : -1;
-#pragma unroll
-      for (int i = 0; i < MT; ++i) a[st][i] = __ldg(Ac + i * 8 * K2_BK + ((st * 4 + (lane & 3)) ^ swz));
-    }
-#pragma unroll
-    for (int st = 0; st < 4; ++st)
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-        b[st][j] = (cvalid[j] && code[st] >= 0)
-                       ? __ldg(rvec + (code[st] >> 1) + ((code[st] & 1) ? bp[j] : bq[j]))
-                       : 0.0;
+  auto mma = [&](const double (&a)[4][MT], const double (&b)[4][NT]) {
 #pragma unroll
     for (int st = 0; st < 4; ++st)
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[st][i], b[st][j]);
+  };
+  const int c0 = warp, c1 = warp + nw;
+  int k0[4], k1[4];
+  double a0[4][MT];
+  load_codes(c0, k0);
+  load_codes(c1, k1);
+  if (c0 < nch) load_a(c0, a0);
+  pdl_wait();
+  if (c0 < nch) {
+    double b0[4][NT], b1[4][NT], a1[4][MT];
+    load_b(k0, b0);
+    if (c1 < nch) {
+      load_b(k1, b1);
+      load_a(c1, a1);
+    }
+    mma(a0, b0);
+    if (c1 < nch) mma(a1, b1);
+    for (int ch = c1 + nw; ch < nch; ch += nw) {   // more than two chunks per warp (large C_P)
+      int kc[4];
+      double ac[4][MT], bc[4][NT];
+      load_codes(ch, kc);
+      load_a(ch, ac);
+      load_b(kc, bc);
+      mma(ac, bc);
+    }
   }
 #pragma unroll
   for (int i = 0; i < MT; ++i)
@@ -564,22 +617,22 @@ __global__ void __launch_bounds__(512) patch_gemm_lat_kernel(LevelGeom g, int r,
   __syncthreads();
   for (int t = threadIdx.x; t < MT * NT * 2 * 32; t += blockDim.x) {
     const int ln = t & 31, e = (t >> 5) & 1, j = (t >> 6) % NT, i = (t >> 6) / NT;
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += lred[(((w * MT + i) * NT + j) * 2 + e) * 32 + ln];
+    double sum = 0.0;
+    for (int w = 0; w < nw; ++w) sum += lred[(((w * MT + i) * NT + j) * 2 + e) * 32 + ln];
     const int row = td.m0 + i * 8 + (ln >> 2);
-    const int n = j * 8 + 2 * (ln & 3) + e;
-    if (row < cp && n < td.nn && td.n0 + n < pc.ncols) {
-      int q, p, plo;
-      col_base(td.n0 + n, q, p, plo);
-      Y[(long long)plo * ldy + row] = s;
-    }
+    const int pl = splin[j * 8 + 2 * (ln & 3) + e];
+    if (row < cp && pl >= 0) Y[(long long)pl * ldy + row] = sum;
   }
 }
 
 constexpr int K2L_MT = 4;   // 32-row tiles
 
 template <int NT>
-static int k2l_warps(int lda) { return std::max(1, std::min(16 / NT, lda / K2_BK)); }
+static int k2l_warps(int lda) {   // at most k2l_max_warps(NT), the chunks spread evenly (2 per warp on cfg1's level 4)
+  const int nch = std::max(1, lda / K2_BK), maxw = k2l_max_warps(NT);
+  const int per = (nch + maxw - 1) / maxw;
+  return (nch + per - 1) / per;
+}
 
 template <int NT>
 static size_t k2l_smem(int nw) { return sizeof(double) * nw * K2L_MT * NT * 2 * 32; }
@@ -596,8 +649,8 @@ static cudaError_t launch_k2l(const LevelGeom& g, int r, const PatchClass* cls_d
 template <int NT>
 static int k2l_slots() {
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_lat_kernel<K2L_MT, NT>, 32 * (16 / NT),
-                                                    k2l_smem<NT>(16 / NT)) != cudaSuccess || nb <= 0) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_lat_kernel<K2L_MT, NT>, 32 * k2l_max_warps(NT),
+                                                    k2l_smem<NT>(k2l_max_warps(NT))) != cudaSuccess || nb <= 0) {
     cudaGetLastError();
     nb = 1;
   }

@@ -333,7 +333,8 @@ class Solver:
         return dict(k2_flops=f.value, k2_bytes=bb.value, k1_bytes=b1.value)
 
     def time_kernel(self, kind, level=None, reps=20):
-        """Average ms of one launch (kind 0 = K2 patch GEMM, 1 = K1 apply, 2 = K3 average, 3 = V-cycle)."""
+        """Average ms of one launch (kind 0 = K2 patch GEMM, 1 = K1 apply, 2 = K3 average, 3 = V-cycle,
+        4 / 5 = empty kernel, 6 = one smoothing sweep, 7 = restriction + prolongation)."""
         lev = self.levels - 1 if level is None else level
         ms = ctypes.c_double()
         _check(self.lib.stgmg_time_kernel(self.h, kind, lev, reps, ctypes.byref(ms)), "stgmg_time_kernel")

@@ -24,6 +24,7 @@ for l in range(s.levels - 1, -1, -1):
         t2 = s.time_kernel(0, l, reps=50)
         line += "  K2 %.2f us (%.2f TF/s)" % (t2 * 1e3, w["k2_flops"] / t2 / 1e9)
         line += "  K3 %.2f us" % (s.time_kernel(2, l, reps=50) * 1e3)
+        line += "  sweep %.2f us  R+P %.2f us" % (s.time_kernel(6, l, reps=50) * 1e3, s.time_kernel(7, l, reps=50) * 1e3)
     line += "  K1 %.2f us" % (s.time_kernel(1, l, reps=50) * 1e3)
     print(line)
 print("vcycle %.3f ms" % s.time_kernel(3, s.levels - 1, reps=20))
