@@ -384,6 +384,7 @@ struct stgmg_handle {
   int rank = 0, nranks = 1;
   unsigned char* mask = nullptr;   // owned fine-level DoFs (Krylov inner products)
   bool graphable = true;
+  bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; 2D by choice)
   int nsm = 148;                   // SMs of the device (tile balancing)
 };
 
@@ -475,7 +476,7 @@ static int apply_level(stgmg_handle* h, int l, const double* x, double* y, const
     h->launches += 1;
     return 0;
   }
-  if (h->d == 2) return apply_geom(h, h->lev[l].g, h->c_dev, x, y, base, alpha, beta);
+  if (!h->op_gemm) return apply_geom(h, h->lev[l].g, h->c_dev, x, y, base, alpha, beta);
   LevelData& Lv = h->lev[l];
   const int ne = (int)elem_dofs(h);
   CKE(launch_patch_gemm(Lv.g, h->r, Lv.ek2var, Lv.ecls_dev, Lv.etiles_dev, Lv.entiles, Lv.erelidx_dev, Lv.E_dev,
@@ -594,7 +595,7 @@ static int residual_expand(stgmg_handle* h, int l, const double* b, const double
     h->launches += 1;
     return 0;
   }
-  if (h->d == 2) {
+  if (!h->op_gemm) {
     const long long ycs = cell_count(L.g) * elem_dofs(h);
     CKE(launch_op2d_cells(h->r, h->k1, L.g, h->c_dev, d, h->Yc, 1, 0, ycs, h->s));
     CKE(launch_gather_expand(L.g, h->r, h->k1, h->Yc, b, -1.0, 1.0, 0, L.cls_dev, L.Rexp, h->s));
@@ -1049,6 +1050,7 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
   for (int t = 0; t < nt; ++t) Lv.ecls[t].inv_off = (long long)t * Lv.elda * Lv.elda;
   if (gemm) {   // runtime element GEMM (3D operator): tiles, class records, gather tables, chunk-major matrices
     Lv.ek2var = k2_pick_variant(Lv.ncell_global ? Lv.ncell_global : cell_count(g), ne);
+    if (const char* ev = std::getenv("STGMG_EK2_VARIANT")) Lv.ek2var = std::atoi(ev);   // experiments
     int tbm = 0, tbn = 0;
     k2_tile_shape(Lv.ek2var, &tbm, &tbn);
     std::vector<TileDesc> tiles;
@@ -1679,7 +1681,10 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       CKE(cudaMemcpy(h->lc_dev, &lc, sizeof(LoadConsts), cudaMemcpyHostToDevice));
     }
     if (d == 2) CK(dalloc(h.get(), &h->Yc, (size_t)(cell_count(h->lev[levels - 1].g) * elem_dofs(h.get()))));
-    if (d == 3) {
+    h->op_gemm = d == 3;
+    if (d == 2)
+      if (const char* ev = std::getenv("STGMG_OP2D_GEMM")) h->op_gemm = std::atoi(ev) != 0;
+    if (h->op_gemm) {
       long long nv = 1;
       for (int a = 0; a < 3; ++a) nv *= h->lev[levels - 1].g.n[a] + 1;
       CK(dalloc(h.get(), &h->Ycell, (size_t)(nv * elem_dofs(h.get()))));

@@ -685,10 +685,10 @@ void k2_tile_shape(int variant, int* bm, int* bn) {
 // the expanded residual), 4 / 7 / 8 K2L with 8 / 16 / 32 columns.  Measured choices on B200 in the comments.
 int k2_pick_variant(long long npatch, int maxcp) {
   if (const char* ev = std::getenv("STGMG_K2L_MAX")) { if (npatch < std::atoll(ev)) return 4; }
-  else if (npatch < 200 && maxcp <= 700) return 4;   // latency variant on the smallest 2D levels (25 / 81 patches);
-                                                     // 3D coarse levels stream ~1 GB of inverses: pipelined is faster
-  if (npatch < 2000 && maxcp <= 256) return 7;   // K2L 32 x 16 (cfg1 level 4: 16.4 -> 14.3 us, level 3: 8.0 -> 7.4 us;
-                                                  // slower on cfg2's C_P = 663)
+  else if (npatch < 64 && maxcp <= 700) return 4;   // latency variant 32 x 8 on the smallest 2D levels (25 patches)
+  if (npatch < 2000 && maxcp <= 256) return 7;   // K2L 32 x 16 (cfg1 level 4: 16.4 -> 12.7 us, level 3: 8.0 -> 6.4 us,
+                                                  // level 2: 5.8 -> 5.4 us; slower on cfg2's C_P = 663)
+  if (npatch < 200 && maxcp <= 700) return 4;     // 3D coarse levels stream ~1 GB of inverses: pipelined is faster
   if (npatch >= 20000) return 6;      // wide 112 x 64 (cfg2 fine 25.6 -> 27.6 TF/s, cfg3 fine 27.1 -> 27.3)
   if (npatch >= 2000) return 2;
   if (npatch >= 1000) return maxcp > 256 ? 2 : 1;   // cfg2 level 4 (C_P 663): big 56 us vs medium 90 us
