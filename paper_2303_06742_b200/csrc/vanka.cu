@@ -657,8 +657,175 @@ static int k2l_slots() {
   return nb * 148;
 }
 
+// K2S: shared-B variant for the middle levels (C_P <= 256, up to a few thousand patches).  CTA = 8*NW rows x 32
+// patch columns, no split-K: warp w owns rows [m0 + 8w, m0 + 8w + 8) over the whole K.  The B tile (32 columns x
+// all of K) is gathered from r ONCE per CTA into shared memory (consecutive threads along k: contiguous node runs)
+// and read by every warp; each warp streams only its own A rows from L2 with one 256-bit load per chunk (k = 4q + s
+// lane mapping as K2L), one chunk ahead.  Against K2L (32 x 16 tiles, every warp re-reading A per column tile) this
+// halves the A stream and fits a level in one wave of CTAs.  Static operands (gather codes, column bases, the first
+// A chunk) are fetched before the PDL wait.  Summation over k is sequential per output (chunk order, then the
+// m8n8k4 steps), bitwise reproducible.
+constexpr int K2S_NW = 7;          // 56 rows: C_P = 218 -> 4 row tiles with no empty warp
+constexpr int K2S_BN = 32;
+constexpr int K2S_MAXLDA = 256;
+constexpr int K2S_AD = 6;          // A chunks in flight per warp
+constexpr int K2S_GU = 16;         // B gather loads in flight per thread
+__host__ __device__ constexpr int k2s_ldb(int lda) { return lda + 2; }   // row shift 16 B: conflict-free LDS.128
+
+template <int NJ>
+__device__ __forceinline__ void k2s_chunk(double (&acc)[4][2], const double (&a)[4], const double* bs, int ldb, int k0,
+                                          int lane) {
+  const double* bl = bs + (lane >> 2) * ldb + k0 + ((lane & 3) << 2);
+  double2 b[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    b[j][0] = *reinterpret_cast<const double2*>(bl + j * 8 * ldb);
+    b[j][1] = *reinterpret_cast<const double2*>(bl + j * 8 * ldb + 2);
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) dmma884(acc[j][0], acc[j][1], a[0], b[j][0].x);   // s outer, columns inner:
+#pragma unroll                                                                    // independent accumulators
+  for (int j = 0; j < NJ; ++j) dmma884(acc[j][0], acc[j][1], a[1], b[j][0].y);   // between dependent DMMAs
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) dmma884(acc[j][0], acc[j][1], a[2], b[j][1].x);
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) dmma884(acc[j][0], acc[j][1], a[3], b[j][1].y);
+}
+
+__global__ void __launch_bounds__(32 * K2S_NW, 2) patch_gemm_smb_kernel(LevelGeom g, int r,
+                                                                          const PatchClass* __restrict__ cls,
+                                                                          const TileDesc* __restrict__ tiles,
+                                                                          const int* __restrict__ relidx,
+                                                                          const double* __restrict__ invc, int lda,
+                                                                          const double* __restrict__ rvec,
+                                                                          double* __restrict__ Y, int ldy) {
+  pdl_trigger();
+  extern __shared__ __align__(16) double bsm[];   // [K2S_BN][ldb]
+  __shared__ int sbq[K2S_BN], sbp[K2S_BN], splin[K2S_BN];
+  __shared__ int srel[K2S_MAXLDA];
+  constexpr int NTH = 32 * K2S_NW;
+  const TileDesc td = tiles[blockIdx.x];
+  const PatchClass pc = cls[td.cls];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cp = pc.cp, nch = (cp + K2_BK - 1) / K2_BK, kp = nch * K2_BK;
+  const int ldb = k2s_ldb(lda);
+  if (tid < K2S_BN) {
+    int bq = 0, bp = 0, pl = -1;
+    if (tid < td.nn && td.n0 + tid < pc.ncols) {
+      int rem = td.n0 + tid, vs = 1;
+      pl = 0;
+      for (int a = 0; a < g.d; ++a) {
+        const int v = pc.vlo[a] + (rem % pc.cnt[a]) * pc.vst;
+        rem /= pc.cnt[a];
+        const int c0 = v > 0 ? v - 1 : 0;
+        bq += (r * c0) * (int)g.qs[a];
+        bp += ((r - 1) * c0) * (int)g.ps[a];
+        pl += v * vs;
+        vs *= (g.n[a] + 1);
+      }
+    }
+    sbq[tid] = bq;
+    sbp[tid] = bp;
+    splin[tid] = pl;
+  }
+  for (int k = tid; k < kp; k += NTH) srel[k] = k < cp ? __ldg(relidx + pc.rel_off + k) : -1;
+  const int row0 = td.m0 + 8 * warp;
+  const bool wact = row0 < cp;
+  const double* Aw = invc + pc.inv_off + (long long)(row0 + (lane >> 2)) * K2_BK + (((lane & 3) ^ ((lane >> 2) & 3)) << 2);
+  const long long achunk = (long long)lda * K2_BK;
+  // A ring of K2S_AD chunks in registers (static indexing: the chunk loop is unrolled by K2S_AD)
+  double a[K2S_AD][4];
+#pragma unroll
+  for (int u = 0; u < K2S_AD; ++u) {
+    a[u][0] = a[u][1] = a[u][2] = a[u][3] = 0.0;
+    if (wact && u < nch)
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n"
+                   : "=d"(a[u][0]), "=d"(a[u][1]), "=d"(a[u][2]), "=d"(a[u][3])
+                   : "l"(Aw + u * achunk));
+  }
+  __syncthreads();
+  pdl_wait();
+  const int ncol = td.nn;
+  const int ncz = ((ncol + 7) / 8) * 8;   // columns the DMMAs read (absent ones zero-filled)
+  for (int k = tid; k < kp; k += NTH) {   // B tile, thread per k: one gather code, then every column (no division)
+    const int code = srel[k];
+    const int off = code >> 1;
+    const bool isp = (code & 1) != 0;
+    for (int c0 = 0; c0 < ncz; c0 += K2S_GU) {
+      double v[K2S_GU];
+#pragma unroll
+      for (int u = 0; u < K2S_GU; ++u) {   // all loads of the batch in flight before the stores
+        const int col = c0 + u;
+        v[u] = 0.0;
+        if (col < ncol && code >= 0 && splin[col] >= 0) v[u] = __ldg(rvec + off + (isp ? sbp[col] : sbq[col]));
+      }
+#pragma unroll
+      for (int u = 0; u < K2S_GU; ++u)
+        if (c0 + u < ncz) bsm[(c0 + u) * ldb + k] = v[u];
+    }
+  }
+  __syncthreads();
+  if (!wact) return;
+  const int nj = (ncol + 7) / 8;
+  double acc[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int c0 = 0; c0 < nch; c0 += K2S_AD) {
+#pragma unroll
+    for (int u = 0; u < K2S_AD; ++u) {
+      const int ch = c0 + u;
+      if (ch < nch) {
+        if (nj >= 4) k2s_chunk<4>(acc, a[u], bsm, ldb, ch * K2_BK, lane);
+        else if (nj == 3) k2s_chunk<3>(acc, a[u], bsm, ldb, ch * K2_BK, lane);
+        else if (nj == 2) k2s_chunk<2>(acc, a[u], bsm, ldb, ch * K2_BK, lane);
+        else k2s_chunk<1>(acc, a[u], bsm, ldb, ch * K2_BK, lane);
+        if (ch + K2S_AD < nch)
+          asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n"
+                       : "=d"(a[u][0]), "=d"(a[u][1]), "=d"(a[u][2]), "=d"(a[u][3])
+                       : "l"(Aw + (ch + K2S_AD) * achunk));
+      }
+    }
+  }
+  const int row = row0 + (lane >> 2);
+  if (row < cp)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int pl = splin[j * 8 + 2 * (lane & 3) + e];
+        if (j < nj && pl >= 0) Y[(long long)pl * ldy + row] = acc[j][e];
+      }
+}
+
+static size_t k2s_smem(int lda) { return sizeof(double) * K2S_BN * k2s_ldb(lda); }
+
+static cudaError_t launch_k2s(const LevelGeom& g, int r, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
+                              const int* relidx, const double* invc, int lda, const double* rvec, double* Y, int ldy,
+                              cudaStream_t s) {
+  if (lda > K2S_MAXLDA) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(patch_gemm_smb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2s_smem(K2S_MAXLDA));
+    attr = true;
+  }
+  return launch_pdl(patch_gemm_smb_kernel, dim3(ntiles), dim3(32 * K2S_NW), k2s_smem(lda), s, g, r, cls_dev, tiles,
+                    relidx, invc, lda, rvec, Y, ldy);
+}
+
+static int k2s_slots() {
+  int nb = 0;
+  cudaFuncSetAttribute(patch_gemm_smb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2s_smem(K2S_MAXLDA));
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, patch_gemm_smb_kernel, 32 * K2S_NW, k2s_smem(K2S_MAXLDA)) !=
+          cudaSuccess || nb <= 0) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  return nb * 148;
+}
+
 // resident CTA slots of the whole GPU for a tile variant
 int k2_slots(int variant) {
+  if (variant == 9) return k2s_slots();
   if (variant == 4) return k2l_slots<1>();
   if (variant == 7) return k2l_slots<2>();
   if (variant == 8) return k2l_slots<4>();
@@ -672,7 +839,8 @@ void k2_tile_shape(int variant, int* bm, int* bn) {
   using B = K2Cfg<K2_BIG>;
   using M = K2Cfg<K2_MED>;
   using Sm = K2Cfg<K2_SMALL>;
-  if (variant == 4) { *bm = 8 * K2L_MT; *bn = 8; }
+  if (variant == 9) { *bm = 8 * K2S_NW; *bn = K2S_BN; }
+  else if (variant == 4) { *bm = 8 * K2L_MT; *bn = 8; }
   else if (variant == 7) { *bm = 8 * K2L_MT; *bn = 16; }
   else if (variant == 8) { *bm = 8 * K2L_MT; *bn = 32; }
   else if (variant == 6) { *bm = K2Cfg<K2_WIDE>::BM; *bn = K2Cfg<K2_WIDE>::BN; }
@@ -686,6 +854,8 @@ void k2_tile_shape(int variant, int* bm, int* bn) {
 int k2_pick_variant(long long npatch, int maxcp) {
   if (const char* ev = std::getenv("STGMG_K2L_MAX")) { if (npatch < std::atoll(ev)) return 4; }
   else if (npatch < 64 && maxcp <= 700) return 4;   // latency variant 32 x 8 on the smallest 2D levels (25 patches)
+  if (npatch >= 500 && npatch < 2000 && maxcp <= 256) return 9;   // K2S shared-B 56 x 32 (cfg1 level 4: 12.6 -> 10.4 us;
+                                                                   // slower than K2L below ~500 patches)
   if (npatch < 2000 && maxcp <= 256) return 7;   // K2L 32 x 16 (cfg1 level 4: 16.4 -> 12.7 us, level 3: 8.0 -> 6.4 us,
                                                   // level 2: 5.8 -> 5.4 us; slower on cfg2's C_P = 663)
   if (npatch < 200 && maxcp <= 700) return 4;     // 3D coarse levels stream ~1 GB of inverses: pipelined is faster
@@ -698,6 +868,7 @@ int k2_pick_variant(long long npatch, int maxcp) {
 cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
                               int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
                               double* Y, int ldy, cudaStream_t s) {
+  if (variant == 9) return launch_k2s(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
   if (variant == 4) return launch_k2l<1>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
   if (variant == 7) return launch_k2l<2>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
   if (variant == 8) return launch_k2l<4>(g, r, cls_dev, tiles, ntiles, relidx, invc, lda, rvec, Y, ldy, s);
