@@ -350,6 +350,10 @@ struct LevelData {
   bool dense = false;
   double* Rexp = nullptr;
   long long nrexp = 0;
+  int4* exp_blocks = nullptr;   // expand_pull blocks {class, chunk, first column, columns}
+  int n_exp_blocks = 0;
+  int2* colbase = nullptr;      // per patch column (class-major): gather bases (bq, bp)
+  bool exp_fused = false;       // STGMG_EXPAND_FUSED=1: the push-form gather_expand instead
 };
 
 struct stgmg_handle {
@@ -590,6 +594,16 @@ static int sweep_colored(stgmg_handle* h, int l, const double* b, double* d, boo
 // r = b - A_l d written straight into the patch-expanded B operand of the dense K2 (d == nullptr: r = b)
 static int residual_expand(stgmg_handle* h, int l, const double* b, const double* d) {
   LevelData& L = h->lev[l];
+  if (!L.exp_fused) {   // r = b - A d (node gather), then the pull-form expansion
+    const double* src = b;
+    if (d) {
+      CK(residual(h, l, b, d, L.r));
+      src = L.r;
+    }
+    CKE(launch_expand_pull(L.exp_blocks, L.n_exp_blocks, L.cls_dev, L.relidx_dev, L.colbase, src, L.Rexp, h->s));
+    h->launches += 1;
+    return 0;
+  }
   if (!d) {
     CKE(launch_gather_expand(L.g, h->r, h->k1, nullptr, b, 0.0, 1.0, 0, L.cls_dev, L.Rexp, h->s));
     h->launches += 1;
@@ -854,10 +868,12 @@ static int build_patches(stgmg_handle* h, int l) {
   if (const char* ev = std::getenv("STGMG_K2_DENSE"))   // experiments / tests: 0 = never, 1 = on big / wide levels
     Lv.dense = std::atoi(ev) != 0 && (Lv.k2var == 2 || Lv.k2var == 6) && h->prm.smoother == STGMG_SMOOTH_ADDITIVE;
   {
-    long long off = 0;
+    long long off = 0, coff = 0;
     for (auto& c : Lv.cls) {
       c.rexp_off = off;
       off += (long long)((c.cp + 15) / 16) * c.ncols * 16;
+      c.col_off = coff;
+      coff += c.ncols;
     }
     Lv.nrexp = off;
   }
@@ -870,6 +886,28 @@ static int build_patches(stgmg_handle* h, int l) {
   if (Lv.dense) {
     CK(dalloc(h, &Lv.Rexp, (size_t)Lv.nrexp));
     CKE(cudaMemsetAsync(Lv.Rexp, 0, sizeof(double) * (size_t)Lv.nrexp, h->s));   // slots past C_P stay zero
+    if (const char* ev = std::getenv("STGMG_EXPAND_FUSED")) Lv.exp_fused = std::atoi(ev) != 0;
+    std::vector<int4> eb;
+    std::vector<int2> cb;
+    for (int ci = 0; ci < (int)Lv.cls.size(); ++ci) {
+      const PatchClass& c = Lv.cls[ci];
+      for (int q = 0; q < (c.cp + 15) / 16; ++q)
+        for (int c0 = 0; c0 < c.ncols; c0 += EXPAND_COLS) eb.push_back(make_int4(ci, q, c0, std::min(EXPAND_COLS, c.ncols - c0)));
+      for (int col = 0; col < c.ncols; ++col) {   // gather bases of the patch in column col (as the K2 kernels)
+        int rem = col, bq = 0, bp = 0;
+        for (int a = 0; a < d; ++a) {
+          const int v = c.vlo[a] + (rem % c.cnt[a]) * c.vst;
+          rem /= c.cnt[a];
+          const int c0 = v > 0 ? v - 1 : 0;
+          bq += (h->r * c0) * (int)g.qs[a];
+          bp += ((h->r - 1) * c0) * (int)g.ps[a];
+        }
+        cb.push_back(make_int2(bq, bp));
+      }
+    }
+    Lv.n_exp_blocks = (int)eb.size();
+    CK(upload(h, &Lv.exp_blocks, eb));
+    CK(upload(h, &Lv.colbase, cb));
   }
   CK(upload(h, &Lv.cls_dev, Lv.cls));
   CK(upload(h, &Lv.tiles_dev, tiles));

@@ -69,6 +69,7 @@ struct PatchClass {
   long long rel_off;           // offset of this class's relidx table (cp entries)
   long long inv_off;           // offset of the class inverse (lda x lda)
   long long rexp_off;          // offset of the class block of the expanded residual (dense K2), -1 if unused
+  long long col_off;           // offset of the class's columns in the per-column gather-base table (expand_pull)
 };
 
 struct TileDesc {              // one CTA tile of the grouped patch GEMM: rows [m0, m0+BM), columns [n0, n0+nn)
@@ -131,6 +132,7 @@ std::vector<TileDesc> balanced_tiles(const std::vector<int>& cp, const std::vect
                                      int slots, int cn);
 // A matrices of the grouped GEMM: row-major lda x lda -> chunk-major swizzled (dst needs nmat*lda*lda + slack).
 cudaError_t launch_chunk_swizzle(const double* src, double* dst, int nmat, int lda, cudaStream_t s);
+constexpr int EXPAND_COLS = 32;      // patch columns per expand_pull block (x 16 slots = 512 elements)
 constexpr int kK2Slack = 224 * 16;   // doubles after the last chunk-major matrix (tile rows past lda)
 cudaError_t launch_patch_gemm(const LevelGeom& g, int r, int variant, const PatchClass* cls_dev, const TileDesc* tiles,
                               int ntiles, const int* relidx, const double* invc, int lda, const double* rvec,
@@ -146,6 +148,10 @@ cudaError_t launch_patch_gemm_dense(const LevelGeom& g, int variant, const Patch
                                     cudaStream_t s);
 int k2d_slots(int variant);
 // K1e: residual written in patch-expanded, class chunk-major swizzled form (B operand of the dense K2).
+// Rexp[class block, chunk q, column col, slot] = r[dof(patch col, mu_hat)] for a dense level, one thread per element
+// in Rexp order (coalesced stores); blocks = {class, chunk, first column, columns}, colbase[col_off + col] = (bq, bp)
+cudaError_t launch_expand_pull(const int4* blocks, int nblocks, const PatchClass* cls, const int* relidx,
+                               const int2* colbase, const double* r, double* rexp, cudaStream_t s);
 cudaError_t launch_gather_expand(const LevelGeom& g, int r, int k1, const double* Yc, const double* base, double alpha,
                                  double beta, int ldpm, const PatchClass* cls, double* rexp, cudaStream_t s);
 cudaError_t launch_load_cells(int d, int r, int k1, const LevelGeom& g, const LoadConsts* lc, int kind, double tn,

@@ -896,6 +896,58 @@ cudaError_t launch_chunk_swizzle(const double* src, double* dst, int nmat, int l
   return cudaGetLastError();
 }
 
+// Expanded residual for the dense K2 (pull form): every element of the class chunk-major, bank-swizzled block
+//   Rexp[rexp_off + q * ncols * 16 + col * 16 + pos],  mu_hat = 16 q + (pos XOR 4 (col mod 4)),
+// is r at the DoF of patch-local index mu_hat of patch column col (0 past C_P).  Threads run along Rexp, so the
+// stores are fully coalesced; the gather code of mu_hat and the column bases are static and fetched before the PDL
+// wait.  Replaces the push-form gather_expand (node threads scattering 8-byte stores into <= 3^d patch slots), whose
+// store request rate bounded it (cfg2 fine level: expansion 300 us on top of the node gather).
+// EXPAND_COLS (stgmg_internal.cuh) patch columns per block: 512 elements, 2 per thread
+
+constexpr int EXP_THREADS = 128, EXP_PER = EXPAND_COLS * 16 / EXP_THREADS;   // 4 elements (loads in flight) per thread
+
+__global__ void __launch_bounds__(EXP_THREADS) expand_pull_kernel(const int4* __restrict__ blocks,
+                                                                  const PatchClass* __restrict__ cls,
+                                                                  const int* __restrict__ relidx,
+                                                                  const int2* __restrict__ colbase,
+                                                                  const double* __restrict__ r,
+                                                                  double* __restrict__ rexp) {
+  pdl_trigger();
+  const int4 bd = blocks[blockIdx.x];   // class, chunk, first column, columns in this block
+  const PatchClass& pc = cls[bd.x];
+  const int cp = pc.cp, ncols = pc.ncols;
+  int src[EXP_PER];
+  long long dst[EXP_PER];
+#pragma unroll
+  for (int i = 0; i < EXP_PER; ++i) {
+    const int e = threadIdx.x + EXP_THREADS * i;
+    const int cl = e >> 4, pos = e & 15, col = bd.z + cl;
+    const int mu = bd.y * 16 + (pos ^ ((col & 3) << 2));
+    src[i] = -1;
+    dst[i] = -1;
+    if (cl < bd.w) {
+      dst[i] = pc.rexp_off + ((long long)bd.y * ncols + col) * 16 + pos;
+      if (mu < cp) {
+        const int code = __ldg(relidx + pc.rel_off + mu);
+        const int2 cb = __ldg(colbase + pc.col_off + col);
+        src[i] = (code >> 1) + ((code & 1) ? cb.y : cb.x);
+      }
+    }
+  }
+  pdl_wait();
+  double v[EXP_PER];
+#pragma unroll
+  for (int i = 0; i < EXP_PER; ++i) v[i] = src[i] >= 0 ? __ldg(r + src[i]) : 0.0;
+#pragma unroll
+  for (int i = 0; i < EXP_PER; ++i)
+    if (dst[i] >= 0) rexp[dst[i]] = v[i];
+}
+
+cudaError_t launch_expand_pull(const int4* blocks, int nblocks, const PatchClass* cls, const int* relidx,
+                               const int2* colbase, const double* r, double* rexp, cudaStream_t s) {
+  return launch_pdl(expand_pull_kernel, dim3(nblocks), dim3(EXP_THREADS), 0, s, blocks, cls, relidx, colbase, r, rexp);
+}
+
 // K3 (averaging update) lives in nodal.cu (node-mapped).
 
 // Multiplicative colour-ordered Vanka: the update d[Z(P)] += omega y_P of one colour's
