@@ -363,6 +363,11 @@ struct stgmg_handle {
   std::vector<LevelData> lev;
   double* A0inv = nullptr;
   int n0 = 0;
+  // folded coarse sub-cycle: the V-cycle restricted to levels <= fold_lv is a fixed linear map b_f -> d_f; it is
+  // assembled at setup (run on every unit vector) and applied as one GEMV (fold_ready once assembled)
+  int fold_lv = 0;
+  bool fold_ready = false;
+  double* Vfold = nullptr;
   cudaStream_t s = nullptr;
   bool own_stream = false;
   // Krylov workspace
@@ -646,23 +651,62 @@ static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_s
   return exchange(h, l, d);
 }
 
-static int enqueue_vcycle(stgmg_handle* h) {
-  const int L = h->L;
-  for (int l = L - 1; l >= 1; --l) {
-    LevelData& Lv = h->lev[l];
-    for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, l, Lv.b, Lv.d, j == 0));
-    CK(residual(h, l, Lv.b, Lv.d, Lv.r));
-    CK(restrict_level(h, l, Lv.r, h->lev[l - 1].b));
-    if (Lv.part && h->lev[l - 1].part) CK(exchange(h, l - 1, h->lev[l - 1].b));
-    else if (Lv.part) CK(agglomerate(h, l, h->lev[l - 1].b));
+// V-cycle on levels top..0: input lev[top].b, output lev[top].d.  Below the fold level the assembled
+// sub-cycle matrix replaces the recursion (same linear map, applied as one GEMV).
+static int enqueue_levels(stgmg_handle* h, int top) {
+  if (top == 0) {
+    CKE(launch_gemv(h->A0inv, h->n0, h->n0, h->lev[0].b, h->lev[0].d, h->s));
+    h->launches += 1;
+    return 0;
   }
-  CKE(launch_gemv(h->A0inv, h->n0, h->n0, h->lev[0].b, h->lev[0].d, h->s));
-  h->launches += 1;
-  for (int l = 1; l < L; ++l) {
-    LevelData& Lv = h->lev[l];
-    CK(prolong_level(h, l, h->lev[l - 1].d, Lv.d));
-    for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, l, Lv.b, Lv.d, false));
+  LevelData& Lv = h->lev[top];
+  if (h->fold_ready && top == h->fold_lv) {
+    CKE(launch_gemv(h->Vfold, (int)Lv.g.N, (int)Lv.g.N, Lv.b, Lv.d, h->s));
+    h->launches += 1;
+    return 0;
   }
+  for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, top, Lv.b, Lv.d, j == 0));
+  CK(residual(h, top, Lv.b, Lv.d, Lv.r));
+  CK(restrict_level(h, top, Lv.r, h->lev[top - 1].b));
+  if (Lv.part && h->lev[top - 1].part) CK(exchange(h, top - 1, h->lev[top - 1].b));
+  else if (Lv.part) CK(agglomerate(h, top, h->lev[top - 1].b));
+  CK(enqueue_levels(h, top - 1));
+  CK(prolong_level(h, top, h->lev[top - 1].d, Lv.d));
+  for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, top, Lv.b, Lv.d, false));
+  return 0;
+}
+
+static int enqueue_vcycle(stgmg_handle* h) { return enqueue_levels(h, h->L - 1); }
+
+// Assemble the folded sub-cycle: column i of Vfold (row-major, n x n) = the V-cycle of levels <= fold_lv applied to
+// e_i.  Chosen as the finest replicated level l >= 1 with n_l^2 doubles <= STGMG_FOLD_MB (64 MB by default; 0 = off).
+static int build_fold(stgmg_handle* h) {
+  long long budget = 64ll << 20;
+  if (const char* ev = std::getenv("STGMG_FOLD_MB")) budget = std::atoll(ev) << 20;
+  h->fold_lv = 0;
+  for (int l = 1; l < h->L - 1; ++l) {   // never the fine level (the Krylov operator's own smoother)
+    const long long n = h->lev[l].g.N;
+    if (!h->lev[l].part && n * n * (long long)sizeof(double) <= budget) h->fold_lv = l;
+  }
+  if (h->fold_lv == 0) return 0;
+  LevelData& F = h->lev[h->fold_lv];
+  const long long n = F.g.N;
+  CK(dalloc(h, &h->Vfold, (size_t)(n * n)));
+  double* one = nullptr;
+  CK(dalloc(h, &one, 1));
+  const double v1 = 1.0;
+  CKE(cudaMemcpy(one, &v1, sizeof(double), cudaMemcpyHostToDevice));
+  const long long before = h->launches;
+  for (long long i = 0; i < n; ++i) {
+    CKE(cudaMemsetAsync(F.b, 0, sizeof(double) * n, h->s));
+    CKE(cudaMemcpyAsync(F.b + i, one, sizeof(double), cudaMemcpyDeviceToDevice, h->s));
+    CK(enqueue_levels(h, h->fold_lv));
+    CKE(cudaMemcpy2DAsync(h->Vfold + i, sizeof(double) * n, F.d, sizeof(double), sizeof(double), (size_t)n,
+                          cudaMemcpyDeviceToDevice, h->s));
+  }
+  CKE(cudaStreamSynchronize(h->s));
+  h->launches = before;
+  h->fold_ready = true;
   return 0;
 }
 
@@ -1748,6 +1792,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   CKE(cudaMallocHost(&h->pinned, 16 * sizeof(double)));
   CKE(cudaEventCreate(&h->e0));
   CKE(cudaEventCreate(&h->e1));
+  CK(build_fold(h.get()));
   if (h->graphable) CK(capture_vcycle(h.get()));
   CKE(cudaStreamSynchronize(h->s));
   *out = h.release();

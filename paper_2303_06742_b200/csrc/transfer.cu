@@ -2,7 +2,8 @@
 //   prolongation by interpolation, restriction by the transpose.  Per (Radau node, field, component)
 //   the prolongation is the tensor product of 1D interpolation matrices (coarse Q_r / Q_{r-1} Lagrange basis at
 //   the fine nodes), stored as per-axis CSR tables; no temporal coarsening (reading A15).
-//   direct solve on T_0 = one GEMV with the equilibrated explicit inverse (readings A16, A18).
+//   direct solve on T_0 = one GEMV with the equilibrated explicit inverse (readings A16, A18); the same GEMV
+//   applies the assembled coarse sub-cycle (api.cu build_fold).
 #include "stgmg_internal.cuh"
 
 namespace stgmg {
@@ -19,6 +20,7 @@ __global__ void gemv_kernel(const double* __restrict__ A, int n, int lda, const 
   if (row >= n) return;
   const double* a = A + (long long)row * lda;
   double s = 0.0;
+#pragma unroll 4
   for (int j = lane; j < n; j += 32) s = fma(a[j], x[j], s);
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) y[row] = s;
