@@ -30,6 +30,11 @@ cudaError_t launch_mgs_dot(double* w, const double* vprev, const double* hprev, 
 cudaError_t launch_sqrt(double* v, cudaStream_t s);
 cudaError_t launch_scale(double* y, const double* x, const double* sc, int invert, long long n, cudaStream_t s);
 cudaError_t launch_givens(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, cudaStream_t s);
+cudaError_t launch_givens_cond(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, int* ctl,
+                               int has_next, cudaGraphConditionalHandle next, cudaStream_t s);
+cudaError_t launch_backsub_ctl(const double* H, int ldh, const double* gv, double* y, const int* ctl, cudaStream_t s);
+cudaError_t launch_update_x_ctl(double* x, const double* Z, const double* y, const int* ctl, long long n,
+                                cudaStream_t s);
 cudaError_t launch_backsub(const double* H, int ldh, const double* gv, double* y, int jn, cudaStream_t s);
 cudaError_t launch_update_x(double* x, const double* Z, const double* y, int jn, long long n, cudaStream_t s);
 cudaError_t launch_set_scalar(double* dst, const double* src, cudaStream_t s);
@@ -367,6 +372,18 @@ struct stgmg_handle {
   // assembled at setup (run on every unit vector) and applied as one GEMV (fold_ready once assembled)
   int fold_lv = 0;
   bool fold_ready = false;
+  // device-resident Arnoldi loop (single GPU): one graph per restart length m, an IF node per step whose handle the
+  // previous step's Givens kernel sets (no host round trip per step)
+  cudaGraphExec_t cyc_exec = nullptr;
+  int cyc_m = 0;
+  // Opt-in (STGMG_SOLVE_GRAPH=1; 2 = V-cycle kernels captured into each step instead of a child graph): measured
+  // SLOWER on cfg1 (solve 2.81 -> 3.09 ms): once a graph with conditional nodes is loaded, every launch on the stream,
+  // the plain V-cycle graph included, runs about 40 us per V-cycle slower, more than the per-step host round trip
+  // (about 36 us) it removes.  Default: the host-checked loop.
+  bool cyc_off = true;           // off by default, or the graph could not be built
+  bool cyc_inline = false;
+  std::vector<int> cyc_step_launches;
+  int* ctl = nullptr;            // [0] Arnoldi steps of the solve, [1] steps of the current cycle
   double* Vfold = nullptr;
   cudaStream_t s = nullptr;
   bool own_stream = false;
@@ -378,6 +395,7 @@ struct stgmg_handle {
   double* pinned = nullptr;
   double *stage_rhs = nullptr, *stage_x = nullptr, *rhs_int = nullptr;
   cudaGraphExec_t vgraph = nullptr;
+  cudaGraph_t vgraph_tmpl = nullptr;
   int vgraph_launches = 0;
   long long launches = 0;
   std::vector<void*> allocs;
@@ -1518,7 +1536,7 @@ static int capture_vcycle(stgmg_handle* h) {
   if (rc) return rc;
   CKE(e);
   CKE(cudaGraphInstantiate(&h->vgraph, graph, 0));
-  CKE(cudaGraphDestroy(graph));
+  h->vgraph_tmpl = graph;   // kept: the device-resident FGMRES embeds it as a child graph
   h->vgraph_launches = (int)(h->launches - before);
   h->launches = before;
   return 0;
@@ -1793,6 +1811,11 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   CKE(cudaEventCreate(&h->e0));
   CKE(cudaEventCreate(&h->e1));
   CK(build_fold(h.get()));
+  if (const char* ev = std::getenv("STGMG_SOLVE_GRAPH")) {   // experiment, see cyc_off
+    h->cyc_off = std::atoi(ev) == 0;
+    h->cyc_inline = std::atoi(ev) == 2;
+  }
+  CK(dalloc(h.get(), &h->ctl, 2));
   if (h->graphable) CK(capture_vcycle(h.get()));
   CKE(cudaStreamSynchronize(h->s));
   *out = h.release();
@@ -1803,6 +1826,8 @@ int stgmg_destroy(stgmg_handle* h) {
   if (!h) return 0;
   cudaStreamSynchronize(h->s);
   if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
+  if (h->cyc_exec) cudaGraphExecDestroy(h->cyc_exec);
+  if (h->vgraph_tmpl) cudaGraphDestroy(h->vgraph_tmpl);
   for (void* p : h->allocs) cudaFree(p);
   delete h->tr;
   if (h->pinned) cudaFreeHost(h->pinned);
@@ -2008,6 +2033,112 @@ int stgmg_energy(stgmg_handle* h, const double* x, double* energy) {
   return 0;
 }
 
+// One Arnoldi step j of FGMRES (O11): z_j = V-cycle(v_j), w = A z_j, MGS against v_0..v_j, ||w||, Givens, v_{j+1}.
+// cond: capture mode of the device-resident loop (V-cycle enqueued as kernels, Givens decides step j + 1).
+static int enqueue_arnoldi_step(stgmg_handle* h, int j, int m, bool cond, cudaGraphConditionalHandle next) {
+  const int Lf = h->L - 1, ldh = m + 1;
+  const long long N = h->lev[Lf].g.N;
+  double* vj = h->V + (long long)j * N;
+  double* zj = h->Z + (long long)j * N;
+  if (cond) {
+    LevelData& F = h->lev[Lf];
+    CKE(cudaMemcpyAsync(F.b, vj, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->s));
+    if (h->vgraph_tmpl && !h->cyc_inline) {   // the V-cycle graph as a child node of the capture
+      cudaStreamCaptureStatus st;
+      cudaGraph_t cg;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndep = 0;
+      CKE(cudaStreamGetCaptureInfo(h->s, &st, nullptr, &cg, &deps, &ndep));
+      cudaGraphNode_t child;
+      CKE(cudaGraphAddChildGraphNode(&child, cg, deps, ndep, h->vgraph_tmpl));
+      CKE(cudaStreamUpdateCaptureDependencies(h->s, &child, 1, cudaStreamSetCaptureDependencies));
+      h->launches += h->vgraph_launches;
+    } else {
+      CK(enqueue_vcycle(h));
+    }
+    CKE(cudaMemcpyAsync(zj, F.d, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->s));
+  } else {
+    CK(vcycle_dev(h, vj, zj));                                          // z_j = M^{-1} v_j
+  }
+  CK(apply_level(h, Lf, zj, h->w, nullptr, 1.0, 0.0));                 // w = A z_j
+  double* hcol = h->H + (long long)j * ldh;
+  for (int i = 0; i <= j; ++i)                                         // modified Gram–Schmidt
+    CK(dot(h, h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
+           h->V + (long long)i * N, hcol + i, false));
+  CK(dot(h, h->w, h->V + (long long)j * N, hcol + j, nullptr, hcol + j + 1, true));
+  if (cond) CKE(launch_givens_cond(h->H, ldh, h->cs, h->sn, h->gv, j, h->scal, h->ctl, j + 1 < m ? 1 : 0, next, h->s));
+  else CKE(launch_givens(h->H, ldh, h->cs, h->sn, h->gv, j, h->scal, h->s));
+  CKE(launch_scale(h->V + (long long)(j + 1) * N, h->w, h->scal + 1, 1, N, h->s));   // v_{j+1} = w / h_{j+1,j}
+  h->launches += 2;
+  return exchange(h, Lf, h->V + (long long)(j + 1) * N);
+}
+
+// The device-resident restart cycle: a graph of m IF nodes in a chain, node j's body = Arnoldi step j (captured
+// with cudaStreamBeginCaptureToGraph); handle j defaults to (j == 0) at every launch and is set by step j - 1's
+// Givens kernel.  Single GPU only (the x-slab decomposition's NCCL exchanges stay on the host loop).
+static int build_cycle_graph(stgmg_handle* h, int m) {
+  if (h->cyc_exec && h->cyc_m == m) return 0;
+  if (h->cyc_exec) {
+    cudaGraphExecDestroy(h->cyc_exec);
+    h->cyc_exec = nullptr;
+  }
+  cudaGraph_t G;
+  CKE(cudaGraphCreate(&G, 0));
+  std::vector<cudaGraphConditionalHandle> hd(m);
+  int rc = 0;
+  for (int j = 0; j < m && !rc; ++j)
+    if (cudaGraphConditionalHandleCreate(&hd[j], G, j == 0 ? 1u : 0u, cudaGraphCondAssignDefault) != cudaSuccess) {
+      set_error("cudaGraphConditionalHandleCreate failed");
+      rc = STGMG_ECUDA;
+    }
+  cudaGraphNode_t prev = nullptr;
+  const long long before = h->launches;
+  h->cyc_step_launches.assign(m, 0);
+  for (int j = 0; j < m && !rc; ++j) {
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = hd[j];
+    np.conditional.type = cudaGraphCondTypeIf;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (cudaGraphAddNode(&node, G, prev ? &prev : nullptr, prev ? 1 : 0, &np) != cudaSuccess) {
+      set_error("cudaGraphAddNode (conditional) failed");
+      rc = STGMG_ECUDA;
+      break;
+    }
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    if (cudaStreamBeginCaptureToGraph(h->s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+        cudaSuccess) {
+      set_error("cudaStreamBeginCaptureToGraph failed");
+      rc = STGMG_ECUDA;
+      break;
+    }
+    const long long l0 = h->launches;
+    rc = enqueue_arnoldi_step(h, j, m, true, j + 1 < m ? hd[j + 1] : hd[j]);
+    h->cyc_step_launches[j] = (int)(h->launches - l0);
+    cudaGraph_t out = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(h->s, &out);
+    if (!rc && e != cudaSuccess) {
+      set_error(std::string("capture of an Arnoldi step: ") + cudaGetErrorString(e));
+      rc = STGMG_ECUDA;
+    }
+    prev = node;
+  }
+  h->launches = before;
+  if (!rc) {
+    const cudaError_t e = cudaGraphInstantiate(&h->cyc_exec, G, 0);
+    if (e != cudaSuccess) {
+      set_error(std::string("cudaGraphInstantiate (Arnoldi cycle): ") + cudaGetErrorString(e));
+      h->cyc_exec = nullptr;
+      rc = STGMG_ECUDA;
+    }
+  }
+  cudaGraphDestroy(G);
+  cudaGetLastError();
+  if (!rc) h->cyc_m = m;
+  return rc;
+}
+
 int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int tol_mode, int restart, int maxit,
                 stgmg_stats* stats) {
   if (!h || !rhs || !x || restart < 1 || maxit < 1 || !(tol > 0)) { set_error("bad argument"); return STGMG_EINVAL; }
@@ -2016,6 +2147,13 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
   const LevelGeom& g = h->lev[Lf].g;
   const long long N = g.N;
   const int m = restart, ldh = m + 1;
+  bool graph_ok = h->nranks == 1 && h->graphable && !h->cyc_off;
+  if (graph_ok && build_cycle_graph(h, m)) {   // not buildable here: the host-checked loop
+    if (std::getenv("STGMG_DEBUG")) std::fprintf(stderr, "stgmg: device-resident FGMRES off: %s\n", g_last_error.c_str());
+    h->cyc_off = true;
+    graph_ok = false;
+    cudaGetLastError();
+  }
   h->launches = 0;
   double* scal = h->scal;     // [0] |g_{j+1}|, [1] h_{j+1,j}, [2] beta, [3] ||b||
   double* hp = h->pinned;
@@ -2036,6 +2174,14 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
   const double target = tol_mode == STGMG_TOL_ABS ? tol : tol * bnorm;
   int its = 0, restarts = 0;
   bool converged = beta <= target;
+  int* hctl = reinterpret_cast<int*>(hp + 14);
+  const bool use_graph = graph_ok && !converged;
+  if (use_graph) {   // target, maxit and the step counter of the device loop
+    hp[4] = target;
+    hp[5] = (double)maxit;
+    CKE(cudaMemcpyAsync(scal + 4, hp + 4, 2 * sizeof(double), cudaMemcpyHostToDevice, h->s));
+    CKE(cudaMemsetAsync(h->ctl, 0, 2 * sizeof(int), h->s));
+  }
   while (!converged && its < maxit) {
     CKE(launch_scale(h->V, h->rv, scal + 2, 1, N, h->s));                 // v_0 = r / beta
     CK(exchange(h, Lf, h->V));
@@ -2044,20 +2190,27 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
     CKE(cudaMemsetAsync(h->H, 0, sizeof(double) * ldh * m, h->s));
     h->launches += 2;
     int jdone = 0;
-    for (int j = 0; j < m; ++j) {
-      double* vj = h->V + (long long)j * N;
-      double* zj = h->Z + (long long)j * N;
-      CK(vcycle_dev(h, vj, zj));                                          // z_j = M^{-1} v_j
-      CK(apply_level(h, Lf, zj, h->w, nullptr, 1.0, 0.0));               // w = A z_j
-      double* hcol = h->H + (long long)j * ldh;
-      for (int i = 0; i <= j; ++i)                                        // modified Gram–Schmidt
-        CK(dot(h, h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
-               h->V + (long long)i * N, hcol + i, false));
-      CK(dot(h, h->w, h->V + (long long)j * N, hcol + j, nullptr, hcol + j + 1, true));
-      CKE(launch_givens(h->H, ldh, h->cs, h->sn, h->gv, j, scal, h->s));
-      CKE(launch_scale(h->V + (long long)(j + 1) * N, h->w, scal + 1, 1, N, h->s));   // v_{j+1} = w / h_{j+1,j}
+    if (use_graph) {   // the whole cycle on the device: the Givens kernels chain the steps
+      CKE(cudaGraphLaunch(h->cyc_exec, h->s));
+      CKE(launch_backsub_ctl(h->H, ldh, h->gv, h->yv, h->ctl, h->s));
+      CKE(launch_update_x_ctl(x, h->Z, h->yv, h->ctl, N, h->s));
       h->launches += 2;
-      CK(exchange(h, Lf, h->V + (long long)(j + 1) * N));
+      CK(residual(h, Lf, rhs, x, h->rv));
+      CK(dot(h, h->rv, nullptr, nullptr, nullptr, scal + 2, true));
+      CKE(cudaMemcpyAsync(hp + 2, scal + 2, sizeof(double), cudaMemcpyDeviceToHost, h->s));
+      CKE(cudaMemcpyAsync(hctl, h->ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->s));
+      CKE(cudaStreamSynchronize(h->s));
+      jdone = hctl[1];
+      for (int j = 0; j < jdone; ++j) h->launches += h->cyc_step_launches[j];
+      its = hctl[0];
+      beta = hp[2];
+      if (beta <= target) { converged = true; break; }
+      if (its >= maxit) break;
+      ++restarts;
+      continue;
+    }
+    for (int j = 0; j < m; ++j) {
+      CK(enqueue_arnoldi_step(h, j, m, false, cudaGraphConditionalHandle()));
       CKE(cudaMemcpyAsync(hp, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
       CKE(cudaStreamSynchronize(h->s));
       ++its;

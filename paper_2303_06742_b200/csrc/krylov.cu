@@ -121,6 +121,71 @@ cudaError_t launch_givens(double* H, int ldh, double* cs, double* sn, double* gv
   return cudaGetLastError();
 }
 
+// Device-resident Arnoldi loop (one CUDA graph per restart cycle, one IF node per step j): the Givens step of column
+// j also counts the step (ctl[0]: Arnoldi steps of the solve, ctl[1]: steps of this cycle = j + 1) and decides, with
+// the host loop's test (|g_{j+1}| <= target, breakdown h_{j+1,j} <= 1e-14 beta_cycle, maxit; scal[4] = target,
+// scal[5] = maxit, scal[2] = beta_cycle), whether step j + 1 runs: cudaGraphSetConditional on its IF node's handle.
+__global__ void givens_cond_kernel(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, int* ctl,
+                                   int has_next, cudaGraphConditionalHandle next) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double* h = H + (long long)j * ldh;
+  const double hn = h[j + 1];
+  for (int i = 0; i < j; ++i) {
+    const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double rho = hypot(h[j], hn);
+  cs[j] = h[j] / rho;
+  sn[j] = hn / rho;
+  h[j] = rho;
+  h[j + 1] = 0.0;
+  gv[j + 1] = -sn[j] * gv[j];
+  gv[j] = cs[j] * gv[j];
+  scal[0] = fabs(gv[j + 1]);
+  scal[1] = hn;
+  const int its = ctl[0] + 1;
+  ctl[0] = its;
+  ctl[1] = j + 1;
+  const bool stop = scal[0] <= scal[4] || hn <= 1e-14 * scal[2] || its >= (int)scal[5];
+  if (has_next) cudaGraphSetConditional(next, stop ? 0u : 1u);
+}
+cudaError_t launch_givens_cond(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, int* ctl,
+                               int has_next, cudaGraphConditionalHandle next, cudaStream_t s) {
+  givens_cond_kernel<<<1, 32, 0, s>>>(H, ldh, cs, sn, gv, j, scal, ctl, has_next, next);
+  return cudaGetLastError();
+}
+// Back substitution and x update with the step count of the cycle read from the device (ctl[1]).
+__global__ void backsub_ctl_kernel(const double* H, int ldh, const double* gv, double* y, const int* ctl) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int jn = ctl[1];
+  for (int i = jn - 1; i >= 0; --i) {
+    double s = gv[i];
+    for (int l = i + 1; l < jn; ++l) s -= H[(long long)l * ldh + i] * y[l];
+    y[i] = s / H[(long long)i * ldh + i];
+  }
+}
+cudaError_t launch_backsub_ctl(const double* H, int ldh, const double* gv, double* y, const int* ctl, cudaStream_t s) {
+  backsub_ctl_kernel<<<1, 32, 0, s>>>(H, ldh, gv, y, ctl);
+  return cudaGetLastError();
+}
+__global__ void update_x_ctl_kernel(double* __restrict__ x, const double* __restrict__ Z, const double* __restrict__ y,
+                                    const int* __restrict__ ctl, long long n) {
+  pdl_trigger();
+  pdl_wait();
+  const int jn = ctl[1];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = x[i];
+    for (int j = 0; j < jn; ++j) s = fma(y[j], Z[(long long)j * n + i], s);
+    x[i] = s;
+  }
+}
+cudaError_t launch_update_x_ctl(double* x, const double* Z, const double* y, const int* ctl, long long n,
+                                cudaStream_t s) {
+  return launch_pdl(update_x_ctl_kernel, dim3(RED_BLOCKS), dim3(RED_THREADS), 0, s, x, Z, y, ctl, n);
+}
+
 // Back substitution H(0:jn,0:jn) y = g(0:jn).
 __global__ void backsub_kernel(const double* H, int ldh, const double* gv, double* y, int jn) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
