@@ -109,3 +109,47 @@ def test_nonzero_initial_guess_matches_oracle(pair):
     xo, info = fgmres(lambda v: H.A[-1] @ v, bn, H.vcycle, x0=x0, tol=cfg["rtol"], restart=cfg["restart"])
     assert st["converged"] and abs(st["iterations"] - info["iterations"]) <= 1
     assert np.linalg.norm(to_np(x) - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def test_zero_rhs_and_exact_initial_guess(pair):
+    """Degenerate inputs: b = 0 returns at once (0 iterations, x = 0); an initial guess that already meets the
+    tolerance returns at once with x unchanged (O11 step 1: beta <= target before any Arnoldi step)."""
+    import torch
+    cfg, s, H = pair
+    N = H.fine.N
+    b = torch.zeros(N, dtype=torch.float64, device="cuda")
+    x = torch.zeros_like(b)
+    st = s.solve(b, x, tol=cfg["rtol"], restart=cfg["restart"])
+    torch.cuda.synchronize()
+    assert st["converged"] and st["iterations"] == 0 and torch.count_nonzero(x).item() == 0
+    bn = to_gpu(uniform_load(N, 97))
+    x = torch.zeros_like(bn)
+    s.solve(bn, x, tol=1e-12, restart=cfg["restart"])
+    x1 = x.clone()
+    st = s.solve(bn, x, tol=1e-8, restart=cfg["restart"])
+    torch.cuda.synchronize()
+    assert st["converged"] and st["iterations"] == 0
+    assert torch.equal(x, x1)
+
+
+def test_single_level_is_a_direct_solve():
+    """levels = 1: the preconditioner is the coarse direct solve A_0^{-1} (readings A16/A18), so FGMRES
+    converges in one iteration (exact preconditioner -> 1 iteration) to the oracle's dense solve."""
+    import torch
+    from paper_2303_06742_b200 import Solver
+    from stgmg_inputs import config
+    from oracle.mg import Hierarchy
+    from tests.gpu_common import oracle_params
+    cfg = dict(config(0), levels=1)
+    s = Solver(cfg)
+    d = cfg["dim"]
+    H = Hierarchy(d, cfg["cells"][:d], cfg["lo"][:d], cfg["hi"][:d], cfg["r"], cfg["k"], 1, oracle_params(cfg),
+                  cfg["tau"], bc_u=list(cfg["bc_u"][:2 * d]), bc_p=list(cfg["bc_p"][:2 * d]))
+    bn = uniform_load(H.fine.N, 98)
+    x = torch.zeros(H.fine.N, dtype=torch.float64, device="cuda")
+    st = s.solve(to_gpu(bn), x, tol=1e-10, restart=30)
+    torch.cuda.synchronize()
+    xd = np.linalg.solve(H.A[-1].toarray() if hasattr(H.A[-1], "toarray") else H.A[-1], bn)
+    assert st["converged"] and st["iterations"] == 1
+    assert np.linalg.norm(to_np(x) - xd) <= 1e-9 * np.linalg.norm(xd)
+    s.close()
