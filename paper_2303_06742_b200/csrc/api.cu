@@ -411,7 +411,7 @@ struct stgmg_handle {
   int rank = 0, nranks = 1;
   unsigned char* mask = nullptr;   // owned fine-level DoFs (Krylov inner products)
   bool graphable = true;
-  bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; 2D by choice)
+  bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; large 2D elements)
   int nsm = 148;                   // SMs of the device (tile balancing)
 };
 
@@ -1781,7 +1781,9 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       CKE(cudaMemcpy(h->lc_dev, &lc, sizeof(LoadConsts), cudaMemcpyHostToDevice));
     }
     if (d == 2) CK(dalloc(h.get(), &h->Yc, (size_t)(cell_count(h->lev[levels - 1].g) * elem_dofs(h.get()))));
-    h->op_gemm = d == 3;
+    // 2D: the register kernel on small elements (cfg1, 80 DoFs: K1 9.5 vs 13.8 us), the element GEMM on large ones
+    // (cfg2, r = 3, k = 2, 219 DoFs: fine-level K1 357 -> 303 us, V-cycle 27.0 -> 26.0 ms)
+    h->op_gemm = d == 3 || elem_dofs(h.get()) >= 128;
     if (d == 2)
       if (const char* ev = std::getenv("STGMG_OP2D_GEMM")) h->op_gemm = std::atoi(ev) != 0;
     if (h->op_gemm) {
