@@ -383,6 +383,10 @@ struct stgmg_handle {
   bool cyc_off = true;           // off by default, or the graph could not be built
   bool cyc_inline = false;
   std::vector<int> cyc_step_launches;
+  // STGMG_PROFILE_SOLVE=1: device timestamps of the phases of each Arnoldi step, printed after the solve
+  bool prof = false;
+  cudaEvent_t pev[64] = {};
+  int npev = 0;
   int* ctl = nullptr;            // [0] Arnoldi steps of the solve, [1] steps of the current cycle
   double* Vfold = nullptr;
   cudaStream_t s = nullptr;
@@ -396,6 +400,12 @@ struct stgmg_handle {
   double *stage_rhs = nullptr, *stage_x = nullptr, *rhs_int = nullptr;
   cudaGraphExec_t vgraph = nullptr;
   cudaGraph_t vgraph_tmpl = nullptr;
+  // V-cycle graphs of the Arnoldi steps with the fine level's b / d bound to v_j / z_j (captured at first use): no
+  // copies of v_j in and z_j out around each preconditioner application.  STGMG_STEP_GRAPHS=0: the copying form.
+  std::vector<cudaGraphExec_t> vg_step;
+  std::vector<int> vg_step_launches;
+  int vg_step_m = 0;
+  bool step_graphs = true;
   int vgraph_launches = 0;
   long long launches = 0;
   std::vector<void*> allocs;
@@ -1544,6 +1554,11 @@ static int capture_vcycle(stgmg_handle* h) {
 
 static int ensure_krylov(stgmg_handle* h, int m) {
   if (m <= h->m_alloc) return 0;
+  for (auto& g : h->vg_step)   // bound to the old basis
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
   const long long N = h->lev[h->L - 1].g.N;
   CK(dalloc(h, &h->V, (size_t)(m + 1) * N));
   CK(dalloc(h, &h->Z, (size_t)m * N));
@@ -1813,6 +1828,11 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   CKE(cudaEventCreate(&h->e0));
   CKE(cudaEventCreate(&h->e1));
   CK(build_fold(h.get()));
+  if (const char* ev = std::getenv("STGMG_STEP_GRAPHS")) h->step_graphs = std::atoi(ev) != 0;
+  if (std::getenv("STGMG_PROFILE_SOLVE")) {
+    h->prof = true;
+    for (auto& e : h->pev) CKE(cudaEventCreate(&e));
+  }
   if (const char* ev = std::getenv("STGMG_SOLVE_GRAPH")) {   // experiment, see cyc_off
     h->cyc_off = std::atoi(ev) == 0;
     h->cyc_inline = std::atoi(ev) == 2;
@@ -1830,6 +1850,8 @@ int stgmg_destroy(stgmg_handle* h) {
   if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
   if (h->cyc_exec) cudaGraphExecDestroy(h->cyc_exec);
   if (h->vgraph_tmpl) cudaGraphDestroy(h->vgraph_tmpl);
+  for (auto g : h->vg_step)
+    if (g) cudaGraphExecDestroy(g);
   for (void* p : h->allocs) cudaFree(p);
   delete h->tr;
   if (h->pinned) cudaFreeHost(h->pinned);
@@ -2035,15 +2057,35 @@ int stgmg_energy(stgmg_handle* h, const double* x, double* energy) {
   return 0;
 }
 
-// One Arnoldi step j of FGMRES (O11): z_j = V-cycle(v_j), w = A z_j, MGS against v_0..v_j, ||w||, Givens, v_{j+1}.
-// cond: capture mode of the device-resident loop (V-cycle enqueued as kernels, Givens decides step j + 1).
-static int enqueue_arnoldi_step(stgmg_handle* h, int j, int m, bool cond, cudaGraphConditionalHandle next) {
+// The part of Arnoldi step j after the preconditioner: w = A z_j, MGS against v_0..v_j, ||w||, Givens, v_{j+1}.
+static int arnoldi_tail(stgmg_handle* h, int j, int m, bool cond, cudaGraphConditionalHandle next) {
   const int Lf = h->L - 1, ldh = m + 1;
+  const long long N = h->lev[Lf].g.N;
+  double* zj = h->Z + (long long)j * N;
+  CK(apply_level(h, Lf, zj, h->w, nullptr, 1.0, 0.0));                 // w = A z_j
+  double* hcol = h->H + (long long)j * ldh;
+  for (int i = 0; i <= j; ++i)                                         // modified Gram–Schmidt
+    CK(dot(h, h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
+           h->V + (long long)i * N, hcol + i, false));
+  CK(dot(h, h->w, h->V + (long long)j * N, hcol + j, nullptr, hcol + j + 1, true));
+  if (cond) CKE(launch_givens_cond(h->H, ldh, h->cs, h->sn, h->gv, j, h->scal, h->ctl, j + 1 < m ? 1 : 0, next, h->s));
+  else CKE(launch_givens(h->H, ldh, h->cs, h->sn, h->gv, j, h->scal, h->s));
+  CKE(launch_scale(h->V + (long long)(j + 1) * N, h->w, h->scal + 1, 1, N, h->s));   // v_{j+1} = w / h_{j+1,j}
+  h->launches += 2;
+  return exchange(h, Lf, h->V + (long long)(j + 1) * N);
+}
+
+// One Arnoldi step j of FGMRES (O11): z_j = V-cycle(v_j), then arnoldi_tail.  Single GPU: the whole step is one
+// CUDA graph captured at first use with the fine level's right-hand side / iterate bound to v_j / z_j (no copies
+// around the preconditioner, programmatic dependent launch across the V-cycle / apply / MGS boundary).
+// cond: capture mode of the device-resident loop (V-cycle as a child graph, Givens decides step j + 1).
+static int enqueue_arnoldi_step(stgmg_handle* h, int j, int m, bool cond, cudaGraphConditionalHandle next) {
+  const int Lf = h->L - 1;
   const long long N = h->lev[Lf].g.N;
   double* vj = h->V + (long long)j * N;
   double* zj = h->Z + (long long)j * N;
+  LevelData& F = h->lev[Lf];
   if (cond) {
-    LevelData& F = h->lev[Lf];
     CKE(cudaMemcpyAsync(F.b, vj, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->s));
     if (h->vgraph_tmpl && !h->cyc_inline) {   // the V-cycle graph as a child node of the capture
       cudaStreamCaptureStatus st;
@@ -2059,20 +2101,48 @@ static int enqueue_arnoldi_step(stgmg_handle* h, int j, int m, bool cond, cudaGr
       CK(enqueue_vcycle(h));
     }
     CKE(cudaMemcpyAsync(zj, F.d, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->s));
-  } else {
-    CK(vcycle_dev(h, vj, zj));                                          // z_j = M^{-1} v_j
+    return arnoldi_tail(h, j, m, true, next);
   }
-  CK(apply_level(h, Lf, zj, h->w, nullptr, 1.0, 0.0));                 // w = A z_j
-  double* hcol = h->H + (long long)j * ldh;
-  for (int i = 0; i <= j; ++i)                                         // modified Gram–Schmidt
-    CK(dot(h, h->w, i > 0 ? h->V + (long long)(i - 1) * N : nullptr, i > 0 ? hcol + (i - 1) : nullptr,
-           h->V + (long long)i * N, hcol + i, false));
-  CK(dot(h, h->w, h->V + (long long)j * N, hcol + j, nullptr, hcol + j + 1, true));
-  if (cond) CKE(launch_givens_cond(h->H, ldh, h->cs, h->sn, h->gv, j, h->scal, h->ctl, j + 1 < m ? 1 : 0, next, h->s));
-  else CKE(launch_givens(h->H, ldh, h->cs, h->sn, h->gv, j, h->scal, h->s));
-  CKE(launch_scale(h->V + (long long)(j + 1) * N, h->w, h->scal + 1, 1, N, h->s));   // v_{j+1} = w / h_{j+1,j}
-  h->launches += 2;
-  return exchange(h, Lf, h->V + (long long)(j + 1) * N);
+  if (h->vgraph && h->step_graphs && h->nranks == 1) {
+    if (h->vg_step_m != m) {   // H's leading dimension is m + 1: graphs of another restart length are stale
+      for (auto& g : h->vg_step)
+        if (g) {
+          cudaGraphExecDestroy(g);
+          g = nullptr;
+        }
+      h->vg_step_m = m;
+    }
+    if ((int)h->vg_step.size() <= j) {
+      h->vg_step.resize(j + 1, nullptr);
+      h->vg_step_launches.resize(j + 1, 0);
+    }
+    if (!h->vg_step[j]) {
+      double* b0 = F.b;
+      double* d0 = F.d;
+      cudaGraph_t graph;
+      const long long before = h->launches;
+      CKE(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+      F.b = vj;
+      F.d = zj;
+      int rc = enqueue_vcycle(h);
+      F.b = b0;
+      F.d = d0;
+      if (!rc) rc = arnoldi_tail(h, j, m, false, cudaGraphConditionalHandle());
+      cudaError_t e = cudaStreamEndCapture(h->s, &graph);
+      h->vg_step_launches[j] = (int)(h->launches - before);
+      h->launches = before;
+      if (rc) return rc;
+      CKE(e);
+      e = cudaGraphInstantiate(&h->vg_step[j], graph, 0);
+      cudaGraphDestroy(graph);
+      CKE(e);
+    }
+    CKE(cudaGraphLaunch(h->vg_step[j], h->s));
+    h->launches += h->vg_step_launches[j];
+    return 0;
+  }
+  CK(vcycle_dev(h, vj, zj));                                          // z_j = M^{-1} v_j
+  return arnoldi_tail(h, j, m, false, cudaGraphConditionalHandle());
 }
 
 // The device-resident restart cycle: a graph of m IF nodes in a chain, node j's body = Arnoldi step j (captured
@@ -2212,7 +2282,9 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
       continue;
     }
     for (int j = 0; j < m; ++j) {
+      if (h->prof) CKE(cudaEventRecord(h->pev[h->npev++ % 64], h->s));
       CK(enqueue_arnoldi_step(h, j, m, false, cudaGraphConditionalHandle()));
+      if (h->prof) CKE(cudaEventRecord(h->pev[h->npev++ % 64], h->s));
       CKE(cudaMemcpyAsync(hp, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
       CKE(cudaStreamSynchronize(h->s));
       ++its;
@@ -2235,6 +2307,21 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
   CKE(cudaEventSynchronize(h->e1));
   float ms = 0.f;
   CKE(cudaEventElapsedTime(&ms, h->e0, h->e1));
+  if (h->prof && h->npev >= 2 && h->npev <= 64) {   // per Arnoldi step: device time, then the gap to the next step
+    float t = 0.f;
+    std::fprintf(stderr, "stgmg solve profile (us):");
+    cudaEventElapsedTime(&t, h->e0, h->pev[0]);
+    std::fprintf(stderr, " start->step0 %.1f;", t * 1e3f);
+    for (int i = 0; i + 1 < h->npev; i += 2) {
+      float a = 0.f, g = 0.f;
+      cudaEventElapsedTime(&a, h->pev[i], h->pev[i + 1]);
+      if (i + 2 < h->npev) cudaEventElapsedTime(&g, h->pev[i + 1], h->pev[i + 2]);
+      else cudaEventElapsedTime(&g, h->pev[i + 1], h->e1);
+      std::fprintf(stderr, " | step %.1f next %.1f", a * 1e3f, g * 1e3f);
+    }
+    std::fprintf(stderr, "\n");
+  }
+  h->npev = 0;
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
     stats->iterations = its;
@@ -2341,6 +2428,23 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
   CKE(cudaEventSynchronize(h->e1));
   float ms = 0.f;
   CKE(cudaEventElapsedTime(&ms, h->e0, h->e1));
+  if (h->prof && h->npev >= 4 && h->npev <= 64) {   // per step: [gap] vcycle | apply | MGS + Givens + scale
+    float t = 0.f;
+    std::fprintf(stderr, "stgmg solve profile (us):");
+    cudaEventElapsedTime(&t, h->e0, h->pev[0]);
+    std::fprintf(stderr, " start->step0 %.1f;", t * 1e3f);
+    for (int i = 0; i + 3 < h->npev; i += 4) {
+      float a = 0.f, b = 0.f, c = 0.f, g = 0.f;
+      cudaEventElapsedTime(&a, h->pev[i], h->pev[i + 1]);
+      cudaEventElapsedTime(&b, h->pev[i + 1], h->pev[i + 2]);
+      cudaEventElapsedTime(&c, h->pev[i + 2], h->pev[i + 3]);
+      if (i + 4 < h->npev) cudaEventElapsedTime(&g, h->pev[i + 3], h->pev[i + 4]);
+      else cudaEventElapsedTime(&g, h->pev[i + 3], h->e1);
+      std::fprintf(stderr, " | vc %.1f ap %.1f mgs %.1f next %.1f", a * 1e3f, b * 1e3f, c * 1e3f, g * 1e3f);
+    }
+    std::fprintf(stderr, "\n");
+  }
+  h->npev = 0;
   cudaGraphExecDestroy(ge);
   cudaGraphDestroy(gr);
   *avg_ms = ms / reps;
