@@ -194,6 +194,10 @@ void stgmg_loopback_hub_destroy(void* hub);
  * the last stgmg_solve (for the bench's gpu_launches field). */
 int stgmg_info(const stgmg_handle* h, int level, int* n_classes, int* max_patch_dofs, int64_t* n_patches);
 int64_t stgmg_last_launch_count(const stgmg_handle* h);
+/* The folded coarse sub-cycle (csrc/api.cu build_fold): the finest level f whose V-cycle (levels f..0: Alg. 1
+ * sweeps, transfers, coarse solve) is applied as its assembled n_f x n_f matrix, 0 if none (exact up to
+ * rounding; environment STGMG_FOLD_MB=0 at setup disables it). */
+int stgmg_fold_level(const stgmg_handle* h);
 
 /* Algorithmic work of one launch on level l (measurement): K2 flops = 2 sum_P C_P^2,
  * K2 bytes = 8 (2 sum_P C_P) + 8 sum_classes C_P^2 (gather, Y write, class inverses), K1 bytes = 16 N_l. */

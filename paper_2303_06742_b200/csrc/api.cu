@@ -1878,6 +1878,8 @@ int stgmg_info(const stgmg_handle* h, int level, int* n_classes, int* max_patch_
 
 int64_t stgmg_last_launch_count(const stgmg_handle* h) { return h ? h->launches : 0; }
 
+int stgmg_fold_level(const stgmg_handle* h) { return h && h->fold_ready ? h->fold_lv : 0; }
+
 static int sync_if_own(stgmg_handle* h) {
   if (h->own_stream) CKE(cudaStreamSynchronize(h->s));
   CKE(cudaGetLastError());

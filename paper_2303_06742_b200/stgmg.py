@@ -74,6 +74,7 @@ SIGNATURES = {
     "stgmg_info": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                   ctypes.POINTER(ctypes.c_int64)]),
     "stgmg_last_launch_count": (ctypes.c_int64, [_P]),
+    "stgmg_fold_level": (ctypes.c_int, [_P]),
     "stgmg_level_work": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "stgmg_time_kernel": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -342,3 +343,6 @@ class Solver:
 
     def launch_count(self):
         return int(self.lib.stgmg_last_launch_count(self.h))
+
+    def fold_level(self):
+        return int(self.lib.stgmg_fold_level(self.h))
