@@ -30,8 +30,6 @@ cudaError_t launch_mgs_dot(double* w, const double* vprev, const double* hprev, 
 cudaError_t launch_sqrt(double* v, cudaStream_t s);
 cudaError_t launch_scale(double* y, const double* x, const double* sc, int invert, long long n, cudaStream_t s);
 cudaError_t launch_givens(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, cudaStream_t s);
-cudaError_t launch_copy_words(void* dst, const void* src, int nbytes, cudaStream_t s);
-cudaError_t launch_fill_zero(double* p, long long n, cudaStream_t s);
 cudaError_t launch_givens_cond(double* H, int ldh, double* cs, double* sn, double* gv, int j, double* scal, int* ctl,
                                int has_next, cudaGraphConditionalHandle next, cudaStream_t s);
 cudaError_t launch_backsub_ctl(const double* H, int ldh, const double* gv, double* y, const int* ctl, cudaStream_t s);
@@ -406,15 +404,6 @@ struct stgmg_handle {
   // copies of v_j in and z_j out around each preconditioner application.  STGMG_STEP_GRAPHS=0: the copying form.
   std::vector<cudaGraphExec_t> vg_step;
   std::vector<int> vg_step_launches;
-  // the solve's opening (||b||, r_0, beta, first cycle set-up) and each cycle's closing (back substitution, x update,
-  // true residual) as graphs too, keyed by the caller's rhs / x pointers and m
-  struct Phase {
-    const void* k1 = nullptr;
-    const void* k2 = nullptr;
-    int m = 0;
-    cudaGraphExec_t ex = nullptr;
-    int launches = 0;
-  } ph_open, ph_close;
   int vg_step_m = 0;
   bool step_graphs = true;
   int vgraph_launches = 0;
@@ -1570,11 +1559,6 @@ static int ensure_krylov(stgmg_handle* h, int m) {
       cudaGraphExecDestroy(g);
       g = nullptr;
     }
-  for (auto* p : {&h->ph_open, &h->ph_close})
-    if (p->ex) {
-      cudaGraphExecDestroy(p->ex);
-      p->ex = nullptr;
-    }
   const long long N = h->lev[h->L - 1].g.N;
   CK(dalloc(h, &h->V, (size_t)(m + 1) * N));
   CK(dalloc(h, &h->Z, (size_t)m * N));
@@ -1868,8 +1852,6 @@ int stgmg_destroy(stgmg_handle* h) {
   if (h->vgraph_tmpl) cudaGraphDestroy(h->vgraph_tmpl);
   for (auto g : h->vg_step)
     if (g) cudaGraphExecDestroy(g);
-  if (h->ph_open.ex) cudaGraphExecDestroy(h->ph_open.ex);
-  if (h->ph_close.ex) cudaGraphExecDestroy(h->ph_close.ex);
   for (void* p : h->allocs) cudaFree(p);
   delete h->tr;
   if (h->pinned) cudaFreeHost(h->pinned);
@@ -2231,36 +2213,6 @@ static int build_cycle_graph(stgmg_handle* h, int m) {
   return rc;
 }
 
-// Enqueue `body` through a graph captured at first use for (k1, k2, m) (single GPU with step graphs), else directly.
-static int run_phase(stgmg_handle* h, stgmg_handle::Phase& ph, const void* k1, const void* k2, int m,
-                     const std::function<int()>& body) {
-  if (!h->vgraph || !h->step_graphs || h->nranks != 1) return body();
-  if (ph.ex && (ph.k1 != k1 || ph.k2 != k2 || ph.m != m)) {
-    cudaGraphExecDestroy(ph.ex);
-    ph.ex = nullptr;
-  }
-  if (!ph.ex) {
-    cudaGraph_t graph;
-    const long long before = h->launches;
-    CKE(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
-    const int rc = body();
-    const cudaError_t e = cudaStreamEndCapture(h->s, &graph);
-    ph.launches = (int)(h->launches - before);
-    h->launches = before;
-    if (rc) return rc;
-    CKE(e);
-    const cudaError_t ei = cudaGraphInstantiate(&ph.ex, graph, 0);
-    cudaGraphDestroy(graph);
-    CKE(ei);
-    ph.k1 = k1;
-    ph.k2 = k2;
-    ph.m = m;
-  }
-  CKE(cudaGraphLaunch(ph.ex, h->s));
-  h->launches += ph.launches;
-  return 0;
-}
-
 int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int tol_mode, int restart, int maxit,
                 stgmg_stats* stats) {
   if (!h || !rhs || !x || restart < 1 || maxit < 1 || !(tol > 0)) { set_error("bad argument"); return STGMG_EINVAL; }
@@ -2286,26 +2238,10 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
     CK(exchange(h, Lf, x));
     rhs = h->rhs_int;
   }
-  auto cycle_setup = [&]() -> int {   // v_0 = r / beta, g = beta e_1, H = 0
-    CKE(launch_scale(h->V, h->rv, scal + 2, 1, N, h->s));
-    CK(exchange(h, Lf, h->V));
-    CKE(launch_fill_zero(h->gv, m + 1, h->s));
-    CKE(launch_set_scalar(h->gv, scal + 2, h->s));
-    CKE(launch_fill_zero(h->H, (long long)ldh * m, h->s));
-    h->launches += 4;
-    return 0;
-  };
-  // opening: ||b||, r_0 = b - A x_0, beta; the first cycle's set-up is queued with it (unused if x_0 already meets
-  // the tolerance)
-  CK(run_phase(h, h->ph_open, rhs, x, m, [&]() -> int {
-    CK(dot(h, const_cast<double*>(rhs), nullptr, nullptr, nullptr, scal + 3, true));
-    CK(residual(h, Lf, rhs, x, h->rv));
-    CK(dot(h, h->rv, nullptr, nullptr, nullptr, scal + 2, true));
-    CKE(launch_copy_words(hp, scal, 4 * sizeof(double), h->s));   // into mapped pinned memory
-    h->launches += 1;
-    return cycle_setup();
-  }));
-  bool setup_queued = true;
+  CK(dot(h, const_cast<double*>(rhs), nullptr, nullptr, nullptr, scal + 3, true));
+  CK(residual(h, Lf, rhs, x, h->rv));
+  CK(dot(h, h->rv, nullptr, nullptr, nullptr, scal + 2, true));
+  CKE(cudaMemcpyAsync(hp, scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
   CKE(cudaStreamSynchronize(h->s));
   const double bnorm = hp[3];
   double beta = hp[2];
@@ -2321,8 +2257,12 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
     CKE(cudaMemsetAsync(h->ctl, 0, 2 * sizeof(int), h->s));
   }
   while (!converged && its < maxit) {
-    if (!setup_queued) CK(cycle_setup());
-    setup_queued = false;
+    CKE(launch_scale(h->V, h->rv, scal + 2, 1, N, h->s));                 // v_0 = r / beta
+    CK(exchange(h, Lf, h->V));
+    CKE(cudaMemsetAsync(h->gv, 0, sizeof(double) * (m + 1), h->s));
+    CKE(launch_set_scalar(h->gv, scal + 2, h->s));                        // g_0 = beta
+    CKE(cudaMemsetAsync(h->H, 0, sizeof(double) * ldh * m, h->s));
+    h->launches += 2;
     int jdone = 0;
     if (use_graph) {   // the whole cycle on the device: the Givens kernels chain the steps
       CKE(cudaGraphLaunch(h->cyc_exec, h->s));
@@ -2353,19 +2293,12 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
       jdone = j + 1;
       if (hp[0] <= target || hp[1] <= 1e-14 * beta || its >= maxit) break;
     }
-    // closing: x += Z y (y from the back substitution of the jdone x jdone system), true residual
-    hctl[1] = jdone;
-    CK(run_phase(h, h->ph_close, rhs, x, m, [&]() -> int {
-      CKE(launch_copy_words(h->ctl + 1, hctl + 1, sizeof(int), h->s));   // from mapped pinned memory
-      CKE(launch_backsub_ctl(h->H, ldh, h->gv, h->yv, h->ctl, h->s));
-      CKE(launch_update_x_ctl(x, h->Z, h->yv, h->ctl, N, h->s));
-      h->launches += 2;
-      CK(residual(h, Lf, rhs, x, h->rv));
-      CK(dot(h, h->rv, nullptr, nullptr, nullptr, scal + 2, true));
-      CKE(launch_copy_words(hp + 2, scal + 2, sizeof(double), h->s));
-      h->launches += 2;
-      return 0;
-    }));
+    CKE(launch_backsub(h->H, ldh, h->gv, h->yv, jdone, h->s));
+    CKE(launch_update_x(x, h->Z, h->yv, jdone, N, h->s));
+    h->launches += 2;
+    CK(residual(h, Lf, rhs, x, h->rv));
+    CK(dot(h, h->rv, nullptr, nullptr, nullptr, scal + 2, true));
+    CKE(cudaMemcpyAsync(hp + 2, scal + 2, sizeof(double), cudaMemcpyDeviceToHost, h->s));
     CKE(cudaStreamSynchronize(h->s));
     beta = hp[2];
     if (beta <= target) { converged = true; break; }

@@ -2,8 +2,6 @@
 // modified Gram–Schmidt with the update of step i-1 fused into the dot of step i, deterministic two-level
 // reductions (fixed grid, fixed-order last-block combine), Givens rotations and back substitution on device
 // (readings A2-A4, A35).
-#include <algorithm>
-
 #include "stgmg_internal.cuh"
 
 namespace stgmg {
@@ -230,24 +228,6 @@ cudaError_t launch_noop(int blocks, cudaStream_t s) {
   return launch_pdl(noop_kernel, dim3(blocks), dim3(128), 0, s, 0, (double*)nullptr);
 }
 
-// Small word copies / fills as kernels (graphs of the solve stay kernel-only; the host side is mapped pinned memory).
-__global__ void copy_words_kernel(void* dst, const void* src, int nbytes) {
-  const unsigned char* a = static_cast<const unsigned char*>(src);
-  unsigned char* b = static_cast<unsigned char*>(dst);
-  for (int i = threadIdx.x; i < nbytes; i += blockDim.x) b[i] = a[i];
-}
-cudaError_t launch_copy_words(void* dst, const void* src, int nbytes, cudaStream_t s) {
-  copy_words_kernel<<<1, 32, 0, s>>>(dst, src, nbytes);
-  return cudaGetLastError();
-}
-__global__ void fill_zero_kernel(double* p, long long n) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    p[i] = 0.0;
-}
-cudaError_t launch_fill_zero(double* p, long long n, cudaStream_t s) {
-  fill_zero_kernel<<<(unsigned)std::min(1184LL, (n + 255) / 256), 256, 0, s>>>(p, n);
-  return cudaGetLastError();
-}
 __global__ void set_scalar_kernel(double* dst, const double* src) {
   if (threadIdx.x == 0) *dst = *src;
 }
