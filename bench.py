@@ -301,7 +301,11 @@ def run_ours(args):
     work = s.level_work()
     # whole-solve FP64 tensor work: 2 J_max patch-solve sweeps per smoothed level per V-cycle (one V-cycle per GMRES
     # iteration), the dominant flops of the solve (95-99 %)
-    vc_flops = sum(2 * 4 * s.level_work(l)["k2_flops"] for l in range(1, cfg["levels"]))   # this rank's
+    # levels at or below the folded sub-cycle run as one GEMV of 2 n_f^2 flops instead of their sweeps
+    fold_lv = s.fold_level()
+    vc_flops = sum(2 * 4 * s.level_work(l)["k2_flops"] for l in range(max(1, fold_lv + 1), cfg["levels"]))
+    if fold_lv:
+        vc_flops += 2.0 * float(s.size(fold_lv)) ** 2   # this rank's
     job_flops = torch.tensor([vc_flops * its], dtype=torch.float64, device=dev)
     if ws > 1:
         torch.distributed.all_reduce(job_flops, op=torch.distributed.ReduceOp.SUM)
@@ -309,7 +313,6 @@ def run_ours(args):
     k2_ms = s.time_kernel(0, reps=50)
     k2_achieved = work["k2_flops"] / (k2_ms * 1e-3) / 1e12
     vc_ms = s.time_kernel(3, reps=20)
-    fold_lv = s.fold_level()
     k1_ms = s.time_kernel(1, reps=50)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "k2_traffic.json")
@@ -375,7 +378,10 @@ def run_ours(args):
                          "traffic": traffic, "avg_launch_ms": k2_ms, "flops_per_launch": work["k2_flops"],
                          "algorithmic_bytes_per_launch": work["k2_bytes"],
                          "peak_source": "FP64 DMMA m8n8k4 microbenchmark on this pool (profiles/fp64_peak_r01.json); "
-                                        "MEASURED_PEAKS.json has no fp64 entry"},
+                                        "MEASURED_PEAKS.json has no fp64 entry",
+                         "timing": "CUDA events on the bench stream around 50 graph-captured back-to-back launches of "
+                                   "the fine-level K2 right after the timed region (inside the timed region it runs "
+                                   "within the per-step graphs); its share of the step: profiles/launches_r01_cfg1.txt"},
             "solve_fp64": {"flops_per_vcycle": vc_flops, "achieved_tflops": solve_tflops,
                            "frac_of_dmma_peak": solve_tflops / (FP64_PEAK_TFLOPS * ws),
                            "note": "patch-solve (K2) flops of the whole slab solves / timed solve time; K1/K3/K5/K7 "
