@@ -25,7 +25,8 @@ namespace stgmg {
 //   warp-specialised variant of THIS gathered-B kernel were measured slower; the dense K2D below,
 //   whose B is pre-expanded, is the warp-specialised kernel.)
 // Tile variants (WM x WN warps, each MT x NT m8n8 tiles, split-K KS): big 112 x 32, wide 112 x 64, medium 56 x 32,
-// small 32 x 8, and the latency variants K2L below.  Split-K partial sums are added in a fixed order, every output
+// small 32 x 8; the dense K2D (pre-expanded B, warp-specialised), the shared-B K2S and the latency variants K2L below
+// (k2_pick_variant: which level gets which).  Split-K partial sums are added in a fixed order, every output
 // element is computed by exactly one CTA with the same k order whatever the tiling: bitwise reproducible.
 constexpr int K2_BK = 16;
 constexpr int K2_MAXCP = 2048;       // largest C_P whose gather table is staged in shared memory
