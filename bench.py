@@ -1,18 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the hot path: one space-time slab solve (FGMRES(m) + GMG V-cycle with patch Vanka) per step.
 
-Workload (default): BASELINE.json configs[1] — 2D unit square, 64x64 cells, 6 levels, Q2^2/Q2^2/Q1, dG(1)
-(141,578 DoFs), tau = 0.01, GMRES(30), rel tol 1e-8, load = i.i.d. U[-1,1) seed 1 (reading A21), zero initial
-state; each step forms the slab RHS F_n = L + J X_{n-1} on the device (K8) and solves (slab marching).
+Workload (default): BASELINE.json configs[4] — the largest single-GPU configuration and the one the north star
+asks to scale: 3D clamped beam [0,8]x[0,1]^2, 256x32x32 cells, 6 levels, Q2^3/Q2^3/Q1, dG(1) (26,568,846 DoFs),
+tau = 0.01, GMRES(30) (reading of SURVEY §8(d)), rel tol 1e-8; u = 0 at x = 0, traction (0,0,-sin(pi t/2)) on
+x = 8 (reading A23), p = 0 on z = 1 (A25); zero initial state.  Each step is one slab of the march
+t_n = n tau: the load L_n is assembled on the device (stgmg_slab_load), F_n = L_n + J X_{n-1} (stgmg_slab_rhs, K8),
+then the slab is solved.  --config c selects another BASELINE config (0-3: manufactured / random loads as
+BASELINE states them).
 Metric: MDoF*iter/s = N_slab * GMRES iterations / solve time / 1e6; ms_per_step = s/slab.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
---impl reference runs the oracle (plain fp64 CPU implementation, oracle/) as it stands on the host cores.
+--impl reference runs the oracle (plain fp64 CPU implementation, oracle/) as it stands on the host cores, on a
+bounded sample of the same workload (see cpu_sample()).
 N > 1 (torchrun, one rank per GPU): the x-slab domain decomposition of SURVEY §8(e) — every rank owns a slab of
 cells of the SAME global slab problem (window vectors, halo exchange over NCCL after every smoothing sweep, GMRES
 inner products allreduced), so the scaling is "strong"; value = global DoFs x iterations / max-over-ranks time.
---replicas instead runs N independent copies of the workload ("weak" scaling, no data-path collective).
+A decomposition that cannot be set up is an error (non-zero exit).  --replicas instead runs N independent copies
+of the workload ("weak" scaling, no data-path collective).
 """
 import argparse
 import json
@@ -28,6 +34,8 @@ sys.path.insert(0, ROOT)
 
 from stgmg_inputs import config, uniform_load, dof_count  # noqa: E402
 
+HBM_PEAK_GBS = 6470.8      # MEASURED_PEAKS.json hbm_gbs (driver-written copy bandwidth of this pool's B200s)
+
 FP64_PEAK_TFLOPS = 37.19   # measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peak_r01.json)
 
 
@@ -36,7 +44,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of the decomposition")
@@ -51,6 +59,28 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     lrank = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, lrank
+
+
+def load_label(cfg):
+    if cfg["load"] == "beam":
+        return "beam traction (0,0,-sin(pi t/2)) on x=%g (reading A23), zero initial state; L_n assembled on the " \
+               "device each slab (stgmg_slab_load)" % cfg["hi"][0]
+    if cfg["load"] == "manufactured":
+        return "manufactured solution loads (BASELINE), interpolated initial data (A20); L_n assembled on the " \
+               "device each slab (stgmg_slab_load)"
+    return "uniform[-1,1) seed %s (reading A21), zero initial state" % cfg["seed"]
+
+
+def workload_config(cfg, args, ws, dd):
+    """The config object of the JSON line; identical for both arms (--impl ours / reference)."""
+    d = cfg["dim"]
+    return {"workload": cfg["name"], "dofs": dof_count(cfg), "dim": d, "cells": list(cfg["cells"][:d]),
+            "levels": cfg["levels"], "r": cfg["r"], "k": cfg["k"], "tau": cfg["tau"], "restart": cfg["restart"],
+            "rtol": cfg["rtol"], "load": load_label(cfg), "smoother": args.smoother,
+            "march": "slab n of step i: t_n = (warmup + i) tau, F_n = L_n + J X_{n-1}",
+            "l2": "flushed between timed steps (256 MB write, untimed); inputs > L2 (212 MB per vector at cfg4)",
+            "parallelism": ("x-slab decomposition over %d GPUs (NCCL halo exchange)" % ws) if dd else
+                           ("%d replicas" % ws if ws > 1 else "single GPU")}
 
 
 # ---------------------------------------------------------------------------------------------- clocks -----
@@ -104,32 +134,19 @@ def nvml_energy_mj(index):
         return None
 
 
+def host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
 # ---------------------------------------------------------------------------------------------- oracle -----
-def oracle_slab_solver(cfg):
-    """The oracle as it stands (CPU), for the cpu_baseline / --impl reference legs."""
-    from oracle.mg import Hierarchy
-    from oracle.gmres import fgmres
-    from oracle.loads import slab_rhs, end_state
-    d = cfg["dim"]
-    p = dict(cfg["params"])
-    p["K"] = np.array(p["K"], dtype=float).reshape(3, 3)[:d, :d].ravel().tolist()
-    H = Hierarchy(d, cfg["cells"][:d], cfg["lo"][:d], cfg["hi"][:d], cfg["r"], cfg["k"], cfg["levels"], p, cfg["tau"],
-                  bc_u=list(cfg["bc_u"][:2 * d]), bc_p=list(cfg["bc_p"][:2 * d]))
-    S = H.ops[-1].assemble_spatial()
-    lev, op, A = H.fine, H.ops[-1], H.A[-1]
-    L = uniform_load(lev.N, cfg["seed"] or 1)
-    state = {"X": np.zeros(lev.N)}
-
-    def step():
-        U, V, P = end_state(lev, state["X"])
-        b = slab_rhs(lev, S, op.chi_m1, op.th, U, V, P, None, None) + L
-        x, info = fgmres(lambda v: A @ v, b, H.vcycle, tol=cfg["rtol"], restart=cfg["restart"])
-        state["X"] = x
-        return info["iterations"]
-
-    return lev.N, step
-
-
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -139,18 +156,30 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(cfg, budget_s=25.0):
-    N, step = oracle_slab_solver(cfg)
+def cpu_sample(cfg, iterations=1):
+    """The oracle as it stands (oracle/ebe.py: element-by-element operator, class-batched patch solves, no global
+    matrix) on the same workload: setup (untimed), the slab-1 right-hand side, then `iterations` FGMRES iterations
+    (each = one V-cycle + one operator apply + the MGS step).  MDoF*iter/s = N / (time per GMRES iteration), so the
+    bounded sample measures the metric directly.  Returns (value, seconds_per_iteration, sample description)."""
+    from oracle.ebe import EbeHierarchy, ebe_slab_rhs, fgmres_iterations
+    H = EbeHierarchy.from_config(cfg)
+    b = ebe_slab_rhs(H, cfg, 0)
     t0 = time.perf_counter()
-    its, n = 0, 0
-    while True:
-        its += step()
-        n += 1
-        if time.perf_counter() - t0 > budget_s / 2 or n >= 3:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": N * its / dt / 1e6, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle",
-            "sample": "%d slab solve(s) of %s (setup excluded), %.2f s/slab, %d GMRES its" % (n, cfg["name"], dt / n, its)}
+    fgmres_iterations(H, b, iterations, restart=cfg["restart"])
+    dt = (time.perf_counter() - t0) / iterations
+    N = H.fine_op.lev.N
+    return N / dt / 1e6, dt, "%d FGMRES iteration(s) (V-cycle + apply + MGS) of slab 1 of %s, setup excluded, " \
+                             "%.2f s per iteration" % (iterations, cfg["name"], dt)
+
+
+def cpu_baseline(cfg):
+    try:
+        val, dt, sample = cpu_sample(cfg, 1)
+    except MemoryError as e:
+        return {"value": None, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle",
+                "sample": "not run: %s" % e}
+    return {"value": val, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle", "sample": sample,
+            "host": host_info()}
 
 
 def run_reference(args):
@@ -158,22 +187,29 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = config(args.config)
-    N, step = oracle_slab_solver(cfg)
+    from oracle.ebe import EbeHierarchy, ebe_slab_rhs, fgmres_iterations
+    t_setup = time.perf_counter()
+    H = EbeHierarchy.from_config(cfg)
+    b = ebe_slab_rhs(H, cfg, 0)
+    t_setup = time.perf_counter() - t_setup
+    N = H.fine_op.lev.N
+    # one reference step = one FGMRES iteration of the slab solve (V-cycle + apply + MGS): MDoF*iter/s = N / t_step
     for _ in range(args.warmup):
-        step()
+        fgmres_iterations(H, b, 1, restart=cfg["restart"])
     t0 = time.perf_counter()
-    its = 0
     for _ in range(args.steps):
-        its += step()
+        fgmres_iterations(H, b, 1, restart=cfg["restart"])
     dt = time.perf_counter() - t0
-    val = N * its / dt / 1e6
+    val = N * args.steps / dt / 1e6
     cores = blas_threads()
-    sample = "%d slab solves of %s on host cores (oracle as it stands)" % (args.steps, cfg["name"])
+    sample = ("%d steps, each one FGMRES iteration (V-cycle + operator apply + MGS) of slab 1 of %s, on the host "
+              "cores (oracle as it stands, oracle/ebe.py); setup %.1f s excluded" % (args.steps, cfg["name"], t_setup))
     out = {"impl": "reference", "metric": "slab_solve_throughput", "value": val, "unit": "MDoF*iter/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": cfg["name"], "dofs": N, "gmres_iterations": its},
-           "cpu_baseline": {"value": val, "unit": "MDoF*iter/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "config": workload_config(cfg, args, 1, False),
+           "cpu_baseline": {"value": val, "unit": "MDoF*iter/s", "cores": cores, "kind": "oracle", "sample": sample,
+                            "host": host_info()},
            "e2e": {"value": val, "unit": "MDoF*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -182,67 +218,66 @@ def run_reference(args):
 def run_ours(args):
     import torch
     ws, rank, lrank = dist_env()
+    dd = ws > 1 and not args.replicas
     if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # lets the driver count the communicator's ranks
         torch.cuda.set_device(lrank)
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
     dev = torch.device("cuda", lrank if ws > 1 else 0)
     from paper_2303_06742_b200 import Solver
-    from paper_2303_06742_b200.stgmg import nccl_unique_id, nccl_comm_create, nccl_comm_destroy, partition_plan
+    from paper_2303_06742_b200.stgmg import (nccl_unique_id, nccl_comm_create, nccl_comm_destroy, partition_plan,
+                                             LOAD_MANUFACTURED, LOAD_BEAM_TRACTION)
     from paper_2303_06742_b200.partition import window_index
     cfg = config(args.config)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    dd = ws > 1 and not args.replicas
     smoother = {"additive": 0, "colored": 1, "element": 2, "overwrite": 3}[args.smoother]
     comm = None
     t_setup = time.perf_counter()
-    dd_error = None
     if dd:
-        # the library's own NCCL communicator: rank 0 draws the id, torch.distributed broadcasts it (stgmg.h)
-        try:
-            uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
-            torch.distributed.broadcast(uid, 0)
-            comm = nccl_comm_create(bytes(uid.cpu().tolist()), ws, rank)
-            s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm, smoother=smoother)
-        except Exception as e:   # every rank fails the same way: report it and run replicas instead
-            dd_error = "%s: %s" % (type(e).__name__, e)
-            ok = torch.tensor([0.0], device=dev)
-        else:
-            ok = torch.tensor([1.0], device=dev)
-        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
-        if ok.item() < 1.0:
-            if dd_error is None:
-                s.close()
-                dd_error = "another rank failed to set up the decomposition"
-            if comm is not None:
-                nccl_comm_destroy(comm)
-                comm = None
-            dd = False
-            print("bench: x-slab decomposition unavailable (%s); running %d replicas" % (dd_error, ws), file=sys.stderr)
-            s = Solver(cfg, stream=stream, smoother=smoother)
+        # the library's own NCCL communicator: rank 0 draws the id, torch.distributed broadcasts it (stgmg.h).
+        # Any failure here raises: a decomposition that cannot be set up ends the run with a non-zero exit.
+        uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
+        torch.distributed.broadcast(uid, 0)
+        comm = nccl_comm_create(bytes(uid.cpu().tolist()), ws, rank)
+        s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm, smoother=smoother)
     else:
         s = Solver(cfg, stream=stream, smoother=smoother)
     t_setup = time.perf_counter() - t_setup
     N = s.size()                       # this rank's (window) vector length
     Nglob = dof_count(cfg)             # DoFs of the global slab problem
-    Lg = uniform_load(Nglob, cfg["seed"] or 1)
-    if dd:
-        idx, _own = window_index(cfg, cfg["levels"] - 1, partition_plan(cfg, cfg["levels"] - 1, rank, ws))
-        Lg = Lg[idx]
-    L = torch.as_tensor(Lg, device=dev)
-    Xp = torch.zeros(N, dtype=torch.float64, device=dev)
-    rhs = torch.zeros_like(Xp)
-    x = torch.zeros_like(Xp)
+    load_kind = {"manufactured": LOAD_MANUFACTURED, "beam": LOAD_BEAM_TRACTION}.get(cfg["load"])
+    if load_kind is None:
+        Lg = uniform_load(Nglob, cfg["seed"] or 1)
+        if dd:
+            idx, _own = window_index(cfg, cfg["levels"] - 1, partition_plan(cfg, cfg["levels"] - 1, rank, ws))
+            Lg = Lg[idx]
+        L = torch.as_tensor(Lg, device=dev)
+    else:
+        L = torch.zeros(N, dtype=torch.float64, device=dev)
+    X = [torch.zeros(N, dtype=torch.float64, device=dev), torch.zeros(N, dtype=torch.float64, device=dev)]
+    if load_kind == LOAD_MANUFACTURED:
+        s.initial_state(LOAD_MANUFACTURED, 0.0, X[0])
+    rhs = torch.zeros(N, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # > 126 MB L2
-    rhs_launches = 1 << cfg["dim"]
+    state = {"n": 0}
 
     def step():
-        s.slab_rhs(L, Xp, rhs)
-        x.zero_()
-        st = s.solve(rhs, x, tol=cfg["rtol"], restart=cfg["restart"])
-        Xp.copy_(x)
-        return st
+        """One slab of the march: L_n (device), F_n = L_n + J X_{n-1} (K8), solve; returns (stats, launches)."""
+        t_n = state["n"] * cfg["tau"]
+        nl = 0
+        if load_kind is not None:
+            s.slab_load(load_kind, t_n, L)
+            nl += s.launch_count()
+        s.slab_rhs(L, X[0], rhs)
+        nl += s.launch_count()
+        X[1].zero_()
+        st = s.solve(rhs, X[1], tol=cfg["rtol"], restart=cfg["restart"])
+        nl += s.launch_count()
+        X[0], X[1] = X[1], X[0]
+        state["n"] += 1
+        return st, nl
 
     for _ in range(args.warmup):
         step()
@@ -252,18 +287,20 @@ def run_ours(args):
     clocks = ClockSampler(dev.index)
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    its, launches, resid = 0, 0, []
+    its, launches, resid, its_list = 0, 0, [], []
     for i in range(args.steps):
         flush.fill_(float(i))                      # L2 flush between timed steps (untimed)
         ev0[i].record(stream)
-        st = step()
+        st, nl = step()
         ev1[i].record(stream)
         its += st["iterations"]
+        its_list.append(st["iterations"])
         resid.append(st["rel_residual"])
-        launches += s.launch_count() + rhs_launches
+        launches += nl
     torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
-    # energy window: NVML's counter updates coarsely, so measure over >= 1.5 s of back-to-back slab solves
+    per_step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    ms = sum(per_step_ms)
+    # energy window: NVML's counter updates coarsely, so measure over >= 1.5 s and >= 2 back-to-back slab solves
     # (same step, no flushes); the clock sampler keeps running through it
     e_start = nvml_energy_mj(dev.index)
     t_e0 = time.perf_counter()
@@ -271,7 +308,7 @@ def run_ours(args):
     while True:
         step()
         n_e += 1
-        if n_e >= args.steps and time.perf_counter() - t_e0 > 1.5:
+        if n_e >= 2 and time.perf_counter() - t_e0 > 1.5:
             torch.cuda.synchronize()
             if time.perf_counter() - t_e0 > 1.5:
                 break
@@ -297,23 +334,34 @@ def run_ours(args):
               "avg_watts": energy_j / t_e if energy_j is not None else None, "solves": n_e, "window_s": t_e,
               "source": "NVML nvmlDeviceGetTotalEnergyConsumption (board), >= 1.5 s window of back-to-back solves"}
 
-    # roofline of the dominant kernel: K2 patch GEMM on the fine level (FP64 DMMA), timed alone
-    work = s.level_work()
     # whole-solve FP64 tensor work: 2 J_max patch-solve sweeps per smoothed level per V-cycle (one V-cycle per GMRES
-    # iteration), the dominant flops of the solve (95-99 %)
-    # levels at or below the folded sub-cycle run as one GEMV of 2 n_f^2 flops instead of their sweeps
+    # iteration), the dominant flops of the solve (95-99 %).  Levels at or below a folded
+    # sub-cycle (2D configs) run as one FFMA GEMV instead; its 2 n_f^2 flops are reported apart and not counted
+    # against the DMMA peak.  On split levels every rank counts the patches of its own window.
     fold_lv = s.fold_level()
     vc_flops = sum(2 * 4 * s.level_work(l)["k2_flops"] for l in range(max(1, fold_lv + 1), cfg["levels"]))
-    if fold_lv:
-        vc_flops += 2.0 * float(s.size(fold_lv)) ** 2   # this rank's
+    fold_flops = 2.0 * float(s.size(fold_lv)) ** 2 if fold_lv else 0.0
     job_flops = torch.tensor([vc_flops * its], dtype=torch.float64, device=dev)
     if ws > 1:
         torch.distributed.all_reduce(job_flops, op=torch.distributed.ReduceOp.SUM)
     solve_tflops = float(job_flops.item()) / t_max_s / 1e12
-    k2_ms = s.time_kernel(0, reps=50)
-    k2_achieved = work["k2_flops"] / (k2_ms * 1e-3) / 1e12
-    vc_ms = s.time_kernel(3, reps=20)
-    k1_ms = s.time_kernel(1, reps=50)
+
+    # per-kernel rooflines on the fine level (CUDA events around graph-captured back-to-back launches on the bench
+    # stream, right after the timed region): K2 against the FP64 DMMA peak, the HBM-bound kernels against HBM
+    Lf = cfg["levels"] - 1
+    kernels = {}
+    for name, kind, reps in [("K2_patch_gemm", 0, 10), ("K1_apply", 1, 10), ("K3_average", 2, 10),
+                             ("K5_restrict_prolong", 7, 10), ("K7_mgs_pass", 8, 20)]:
+        t_ms = s.time_kernel(kind, Lf, reps=reps)
+        fl, by = s.kernel_work(kind, Lf)
+        ent = {"avg_launch_ms": t_ms, "algorithmic_bytes": by, "hbm_gbs": by / (t_ms * 1e-3) / 1e9,
+               "hbm_frac": by / (t_ms * 1e-3) / 1e9 / HBM_PEAK_GBS}
+        if fl:
+            ent.update({"flops": fl, "tflops": fl / (t_ms * 1e-3) / 1e12,
+                        "fp64_frac": fl / (t_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS})
+        kernels[name] = ent
+    k2 = kernels["K2_patch_gemm"]
+    vc_ms = s.time_kernel(3, reps=3)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "k2_traffic.json")
     if os.path.exists(tp):
@@ -322,17 +370,20 @@ def run_ours(args):
         except Exception:
             traffic = None
 
-    # e2e: the same solve through the C ABI with host buffers (H2D rhs + x, D2H x inside the timed region)
+    # e2e: the same slab solve through the C ABI with HOST buffers (H2D rhs + x, solve, D2H x inside the timed
+    # region), on the right-hand side of the last marched slab
     rhs_h = torch.empty(N, dtype=torch.float64).pin_memory()
     x_h = torch.zeros(N, dtype=torch.float64).pin_memory()
-    rhs_h.copy_(L.cpu())
-    e2e_its = 0
-    for _ in range(1):
-        x_h.zero_()
-        s.solve_host(rhs_h, x_h)
+    rhs_h.copy_(rhs.cpu())
+    n_e2e = max(1, min(args.steps, 5)) if Nglob > 5e6 else args.steps
+    x_h.zero_()
+    s.solve_host(rhs_h, x_h)                       # warm-up
     torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    e2e_its = 0
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(n_e2e):
         x_h.zero_()
         st = s.solve_host(rhs_h, x_h)
         e2e_its += st["iterations"]
@@ -354,41 +405,37 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max_s * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "strong" if dd else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": cfg["name"], "dofs": Nglob, "levels": cfg["levels"], "r": cfg["r"], "k": cfg["k"],
-                       "restart": cfg["restart"], "rtol": cfg["rtol"], "load": "uniform[-1,1) seed %s" % cfg["seed"],
-                       "smoother": args.smoother,
-                       "gmres_iterations_total": its, "final_rel_residual_max": max(resid),
-                       "l2": "flushed between timed steps (256 MB write, untimed)",
-                       "parallelism": ("x-slab decomposition over %d GPUs (NCCL halo exchange)" % ws) if dd else
-                                      (("%d replicas" % ws + (" (decomposition unavailable: %s)" % dd_error
-                                                              if dd_error else "")) if ws > 1 else "single GPU"),
-                       "setup_s": t_setup,
-                       "s_per_slab": t_max_s / args.steps,
-                       "vcycle_ms": vc_ms, "k1_fine_apply_ms": k1_ms,
-                       "coarse_fold": ({"level": fold_lv, "dofs": s.size(fold_lv),
-                                        "note": "V-cycle of levels %d..0 (Alg. 1 sweeps, transfers, coarse solve) "
-                                                "applied as its assembled matrix, built at setup from the same "
-                                                "kernels; exact up to rounding (DESIGN.md 7.1)" % fold_lv}
-                                       if fold_lv else None),
-                       "k1_fine_hbm_gbs": work["k1_bytes"] / (k1_ms * 1e-3) / 1e9},
+            "config": workload_config(cfg, args, ws, dd),
+            "solve": {"gmres_iterations_total": its, "gmres_iterations_per_slab": its_list,
+                      "final_rel_residual_max": max(resid), "s_per_slab": t_max_s / args.steps,
+                      "s_per_slab_each": [t * 1e-3 for t in per_step_ms], "setup_s": t_setup,
+                      "vcycle_ms": vc_ms, "slabs_marched": state["n"],
+                      "coarse_fold": ({"level": fold_lv, "dofs": s.size(fold_lv),
+                                       "note": "V-cycle of levels %d..0 (Alg. 1 sweeps, transfers, coarse solve) "
+                                               "applied as its assembled matrix, built at setup from the same "
+                                               "kernels; exact up to rounding (DESIGN.md 7.1)" % fold_lv}
+                                      if fold_lv else None)},
             "gpu_launches": launches,
             "energy": energy,
-            "roofline": {"kernel": "K2 vanka_patch_gemm (fine level)", "bound": "tensor", "achieved": k2_achieved,
-                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": k2_achieved / FP64_PEAK_TFLOPS,
-                         "traffic": traffic, "avg_launch_ms": k2_ms, "flops_per_launch": work["k2_flops"],
-                         "algorithmic_bytes_per_launch": work["k2_bytes"],
+            "roofline": {"kernel": "K2 vanka_patch_gemm (fine level)", "bound": "tensor", "achieved": k2["tflops"],
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": k2["fp64_frac"],
+                         "traffic": traffic, "avg_launch_ms": k2["avg_launch_ms"], "flops_per_launch": k2["flops"],
+                         "algorithmic_bytes_per_launch": k2["algorithmic_bytes"],
                          "peak_source": "FP64 DMMA m8n8k4 microbenchmark on this pool (profiles/fp64_peak_r01.json); "
                                         "MEASURED_PEAKS.json has no fp64 entry",
-                         "timing": "CUDA events on the bench stream around 50 graph-captured back-to-back launches of "
+                         "timing": "CUDA events on the bench stream around graph-captured back-to-back launches of "
                                    "the fine-level K2 right after the timed region (inside the timed region it runs "
-                                   "within the per-step graphs); its share of the step: profiles/launches_r01_cfg1.txt"},
+                                   "within the per-step graphs); its share of the step: profiles/launches_r02_*.txt"},
+            "kernels": kernels,
             "solve_fp64": {"flops_per_vcycle": vc_flops, "achieved_tflops": solve_tflops,
                            "frac_of_dmma_peak": solve_tflops / (FP64_PEAK_TFLOPS * ws),
-                           "note": "patch-solve (K2) flops of the whole slab solves / timed solve time; K1/K3/K5/K7 "
-                                   "flops (<5 %) not counted"},
+                           "fold_gemv_flops_per_vcycle": fold_flops,
+                           "note": "patch-solve (K2, DMMA) flops of the whole slab solves / timed solve time; the "
+                                   "folded sub-cycle GEMV (FFMA) and K1/K3/K5/K7 flops (<5 %) are not counted"},
             "clocks": clk,
             "e2e": {"value": e2e_val, "unit": "MDoF*iter/s", "h2d_bytes_per_step": 16 * N * ws,
-                    "d2h_bytes_per_step": 8 * N * ws},
+                    "d2h_bytes_per_step": 8 * N * ws, "steps": n_e2e,
+                    "how": "stgmg_solve_host: pinned host rhs/x copied H2D, solve, x copied D2H, host clock"},
             "cpu_baseline": cpu,
         }
         print(json.dumps(out), flush=True)

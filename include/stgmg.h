@@ -205,9 +205,17 @@ int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double*
 
 /* Times reps back-to-back launches of one hot-path kernel on level l with CUDA events on params.stream:
  * kind 0 = K2 patch GEMM, 1 = K1 operator apply (all colours), 2 = K3 averaging, 3 = whole V-cycle graph,
- * 4 / 5 = empty kernel on 1 / 148 CTAs, 6 = one smoothing sweep (level >= 1), 7 = restriction + prolongation.
+ * 4 / 5 = empty kernel on 1 / 148 CTAs, 6 = one smoothing sweep (level >= 1), 7 = restriction + prolongation,
+ * 8 = one fused MGS pass of K7 (fine level only, after a solve has allocated the Krylov basis).
  * Operates on the level's internal work buffers (their contents are overwritten). */
 int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms);
+
+/* Algorithmic work of one launch of stgmg_time_kernel's kind on level l (SURVEY §8(d) "Binding roofline"):
+ * kind 0 (K2): flops 2 sum_P C_P^2, bytes 16 sum_P C_P + 8 sum_classes C_P^2; kind 1 (K1, y = A x): 16 N_l bytes;
+ * kind 2 (K3): 16 N_l + 8 sum_P C_P bytes (read Y, read and write d; 1/p is structural); kind 7 (K5 restrict +
+ * prolong-add): 24 N_l + 16 N_{l-1} bytes; kind 8 (K7 fused MGS pass): 32 N bytes.  flops = 0 for the HBM kinds.
+ * EINVAL for other kinds. */
+int stgmg_kernel_work(const stgmg_handle* h, int kind, int level, double* flops, double* bytes);
 
 #ifdef __cplusplus
 }

@@ -2367,12 +2367,44 @@ int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double*
   return 0;
 }
 
+int stgmg_kernel_work(const stgmg_handle* h, int kind, int level, double* flops, double* bytes) {
+  if (!h || level < 0 || level >= h->L || !flops || !bytes) { set_error("bad argument"); return STGMG_EINVAL; }
+  const LevelData& Lv = h->lev[level];
+  const double N = (double)Lv.g.N;
+  double sumcp = 0.0, fl2 = 0.0, invb = 0.0;
+  for (const auto& c : Lv.cls) {
+    fl2 += 2.0 * (double)c.cp * (double)c.cp * (double)c.ncols;
+    sumcp += (double)c.cp * (double)c.ncols;
+    invb += 8.0 * (double)c.cp * (double)c.cp;
+  }
+  *flops = 0.0;
+  switch (kind) {
+    case 0: *flops = fl2; *bytes = 16.0 * sumcp + invb; break;                 // K2
+    case 1: *bytes = 16.0 * N; break;                                          // K1: read x, write y
+    case 2: *bytes = 16.0 * N + 8.0 * sumcp; break;                            // K3: read Y, read + write d
+    case 7: {                                                                  // K5: restrict + prolong-add
+      if (level < 1) { set_error("kind 7 needs level >= 1"); return STGMG_EINVAL; }
+      const double Nc = (double)h->lev[level - 1].g.N;
+      *bytes = 8.0 * N + 8.0 * Nc + 8.0 * Nc + 16.0 * N;
+      break;
+    }
+    case 8: *bytes = 32.0 * N; break;                                          // K7: read w, v_prev, v_next; write w
+    default: set_error("no work model for this kind"); return STGMG_EINVAL;
+  }
+  return 0;
+}
+
 int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms) {
   if (!h || level < 0 || level >= h->L || reps < 1 || !avg_ms) { set_error("bad argument"); return STGMG_EINVAL; }
   if ((kind == 0 || kind == 2 || kind == 6 || kind == 7) && level < 1) {
     set_error("smoother kernels need level >= 1");
     return STGMG_EINVAL;
   }
+  if (kind == 8 && (level != h->L - 1 || h->m_alloc < 1)) {
+    set_error("kind 8 (MGS pass) needs the fine level and an allocated Krylov basis (run a solve first)");
+    return STGMG_EINVAL;
+  }
+  if (kind == 8) CKE(cudaMemsetAsync(h->scal + 12, 0, sizeof(double), h->s));   // h = 0: w is left unchanged
   LevelData& Lv = h->lev[level];
   auto one = [&]() -> int {
     if (kind == 0) {
@@ -2395,6 +2427,8 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
     } else if (kind == 7) {   // restriction to and prolongation from level - 1
       CK(restrict_level(h, level, Lv.r, h->lev[level - 1].b));
       CK(prolong_level(h, level, h->lev[level - 1].d, Lv.d));
+    } else if (kind == 8) {   // one fused MGS pass of K7 on the fine level: w -= h v_0, <w, v_1>
+      CK(dot(h, h->w, h->V, h->scal + 12, h->V + h->lev[h->L - 1].g.N, h->scal + 13, false));
     } else if (h->vgraph) {
       CKE(cudaGraphLaunch(h->vgraph, h->s));
     } else {

@@ -79,6 +79,8 @@ SIGNATURES = {
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "stgmg_time_kernel": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_double)]),
+    "stgmg_kernel_work": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double)]),
     "stgmg_partition_plan": (ctypes.c_int, [ctypes.POINTER(Mesh), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 6),
     "stgmg_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
@@ -335,11 +337,19 @@ class Solver:
 
     def time_kernel(self, kind, level=None, reps=20):
         """Average ms of one launch (kind 0 = K2 patch GEMM, 1 = K1 apply, 2 = K3 average, 3 = V-cycle,
-        4 / 5 = empty kernel, 6 = one smoothing sweep, 7 = restriction + prolongation)."""
+        4 / 5 = empty kernel, 6 = one smoothing sweep, 7 = restriction + prolongation, 8 = one MGS pass)."""
         lev = self.levels - 1 if level is None else level
         ms = ctypes.c_double()
         _check(self.lib.stgmg_time_kernel(self.h, kind, lev, reps, ctypes.byref(ms)), "stgmg_time_kernel")
         return ms.value
+
+    def kernel_work(self, kind, level=None):
+        """Algorithmic (flops, bytes) of one launch of time_kernel's kind (stgmg_kernel_work)."""
+        lev = self.levels - 1 if level is None else level
+        f, b = ctypes.c_double(), ctypes.c_double()
+        _check(self.lib.stgmg_kernel_work(self.h, int(kind), lev, ctypes.byref(f), ctypes.byref(b)),
+               "stgmg_kernel_work")
+        return f.value, b.value
 
     def launch_count(self):
         return int(self.lib.stgmg_last_launch_count(self.h))
