@@ -114,7 +114,7 @@ class SlabOperator:
 
     # spatial matrices (for closed-form pins) ---------------------------------------------------------
     def assemble_spatial(self):
-        """Global Mq (scalar Q_r mass), Mp, Mrho, Mc, A, C, B of the level (CSR)."""
+        """Global Mq (scalar Q_r mass), Mp, Mrho, Mc, A, C, B and Cvol (volume part of C) of the level (CSR)."""
         lev = self.lev
         d = lev.d
         out = {}
@@ -127,7 +127,8 @@ class SlabOperator:
         vec = np.concatenate([qn + c * lev.nq for c in range(d)], axis=1)
         spec = {"Mq": (qn, qn, lev.nq, lev.nq), "Mp": (pn, pn, lev.np_, lev.np_),
                 "Mrho": (vec, vec, lev.R, lev.R), "Mc": (pn, pn, lev.np_, lev.np_),
-                "A": (vec, vec, lev.R, lev.R), "C": (pn, vec, lev.np_, lev.R), "B": (pn, pn, lev.np_, lev.np_)}
+                "A": (vec, vec, lev.R, lev.R), "C": (pn, vec, lev.np_, lev.R), "B": (pn, pn, lev.np_, lev.np_),
+                "Cvol": (pn, vec, lev.np_, lev.R)}
         for name, (Rm, Cm, nr, nc) in spec.items():
             rows, cols, vals = [], [], []
             for ti, key in enumerate(self.type_keys):

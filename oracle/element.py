@@ -136,6 +136,7 @@ class ElementForms:
         A = np.einsum("Jqab,Iqab,q->IJ", sig, eps, w)
         div = np.trace(G, axis1=2, axis2=3)                    # (nv, nq)
         C = -p["alpha"] * np.einsum("Jq,sq,q->sJ", div, php, w)
+        Cvol = C.copy()                                       # volume part -alpha <div chi, q> only
         K = np.asarray(p["K"], dtype=np.float64).reshape(d, d)
         Kg = np.einsum("ab,sqb->sqa", K, gp)
         B = np.einsum("sqa,rqa,q->rs", Kg, gp, w)
@@ -161,7 +162,7 @@ class ElementForms:
                   + pen * np.einsum("sq,rq,q->rs", fphp, fphp, fw))
         Mrho = p["rho"] * np.kron(np.eye(d), Mq)
         Mc = p["c0"] * Mp
-        return {"Mq": Mq, "Mp": Mp, "Mrho": Mrho, "Mc": Mc, "A": A, "C": C, "B": B}
+        return {"Mq": Mq, "Mp": Mp, "Mrho": Mrho, "Mc": Mc, "A": A, "C": C, "B": B, "Cvol": Cvol}
 
 
 def slab_element_matrix(mats, T, th, ds=False):

@@ -192,16 +192,22 @@ def goal_quantities(lev, X, face):
     return bu, bp
 
 
-def slab_rhs(lev, spatial, chi_m1, th, U_prev, V_prev, P_prev, Floads, Gloads, ds=False):
+def slab_rhs(lev, spatial, chi_m1, th, U_prev, V_prev, P_prev, Floads, Gloads, ds=False, uD_trace=None):
     """Assemble F_n in ABI layout.  Floads[b], Gloads[b]: spatial loads at t_{n,b} (None = 0).
-    ds=True (Problem B.1): the jump term of the pressure equation adds -chi_b(-1) C U^{n-1} to the
-    psi-row (the u^- part of -C([u]_{n-1}, psi^+))."""
+    ds=True (Problem B.1, Eq:DPQ_3): the right-hand side of the pressure equation carries
+    <c0 p^{n-1} + alpha div u^{n-1}, psi^+(t_{n-1})> - alpha <u_D(t_{n-1}).n, psi^+(t_{n-1})>_{G_D^u}, i.e. at node b
+    chi_b(-1) (M_c P^{n-1} - Cvol U^{n-1}) - chi_b(-1) uD_trace, with Cvol = -alpha <div chi, q> (the volume part of
+    C) and uD_trace = alpha <u_D(t_{n-1}).n, xi_s>_{G_D^u} (None = 0: homogeneous Dirichlet data, readings A25/A26).
+    The discrete trace u_h^{n-1}.n does NOT enter the right-hand side (it does enter the operator through
+    -C(u^+(t_{n-1}), psi^+))."""
     Rv = np.zeros(lev.N)
     MU = spatial["Mrho"] @ U_prev
     MV = spatial["Mrho"] @ V_prev
     MP = spatial["Mc"] @ P_prev
     if ds:
-        MP = MP - spatial["C"] @ U_prev
+        MP = MP - spatial["Cvol"] @ U_prev
+        if uD_trace is not None:
+            MP = MP - uD_trace
     for b in range(lev.k + 1):
         o = b * lev.block
         Rv[o: o + lev.R] = chi_m1[b] * MU

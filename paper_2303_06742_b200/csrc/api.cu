@@ -190,6 +190,7 @@ static OpConsts make_consts(int d, int r, int k, const stgmg_params& p) {
     for (int a = 0; a <= k; ++a) c.T[b][a] = w[b] * dlag(t, a, t[b]) + c.chim1[a] * c.chim1[b];
   c.rho = p.rho; c.alpha = p.alpha; c.c0 = p.c0; c.lam = p.lambda; c.mu = p.mu;
   c.ds = p.formulation == STGMG_FORM_DS ? 1.0 : 0.0;
+  c.ds_face = 1.0;
   c.gamma_a = p.gamma_a < 0 ? 5.0e4 * r * (r + 1) : p.gamma_a;
   c.gamma_b = p.gamma_b < 0 ? 0.5 * r * (r - 1) : p.gamma_b;
   for (int i = 0; i < 9; ++i) c.K[i] = 0.0;
@@ -1742,6 +1743,9 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   }
   {
     OpConsts cj = h->c;
+    // DS (Problem B.1, Eq:DPQ_3 P:L1071-1073): the jump data of the p-equation are <c0 p^{n-1} + alpha div u^{n-1},
+    // psi^+> - alpha <u_D(t_{n-1}).n, psi^+>_{G_D^u}; u_D = 0 (readings A25/A26), so no trace term of u^{n-1}
+    cj.ds_face = 0.0;
     for (int b = 0; b < kMaxK1; ++b) {
       cj.theta[b] = 0.0;
       for (int a = 0; a < kMaxK1; ++a) cj.T[b][a] = (a == h->k1 - 1) ? h->c.chim1[b] : 0.0;

@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(OP2D_CPB * 4) op2d_cell_kernel(LevelGeom g, co
           nod[j] = s;
         }
         if (fa == 0) tp2<NQ1, 1, NF>(nod, Vn, Vq, Wq); else tp2<NQ1, NF, 1>(nod, Vn, Vq, Wq);
-        const double cth = ds ? 1.0 : th;
+        const double cth = ds ? c.ds_face : th;   // slab RHS (DS): 0, P:L1073 has u_D(t_{n-1}) = 0 there
 #pragma unroll
         for (int q = 0; q < NF; ++q) psiv[q] += -c.alpha * Vn[q] * nrm * cth * area * c.wg[q];
       }

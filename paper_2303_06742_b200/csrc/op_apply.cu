@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, const OpCons
               fgU[(i * D + l) * NF + q] = -th * Gc * w * hinv[l];
             }
           }
-          psi_val += -(c.ds != 0.0 ? 1.0 : th) * c.alpha * vn * w;
+          psi_val += -(c.ds != 0.0 ? c.ds_face : th) * c.alpha * vn * w;
         }
         if (dp) {
           double gpn = 0.0;

@@ -29,6 +29,8 @@ struct OpConsts {
   double rho, alpha, c0, lam, mu, gamma_a, gamma_b;
   double K[9];                 // row-major d x d (stride 3)
   double ds;                   // 1: Problem B.1 (DS) — psi rows couple sum_a T_ba U_a instead of theta_b V_b (N4)
+  double ds_face;              // DS only: weight of the G_D^u trace term alpha <(sum_a T_ba U_a).n, psi> (1 in the
+                               // operator; 0 in the slab-RHS constants: P:L1073 has u_D(t_{n-1}), not u_h^{n-1})
 };
 
 // Constants of the on-device load assembly and initial data (csrc/loads.cu).
