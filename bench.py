@@ -63,11 +63,9 @@ def dist_env():
 
 def load_label(cfg):
     if cfg["load"] == "beam":
-        return "beam traction (0,0,-sin(pi t/2)) on x=%g (reading A23), zero initial state; L_n assembled on the " \
-               "device each slab (stgmg_slab_load)" % cfg["hi"][0]
+        return "beam traction (0,0,-sin(pi t/2)) on x=%g (reading A23), zero initial state" % cfg["hi"][0]
     if cfg["load"] == "manufactured":
-        return "manufactured solution loads (BASELINE), interpolated initial data (A20); L_n assembled on the " \
-               "device each slab (stgmg_slab_load)"
+        return "manufactured solution loads (BASELINE), interpolated initial data (A20)"
     return "uniform[-1,1) seed %s (reading A21), zero initial state" % cfg["seed"]
 
 
@@ -156,29 +154,50 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
-def cpu_sample(cfg, iterations=1):
+def limit_blas():
+    """OpenBLAS on every logical CPU of a shared host is pathologically slow for the oracle's LAPACK calls (DESIGN.md
+    §3: a 1000^2 inverse 0.09 s on 4 threads, 1.4 s on 8 in the dev container); use half the CPUs, like the tests."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(max(1, (os.cpu_count() or 2) // 2))
+    except Exception:
+        return None
+
+
+def oracle_fine_setup(cfg):
     """The oracle as it stands (oracle/ebe.py: element-by-element operator, class-batched patch solves, no global
-    matrix) on the same workload: setup (untimed), the slab-1 right-hand side, then `iterations` FGMRES iterations
-    (each = one V-cycle + one operator apply + the MGS step).  MDoF*iter/s = N / (time per GMRES iteration), so the
-    bounded sample measures the metric directly.  Returns (value, seconds_per_iteration, sample description)."""
-    from oracle.ebe import EbeHierarchy, ebe_slab_rhs, fgmres_iterations
-    H = EbeHierarchy.from_config(cfg)
-    b = ebe_slab_rhs(H, cfg, 0)
+    matrix) on the bench workload: hierarchy, fine-level smoother (class inverses), slab-1 right-hand side.  Also the
+    extrapolation factor S = (K2 flops of one GMRES iteration's V-cycle) / (K2 flops of one fine-level sweep)."""
+    from oracle.ebe import EbeHierarchy, ebe_slab_rhs, vcycle_k2_flops, level_k2_flops
     t0 = time.perf_counter()
-    fgmres_iterations(H, b, iterations, restart=cfg["restart"])
-    dt = (time.perf_counter() - t0) / iterations
-    N = H.fine_op.lev.N
-    return N / dt / 1e6, dt, "%d FGMRES iteration(s) (V-cycle + apply + MGS) of slab 1 of %s, setup excluded, " \
-                             "%.2f s per iteration" % (iterations, cfg["name"], dt)
+    H = EbeHierarchy.from_config(cfg)
+    L = len(H.levels) - 1
+    sm = H.smoother(L)
+    b = ebe_slab_rhs(H, cfg, 0)
+    S = vcycle_k2_flops(H) / level_k2_flops(H.fine, H.params, H.tau)
+    return H, sm, b, S, time.perf_counter() - t0
 
 
 def cpu_baseline(cfg):
+    """Bounded sample: ONE full fine-level Alg. 1 sweep of the oracle (residual element by element, every patch solve,
+    averaging) on slab 1 of the workload.  A GMRES iteration = one V-cycle (+ one apply + MGS); its time is
+    extrapolated as t_sweep x S (S = V-cycle K2 flops / fine-sweep K2 flops; the patch solves are 95-99 % of the
+    flops), and MDoF*iter/s = N / t_iteration."""
+    _lim = limit_blas()
     try:
-        val, dt, sample = cpu_sample(cfg, 1)
+        H, sm, b, S, t_setup = oracle_fine_setup(cfg)
+        d = sm.sweep(b, None)                  # first sweep (r = b), as in Alg. 1 from d = 0
+        t0 = time.perf_counter()
+        sm.sweep(b, d)                         # a later sweep: residual + patch solves + averaging
+        dt = time.perf_counter() - t0
     except MemoryError as e:
         return {"value": None, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle",
                 "sample": "not run: %s" % e}
-    return {"value": val, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle", "sample": sample,
+    N = H.fine.N
+    return {"value": N / (dt * S) / 1e6, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle",
+            "sample": "one fine-level Alg. 1 sweep of slab 1 of %s (residual, all patch solves, averaging): %.2f s; "
+                      "GMRES iteration extrapolated as %.2f sweeps (V-cycle K2 flops / fine-sweep K2 flops); oracle "
+                      "setup %.1f s excluded" % (cfg["name"], dt, S, t_setup),
             "host": host_info()}
 
 
@@ -187,23 +206,36 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = config(args.config)
-    from oracle.ebe import EbeHierarchy, ebe_slab_rhs, fgmres_iterations
-    t_setup = time.perf_counter()
-    H = EbeHierarchy.from_config(cfg)
-    b = ebe_slab_rhs(H, cfg, 0)
-    t_setup = time.perf_counter() - t_setup
-    N = H.fine_op.lev.N
-    # one reference step = one FGMRES iteration of the slab solve (V-cycle + apply + MGS): MDoF*iter/s = N / t_step
-    for _ in range(args.warmup):
-        fgmres_iterations(H, b, 1, restart=cfg["restart"])
+    _lim = limit_blas()
+    H, sm, b, S, t_setup = oracle_fine_setup(cfg)
+    N = H.fine.N
+    nx = H.fine.n[0]
+    nslab = 8 if nx >= 16 else 1
+    edges = [nx * i // nslab for i in range(nslab)] + [nx + 1]
+    d = sm.sweep(b, None)
+    # one reference step = the fine-level sweep of one eighth of the patches (vertex x-index slab, rotating), its
+    # residual cells and local solves: nslab consecutive steps are one full sweep
+    state = {"i": 0}
+
+    def step():
+        k = state["i"] % nslab
+        sm.partial_sweep(b, d, edges[k], edges[k + 1])
+        state["i"] += 1
+
+    for _ in range(min(args.warmup, 1)):        # the CPU needs no warm-up beyond the first call
+        step()
+    state["i"] = 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        fgmres_iterations(H, b, 1, restart=cfg["restart"])
+        step()
     dt = time.perf_counter() - t0
-    val = N * args.steps / dt / 1e6
+    t_sweep = dt / args.steps * nslab
+    val = N / (t_sweep * S) / 1e6
     cores = blas_threads()
-    sample = ("%d steps, each one FGMRES iteration (V-cycle + operator apply + MGS) of slab 1 of %s, on the host "
-              "cores (oracle as it stands, oracle/ebe.py); setup %.1f s excluded" % (args.steps, cfg["name"], t_setup))
+    sample = ("%d steps, each the fine-level Alg. 1 sweep restricted to one of %d x-slabs of patches of slab 1 of %s "
+              "(rotating; %d steps = one sweep): sweep %.2f s; GMRES iteration extrapolated as %.2f sweeps (V-cycle "
+              "K2 flops / fine-sweep K2 flops); oracle as it stands (oracle/ebe.py) on the host cores; setup %.1f s "
+              "excluded" % (args.steps, nslab, cfg["name"], nslab, t_sweep, S, t_setup))
     out = {"impl": "reference", "metric": "slab_solve_throughput", "value": val, "unit": "MDoF*iter/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -406,7 +438,9 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong" if dd else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": workload_config(cfg, args, ws, dd),
-            "solve": {"gmres_iterations_total": its, "gmres_iterations_per_slab": its_list,
+            "solve": {"load_assembly": "on the device each slab (stgmg_slab_load + stgmg_slab_rhs, inside the timed "
+                                       "step)" if load_kind is not None else "host vector, resident on the device",
+                      "gmres_iterations_total": its, "gmres_iterations_per_slab": its_list,
                       "final_rel_residual_max": max(resid), "s_per_slab": t_max_s / args.steps,
                       "s_per_slab_each": [t * 1e-3 for t in per_step_ms], "setup_s": t_setup,
                       "vcycle_ms": vc_ms, "slabs_marched": state["n"],

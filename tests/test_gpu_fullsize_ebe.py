@@ -1,0 +1,87 @@
+"""Full-size parity of the whole solver at BASELINE sizes (configs 2 and 3; -m gpu), against the element-by-element
+oracle (oracle/ebe.py: the assembled oracle's definitions without a global matrix, pinned against it in
+tests/test_oracle_ebe.py).  North-star tolerances, on the bench's launch configuration (single GPU, default kernels):
+  * one V-cycle:     ||d_gpu - d_orc|| / ||d_orc|| <= 1e-8
+  * FGMRES solve:    iterations +-1, ||x_gpu - x_orc|| / ||x_orc|| <= 1e-8,
+                     ||r_gpu - r_orc|| / ||b|| <= 1e-10 with each side's own r = b - A x
+Right-hand sides: the configs' slab-1 F_1 (cfg3: manufactured loads + interpolated initial data, assembled by the
+oracle; the device's own F_1 is compared with it too; cfg2: the seed-2 U[-1,1) load, reading A21).
+The oracle runs on the host's cores (minutes); one module-scoped oracle solve per config.
+"""
+import numpy as np
+import pytest
+
+from stgmg_inputs import config
+from tests.gpu_common import to_gpu, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.fixture(scope="module", params=[3, 2], ids=["cfg3", "cfg2"])
+def case(request):
+    import torch
+    from threadpoolctl import threadpool_limits
+    import os
+    from paper_2303_06742_b200 import Solver
+    from oracle.ebe import EbeHierarchy, ebe_slab_rhs
+    from oracle.gmres import fgmres
+    cfg = config(request.param)
+    with threadpool_limits(max(1, (os.cpu_count() or 2) // 2)):
+        H = EbeHierarchy.from_config(cfg)
+        b = ebe_slab_rhs(H, cfg, 0)
+        d_orc = H.vcycle(b)
+        x_orc, info = fgmres(H.fine_op.apply, b, H.vcycle, tol=cfg["rtol"], restart=cfg["restart"])
+        r_orc = b - H.fine_op.apply(x_orc)
+    s = Solver(cfg)
+    yield dict(cfg=cfg, H=H, b=b, d_orc=d_orc, x_orc=x_orc, info=info, r_orc=r_orc, s=s)
+    s.close()
+    torch.cuda.synchronize()
+
+
+def test_fullsize_rhs(case):
+    """The device's slab-1 right-hand side (on-device loads + K8) equals the oracle's (cfg3)."""
+    import torch
+    cfg, s, b = case["cfg"], case["s"], case["b"]
+    if cfg["load"] != "manufactured":
+        pytest.skip("random load: the vector is an input")
+    from paper_2303_06742_b200.stgmg import LOAD_MANUFACTURED
+    N = s.size()
+    X0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+    L, F = torch.zeros_like(X0), torch.zeros_like(X0)
+    s.initial_state(LOAD_MANUFACTURED, 0.0, X0)
+    s.slab_load(LOAD_MANUFACTURED, 0.0, L)
+    s.slab_rhs(L, X0, F)
+    torch.cuda.synchronize()
+    assert rel(to_np(F), b) < 1e-12, rel(to_np(F), b)
+
+
+def test_fullsize_vcycle(case):
+    import torch
+    s, b = case["s"], case["b"]
+    d = torch.zeros(len(b), dtype=torch.float64, device="cuda")
+    s.vcycle(to_gpu(b), d)
+    torch.cuda.synchronize()
+    e = rel(to_np(d), case["d_orc"])
+    assert e <= 1e-8, e
+
+
+def test_fullsize_solve(case):
+    import torch
+    cfg, s, b, H = case["cfg"], case["s"], case["b"], case["H"]
+    x = torch.zeros(len(b), dtype=torch.float64, device="cuda")
+    st = s.solve(to_gpu(b), x, tol=cfg["rtol"], restart=cfg["restart"])
+    r_gpu = torch.zeros_like(x)
+    s.residual(to_gpu(b), x, r_gpu)
+    torch.cuda.synchronize()
+    xg = to_np(x)
+    assert st["converged"] and case["info"]["converged"]
+    assert abs(st["iterations"] - case["info"]["iterations"]) <= 1, (st["iterations"], case["info"]["iterations"])
+    assert rel(xg, case["x_orc"]) <= 1e-8, rel(xg, case["x_orc"])
+    nb = np.linalg.norm(b)
+    assert np.linalg.norm(to_np(r_gpu) - case["r_orc"]) / nb <= 1e-10
+    # the GPU iterate's residual evaluated by the oracle meets the tolerance too
+    assert np.linalg.norm(b - H.fine_op.apply(xg)) <= 1.01 * cfg["rtol"] * nb
