@@ -41,7 +41,7 @@ enum {
   STGMG_EINVAL = -1,       /* invalid argument: r<2, k<0, cells not divisible by 2^(levels-1), rho/c0/tau<=0, ... */
   STGMG_ENOMEM = -2,       /* device allocation failed */
   STGMG_ECUDA = -3,        /* CUDA runtime error; message carries cudaGetErrorString */
-  STGMG_ENCCL = -4,        /* reserved for the multi-GPU path */
+  STGMG_ENCCL = -4,        /* multi-GPU transport error (NCCL call failed / libnccl not loadable); message names it */
   STGMG_ESINGULAR = -5,    /* zero pivot in a patch-class or coarse inverse; message names level and class */
   STGMG_ECOVER = -6,       /* a DoF lies in no patch (p_mu == 0) */
   STGMG_ENOTSUP = -7       /* (d, r, k) combination not compiled into this library */
@@ -89,7 +89,8 @@ typedef struct {
   int smoother;                      /* STGMG_SMOOTH_ADDITIVE (default) | _COLORED_MULT | _ELEMENT | _OVERWRITE */
   void* nccl_comm;                   /* multi-GPU: ncclComm_t (STGMG_COMM_NCCL) or loopback hub; NULL if nranks = 1 */
   int rank, nranks;                  /* x-slab domain decomposition over nranks GPUs */
-  void* stream;                      /* cudaStream_t for all work; NULL = default stream */
+  void* stream;                      /* cudaStream_t for all work; NULL = a library-owned BLOCKING stream (ordered after
+                                        work queued on the legacy default stream; calls sync it before returning) */
   int comm_kind;                     /* STGMG_COMM_NCCL | STGMG_COMM_LOOPBACK */
   int formulation;                   /* STGMG_FORM_DSA (Problem 3.1, default) | STGMG_FORM_DS (Problem B.1) */
 } stgmg_params;
@@ -100,7 +101,10 @@ typedef struct {
   double rel_residual;    /* true ||b - A x|| / ||b|| at return */
   double abs_residual;    /* true ||b - A x|| at return */
   double seconds;         /* device time of the solve (CUDA events on params.stream) */
-  double level_seconds[16];/* reserved */
+  double level_seconds[16];/* [l] = iterations x device time of level l's share of one V-cycle (its sweeps, residual,
+                              transfers; level 0 / the folded level: the coarse solve), measured once per handle by an
+                              event-bracketed eager V-cycle after the first solve (outside `seconds`); 0 above L-1 and
+                              below the folded level (SPEC SolveStats) */
 } stgmg_stats;
 
 /* Build the level hierarchy, the matrix-free operators, the patch-class inverses (equilibrated LU /
@@ -116,7 +120,8 @@ int stgmg_local_size(const stgmg_handle* h, int level, int64_t* n_owned);
 
 /* Multi-GPU partition of level l (host-only, no GPU needed): global cells along x, window start (global cell),
  * owned cells [c0, c1) in window-local cell indices, window cells along x, and whether the level is split
- * (1) or agglomerated / replicated (0).  A level is split while every rank owns >= 4 cells along x. */
+ * (1) or agglomerated / replicated (0).  A level is split while every rank owns an even number >= 4 of cells along x
+ * and all finer levels are split. */
 int stgmg_partition_plan(const stgmg_mesh* mesh, int levels, int level, int rank, int nranks, int* split,
                          int* gnx, int* w0, int* c0, int* c1, int* nx_window);
 

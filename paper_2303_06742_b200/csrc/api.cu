@@ -15,11 +15,20 @@
 #include <functional>
 #include <memory>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/stgmg.h"
 #include "dist.cuh"
 #include "stgmg_internal.cuh"
 
 namespace stgmg {
+
+// NVTX range for the lifetime of a scope (host-side phases: setup steps, solve, Arnoldi steps, per-level timing
+// V-cycle).  Header-only NVTX v3; a no-op unless a profiler is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -424,6 +433,33 @@ struct stgmg_handle {
   bool graphable = true;
   bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; large 2D elements)
   int nsm = 148;                   // SMs of the device (tile balancing)
+  // per-level share of one V-cycle (stgmg_stats.level_seconds): events at entry / before the recursion / after it /
+  // exit of every level, recorded by one eager (not graph-launched) V-cycle after the first solve
+  bool lvprof = false, lev_ready = false;
+  cudaEvent_t lev_ev[16][4] = {};
+  double lev_ms[16] = {};
+
+  // Releases everything the handle owns: stgmg_destroy, and every error return of stgmg_setup (whose unique_ptr
+  // drops a partly built handle).  The caller's communicator and stream are not owned.
+  ~stgmg_handle() {
+    if (s) cudaStreamSynchronize(s);
+    if (vgraph) cudaGraphExecDestroy(vgraph);
+    if (cyc_exec) cudaGraphExecDestroy(cyc_exec);
+    if (vgraph_tmpl) cudaGraphDestroy(vgraph_tmpl);
+    for (auto g : vg_step)
+      if (g) cudaGraphExecDestroy(g);
+    for (void* p : allocs) cudaFree(p);
+    delete tr;
+    if (pinned) cudaFreeHost(pinned);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    for (auto e : pev)
+      if (e) cudaEventDestroy(e);
+    for (auto& le : lev_ev)
+      for (auto e : le)
+        if (e) cudaEventDestroy(e);
+    if (own_stream) cudaStreamDestroy(s);
+  }
 };
 
 static constexpr int kGhost = 3;   // ghost cells per interior side: one halo exchange of d per smoothing sweep
@@ -683,33 +719,73 @@ static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_s
 // V-cycle on levels top..0: input lev[top].b, output lev[top].d.  Below the fold level the assembled
 // sub-cycle matrix replaces the recursion (same linear map, applied as one GEMV).
 static int enqueue_levels(stgmg_handle* h, int top) {
+  auto mark = [&](int i) -> int {   // per-level timing V-cycle only (never inside a captured graph)
+    if (h->lvprof && top < 16) CKE(cudaEventRecord(h->lev_ev[top][i], h->s));
+    return 0;
+  };
+  CK(mark(0));
   if (top == 0) {
     CKE(launch_gemv(h->A0inv, h->n0, h->n0, h->lev[0].b, h->lev[0].d, h->s));
     h->launches += 1;
-    return 0;
+    return mark(3);
   }
   LevelData& Lv = h->lev[top];
   if (h->fold_ready && top == h->fold_lv) {
     CKE(launch_gemv(h->Vfold, (int)Lv.g.N, (int)Lv.g.N, Lv.b, Lv.d, h->s));
     h->launches += 1;
-    return 0;
+    return mark(3);
   }
   for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, top, Lv.b, Lv.d, j == 0));
   CK(residual(h, top, Lv.b, Lv.d, Lv.r));
   CK(restrict_level(h, top, Lv.r, h->lev[top - 1].b));
   if (Lv.part && h->lev[top - 1].part) CK(exchange(h, top - 1, h->lev[top - 1].b));
   else if (Lv.part) CK(agglomerate(h, top, h->lev[top - 1].b));
+  CK(mark(1));
   CK(enqueue_levels(h, top - 1));
+  CK(mark(2));
   CK(prolong_level(h, top, h->lev[top - 1].d, Lv.d));
   for (int j = 0; j < h->prm.jmax; ++j) CK(sweep(h, top, Lv.b, Lv.d, false));
-  return 0;
+  return mark(3);
 }
 
 static int enqueue_vcycle(stgmg_handle* h) { return enqueue_levels(h, h->L - 1); }
 
+// Per-level device time of one V-cycle (SPEC SolveStats' per-level smoother timings): level l's own
+// work = pre-smoothing, residual, restriction (+ halo / agglomeration) and prolongation + post-smoothing, i.e. the
+// time between its entry and exit events minus the coarser levels' recursion; level 0 (or the folded sub-cycle's
+// level) is the coarse solve.  Measured once per handle by an eager V-cycle on the levels' own b / d buffers.
+static int profile_levels(stgmg_handle* h) {
+  NvtxRange nv("stgmg level timing V-cycle");
+  if (!h->lev_ev[0][0])
+    for (auto& le : h->lev_ev)
+      for (auto& e : le) CKE(cudaEventCreate(&e));
+  for (int l = 0; l < h->L && l < 16; ++l) h->lev_ms[l] = 0.0;
+  h->lvprof = true;
+  const long long saved = h->launches;
+  const int rc = enqueue_vcycle(h);
+  h->lvprof = false;
+  h->launches = saved;
+  CK(rc);
+  CKE(cudaStreamSynchronize(h->s));
+  const int lo = h->fold_ready ? h->fold_lv : 0;
+  for (int l = lo; l < h->L && l < 16; ++l) {
+    float a = 0.f, b = 0.f;
+    if (l == lo) {
+      CKE(cudaEventElapsedTime(&a, h->lev_ev[l][0], h->lev_ev[l][3]));
+    } else {
+      CKE(cudaEventElapsedTime(&a, h->lev_ev[l][0], h->lev_ev[l][1]));
+      CKE(cudaEventElapsedTime(&b, h->lev_ev[l][2], h->lev_ev[l][3]));
+    }
+    h->lev_ms[l] = (double)a + (double)b;
+  }
+  h->lev_ready = true;
+  return 0;
+}
+
 // Assemble the folded sub-cycle: column i of Vfold (row-major, n x n) = the V-cycle of levels <= fold_lv applied to
 // e_i.  Chosen as the finest replicated level l >= 1 with n_l^2 doubles <= STGMG_FOLD_MB (64 MB by default; 0 = off).
 static int build_fold(stgmg_handle* h) {
+  NvtxRange nv("stgmg setup: fold");
   long long budget = 64ll << 20;
   if (const char* ev = std::getenv("STGMG_FOLD_MB")) budget = std::atoll(ev) << 20;
   h->fold_lv = 0;
@@ -814,6 +890,7 @@ std::vector<TileDesc> stgmg::balanced_tiles(const std::vector<int>& cp, const st
 }
 
 static int build_patches(stgmg_handle* h, int l) {
+  NvtxRange nv("stgmg setup: patch classes + inverses (K4)");
   LevelData& Lv = h->lev[l];
   const LevelGeom& g = Lv.g;
   const int d = h->d, r = h->r, k1 = h->k1;
@@ -1208,6 +1285,7 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
 }
 
 static int build_coarse(stgmg_handle* h) {
+  NvtxRange nv("stgmg setup: coarse inverse");
   const LevelGeom& g = h->lev[0].g;
   const long long N = g.N;
   h->n0 = (int)N;
@@ -1539,6 +1617,7 @@ static int build_small(stgmg_handle* h, int l) {
 }
 
 static int capture_vcycle(stgmg_handle* h) {
+  NvtxRange nv("stgmg setup: capture V-cycle graph");
   cudaGraph_t graph;
   const long long before = h->launches;
   CKE(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
@@ -1579,6 +1658,7 @@ const char* stgmg_last_error(void) { return g_last_error.c_str(); }
 
 int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, const stgmg_params* params,
                 stgmg_handle** out) {
+  NvtxRange nv("stgmg_setup");
   if (!mesh || !order || !params || !out) { set_error("null argument"); return STGMG_EINVAL; }
   const int d = mesh->dim, r = order->r, k = order->k;
   if ((d != 2 && d != 3) || r < 2 || r > 3 || k < 0 || k > 3 || levels < 1 || levels > 16) {
@@ -1655,7 +1735,8 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   if (params->stream) {
     h->s = (cudaStream_t)params->stream;
   } else {
-    CKE(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    // a BLOCKING stream: it orders itself after work the caller queued on the legacy default stream (stgmg.h)
+    CKE(cudaStreamCreateWithFlags(&h->s, cudaStreamDefault));
     h->own_stream = true;
   }
   h->c = make_consts(d, r, k, h->prm);
@@ -1676,9 +1757,11 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       Lv.ncell_global *= n[a];
     }
     // x-slab partition: a level is split while every rank owns >= 4 cells along x and all finer
-    // levels are split; coarser levels are agglomerated (replicated on every rank)
+    // levels are split; coarser levels are agglomerated (replicated on every rank).  A split level must own an
+    // EVEN number of cells per rank, so that rank q's cells coarsen onto exactly the coarse cells [q oc, (q+1) oc)
+    // whether or not the coarser level is split (agglomerate() relies on it).
     const bool finer_part = (l == levels - 1) || h->lev[l + 1].part;
-    Lv.part = nranks > 1 && l >= 1 && finer_part && n[0] % nranks == 0 && n[0] / nranks >= 4;
+    Lv.part = nranks > 1 && l >= 1 && finer_part && n[0] % (2 * nranks) == 0 && n[0] / nranks >= 4;
     int bcu[6], bcp[6];
     for (int f = 0; f < 6; ++f) { bcu[f] = mesh->bc_u[f]; bcp[f] = mesh->bc_p[f]; }
     if (Lv.part) {
@@ -1711,7 +1794,8 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     CKE(cudaMemset(Lv.r, 0, sizeof(double) * N));
   }
   if (nranks > 1 && !h->lev[levels - 1].part) {
-    set_error("multi-GPU: the fine level must split into >= 4 cells per rank along x (cells[0] % nranks == 0)");
+    set_error("multi-GPU: the fine level must split into an even number >= 4 of cells per rank along x "
+              "(cells[0] % (2 nranks) == 0)");
     return STGMG_EINVAL;
   }
   if (nranks > 1) {
@@ -1849,20 +1933,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
 }
 
 int stgmg_destroy(stgmg_handle* h) {
-  if (!h) return 0;
-  cudaStreamSynchronize(h->s);
-  if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
-  if (h->cyc_exec) cudaGraphExecDestroy(h->cyc_exec);
-  if (h->vgraph_tmpl) cudaGraphDestroy(h->vgraph_tmpl);
-  for (auto g : h->vg_step)
-    if (g) cudaGraphExecDestroy(g);
-  for (void* p : h->allocs) cudaFree(p);
-  delete h->tr;
-  if (h->pinned) cudaFreeHost(h->pinned);
-  if (h->e0) cudaEventDestroy(h->e0);
-  if (h->e1) cudaEventDestroy(h->e1);
-  if (h->own_stream) cudaStreamDestroy(h->s);
-  delete h;
+  delete h;   // ~stgmg_handle
   return 0;
 }
 
@@ -1938,6 +2009,7 @@ static int vcycle_dev(stgmg_handle* h, const double* b, double* x) {
 }
 
 int stgmg_vcycle(stgmg_handle* h, const double* b, double* x) {
+  NvtxRange nv("stgmg_vcycle");
   if (!h || !b || !x) { set_error("bad argument"); return STGMG_EINVAL; }
   h->launches = 0;
   CK(vcycle_dev(h, b, x));
@@ -2009,6 +2081,7 @@ int stgmg_goal_quantities(stgmg_handle* h, const double* x, int face, double* bu
 }
 
 int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, double* rhs) {
+  NvtxRange nv("stgmg_slab_rhs");
   if (!h || !x_prev || !rhs) { set_error("bad argument"); return STGMG_EINVAL; }
   const LevelGeom& g = h->lev[h->L - 1].g;
   h->launches = 0;
@@ -2219,6 +2292,7 @@ static int build_cycle_graph(stgmg_handle* h, int m) {
 
 int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int tol_mode, int restart, int maxit,
                 stgmg_stats* stats) {
+  NvtxRange nv("stgmg_solve");
   if (!h || !rhs || !x || restart < 1 || maxit < 1 || !(tol > 0)) { set_error("bad argument"); return STGMG_EINVAL; }
   CK(ensure_krylov(h, restart));
   const int Lf = h->L - 1;
@@ -2329,12 +2403,14 @@ int stgmg_solve(stgmg_handle* h, const double* rhs, double* x, double tol, int t
   }
   h->npev = 0;
   if (stats) {
+    if (!h->lev_ready && its > 0) CK(profile_levels(h));   // once per handle, outside the timed solve
     std::memset(stats, 0, sizeof(*stats));
     stats->iterations = its;
     stats->restarts = restarts;
     stats->abs_residual = beta;
     stats->rel_residual = bnorm > 0 ? beta / bnorm : 0.0;
     stats->seconds = ms * 1e-3;
+    for (int l = 0; l < h->L && l < 16; ++l) stats->level_seconds[l] = its * h->lev_ms[l] * 1e-3;
   }
   return converged ? STGMG_OK : STGMG_NOT_CONVERGED;
 }
@@ -2501,7 +2577,7 @@ int stgmg_partition_plan(const stgmg_mesh* mesh, int levels, int level, int rank
   int out[6] = {0, 0, 0, 0, 0, 0};
   for (int l = levels - 1; l >= level; --l) {
     const int n = mesh->cells[0] >> (levels - 1 - l);
-    const bool part = nranks > 1 && l >= 1 && finer && n % nranks == 0 && n / nranks >= 4;
+    const bool part = nranks > 1 && l >= 1 && finer && n % (2 * nranks) == 0 && n / nranks >= 4;   // as stgmg_setup
     finer = part;
     if (l == level) {
       if (part) {

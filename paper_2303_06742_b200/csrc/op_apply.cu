@@ -257,11 +257,11 @@ static cudaError_t launch_impl(const LevelGeom& g, const OpConsts* cdev, const d
   using T = Tr<D, R, K1>;
   const int wpb = 4;
   const size_t smem = (size_t)wpb * T::SMEM * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(op_apply_kernel<D, R, K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  static PerDeviceOnce attr;
+  attr.run([] {
+    cudaFuncSetAttribute(op_apply_kernel<D, R, K1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+  });
   for (int color = 0; color < (1 << D); ++color) {
     long long ncol = 1;
     for (int a = 0; a < D; ++a) ncol *= (g.n[a] - ((color >> a) & 1) + 1) / 2;

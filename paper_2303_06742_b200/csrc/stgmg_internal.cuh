@@ -2,11 +2,31 @@
 // Public ABI: include/stgmg.h.  Paper references: P:Ln = line n of PAPER.md (arXiv:2303.06742).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
 namespace stgmg {
+
+// Per-device "done once" flag: function attributes (dynamic shared memory opt-in) belong to each device's context,
+// so a second handle on another GPU of the same process must set them again.  Race-free across host threads.
+struct PerDeviceOnce {
+  std::atomic<unsigned long long> mask{0};
+  std::mutex mu;
+  // runs f() once per device; concurrent callers wait until it has finished
+  template <class F> void run(F f) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    if (mask.load(std::memory_order_acquire) & bit) return;
+    std::lock_guard<std::mutex> g(mu);
+    if (mask.load(std::memory_order_relaxed) & bit) return;
+    f();
+    mask.fetch_or(bit, std::memory_order_release);
+  }
+};
 
 constexpr int kMaxR1 = 4;   // max nodes per axis of a Q_r cell (r <= 3)
 constexpr int kMaxK1 = 4;   // max Radau nodes (k <= 3)

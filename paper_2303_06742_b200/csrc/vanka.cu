@@ -249,12 +249,11 @@ __global__ void __launch_bounds__(32 * WM * WN * KS, (MT * NT <= 16 ? 2 : 1)) pa
 template <int WM, int WN, int MT, int NT, int ST, int KS>
 static void k2_set_attr() {
   using C = K2Cfg<WM, WN, MT, NT, ST, KS>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([] {
     cudaFuncSetAttribute(patch_gemm_kernel<WM, WN, MT, NT, ST, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM);
-    attr = true;
-  }
+  });
 }
 
 template <int WM, int WN, int MT, int NT, int ST, int KS>
@@ -450,12 +449,11 @@ template <int WM, int WN, int MT, int NT, int S, int KS>
 static cudaError_t launch_k2d(const LevelGeom& g, const PatchClass* cls_dev, const TileDesc* tiles, int ntiles,
                               const double* invc, int lda, const double* rexp, double* Y, int ldy, cudaStream_t s) {
   using C = K2DCfg<WM, WN, MT, NT, S, KS>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([] {
     cudaFuncSetAttribute(patch_gemm_dense_kernel<WM, WN, MT, NT, S, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM);
-    attr = true;
-  }
+  });
   return launch_pdl(patch_gemm_dense_kernel<WM, WN, MT, NT, S, KS>, dim3(ntiles), dim3(C::THREADS), C::SMEM, s, g,
                     cls_dev, tiles, invc, lda, rexp, Y, ldy);
 }
@@ -804,11 +802,11 @@ static cudaError_t launch_k2s(const LevelGeom& g, int r, const PatchClass* cls_d
                               const int* relidx, const double* invc, int lda, const double* rvec, double* Y, int ldy,
                               cudaStream_t s) {
   if (lda > K2S_MAXLDA) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(patch_gemm_smb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2s_smem(K2S_MAXLDA));
-    attr = true;
-  }
+  static PerDeviceOnce attr;
+  attr.run([] {
+    cudaFuncSetAttribute(patch_gemm_smb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)k2s_smem(K2S_MAXLDA));
+  });
   return launch_pdl(patch_gemm_smb_kernel, dim3(ntiles), dim3(32 * K2S_NW), k2s_smem(lda), s, g, r, cls_dev, tiles,
                     relidx, invc, lda, rvec, Y, ldy);
 }

@@ -44,7 +44,7 @@ class Stats(ctypes.Structure):
 
     def as_dict(self):
         return dict(iterations=self.iterations, restarts=self.restarts, rel_residual=self.rel_residual,
-                    abs_residual=self.abs_residual, seconds=self.seconds)
+                    abs_residual=self.abs_residual, seconds=self.seconds, level_seconds=list(self.level_seconds))
 
 
 # name -> (restype, argtypes) — every symbol declared in include/stgmg.h
@@ -122,14 +122,42 @@ def _check(rc, what):
     return rc
 
 
-def _ptr(t):
-    """Device pointer of a CUDA float64 torch tensor (contiguous)."""
+def _ptr(t, n=None, device=None):
+    """Device pointer of a contiguous CUDA float64 torch tensor, checked against the ABI's expectations: exactly n
+    elements (the level's stgmg_local_size) on the solver's device.  Wrong arguments raise instead of letting the
+    library read or write out of bounds."""
     import torch
     if not isinstance(t, torch.Tensor):
         raise TypeError("expected a torch.Tensor")
     if not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise TypeError("expected a contiguous CUDA float64 tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError("tensor has %d elements, the level vector has %d" % (t.numel(), n))
+    if device is not None and t.device != device:
+        raise ValueError("tensor on %s, solver on %s" % (t.device, device))
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _host_ptr(a, n):
+    """Host pointer of a C-contiguous float64 CPU array (numpy or torch) of exactly n elements."""
+    import numpy as np
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous():
+                raise TypeError("expected a contiguous CPU float64 tensor")
+            if a.numel() != n:
+                raise ValueError("host tensor has %d elements, expected %d" % (a.numel(), n))
+            return ctypes.c_void_p(a.data_ptr())
+    except ImportError:
+        pass
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+        raise TypeError("expected a C-contiguous float64 numpy array or CPU tensor")
+    if a.size != n:
+        raise ValueError("host array has %d elements, expected %d" % (a.size, n))
+    if not a.flags["WRITEABLE"]:
+        raise ValueError("host array must be writeable")
+    return a.ctypes.data_as(ctypes.c_void_p)
 
 
 COMM_NCCL, COMM_LOOPBACK = 0, 1
@@ -233,6 +261,21 @@ class Solver:
         _check(self.lib.stgmg_setup(ctypes.byref(m), self.levels, ctypes.byref(o), ctypes.byref(p), ctypes.byref(h)),
                "stgmg_setup")
         self.h = h
+        self.device = self.stream.device
+        self._n = []
+        for lev in range(self.levels):
+            n = ctypes.c_int64()
+            _check(self.lib.stgmg_local_size(self.h, lev, ctypes.byref(n)), "stgmg_local_size")
+            self._n.append(n.value)
+
+    def _lev(self, level):
+        lev = self.levels - 1 if level is None else int(level)
+        if not 0 <= lev < self.levels:
+            raise ValueError("level %d outside 0..%d" % (lev, self.levels - 1))
+        return lev
+
+    def _p(self, t, level=None):
+        return _ptr(t, self._n[self._lev(level)], self.device)
 
     def close(self):
         if getattr(self, "h", None):
@@ -257,29 +300,36 @@ class Solver:
         return dict(n_classes=nc.value, max_patch_dofs=mx.value, n_patches=npat.value)
 
     def apply(self, x, y, level=None):
-        lev = self.levels - 1 if level is None else level
-        _check(self.lib.stgmg_apply_operator(self.h, lev, _ptr(x), _ptr(y)), "stgmg_apply_operator")
+        lev = self._lev(level)
+        _check(self.lib.stgmg_apply_operator(self.h, lev, self._p(x, lev), self._p(y, lev)), "stgmg_apply_operator")
 
     def residual(self, b, x, r, level=None):
-        lev = self.levels - 1 if level is None else level
-        _check(self.lib.stgmg_residual(self.h, lev, _ptr(b), _ptr(x), _ptr(r)), "stgmg_residual")
+        lev = self._lev(level)
+        _check(self.lib.stgmg_residual(self.h, lev, self._p(b, lev), self._p(x, lev), self._p(r, lev)),
+               "stgmg_residual")
 
     def smooth_sweep(self, b, d, level=None):
-        lev = self.levels - 1 if level is None else level
-        _check(self.lib.stgmg_smooth_sweep(self.h, lev, _ptr(b), _ptr(d)), "stgmg_smooth_sweep")
+        lev = self._lev(level)
+        _check(self.lib.stgmg_smooth_sweep(self.h, lev, self._p(b, lev), self._p(d, lev)), "stgmg_smooth_sweep")
 
     def restrict(self, level, rf, bc):
-        _check(self.lib.stgmg_restrict(self.h, level, _ptr(rf), _ptr(bc)), "stgmg_restrict")
+        lev = self._lev(level)
+        if lev < 1:
+            raise ValueError("restriction needs level >= 1")
+        _check(self.lib.stgmg_restrict(self.h, lev, self._p(rf, lev), self._p(bc, lev - 1)), "stgmg_restrict")
 
     def prolong_add(self, level, dc, df):
-        _check(self.lib.stgmg_prolong_add(self.h, level, _ptr(dc), _ptr(df)), "stgmg_prolong_add")
+        lev = self._lev(level)
+        if lev < 1:
+            raise ValueError("prolongation needs level >= 1")
+        _check(self.lib.stgmg_prolong_add(self.h, lev, self._p(dc, lev - 1), self._p(df, lev)), "stgmg_prolong_add")
 
     def vcycle(self, b, x):
-        _check(self.lib.stgmg_vcycle(self.h, _ptr(b), _ptr(x)), "stgmg_vcycle")
+        _check(self.lib.stgmg_vcycle(self.h, self._p(b), self._p(x)), "stgmg_vcycle")
 
     def solve(self, rhs, x, tol=None, tol_mode=TOL_REL, restart=None, maxit=1000):
         st = Stats()
-        rc = _check(self.lib.stgmg_solve(self.h, _ptr(rhs), _ptr(x), float(tol if tol else self.cfg["rtol"]),
+        rc = _check(self.lib.stgmg_solve(self.h, self._p(rhs), self._p(x), float(tol if tol else self.cfg["rtol"]),
                                          tol_mode, int(restart or self.cfg["restart"]), int(maxit), ctypes.byref(st)),
                     "stgmg_solve")
         out = st.as_dict()
@@ -289,14 +339,9 @@ class Solver:
     def solve_host(self, rhs_host, x_host, tol=None, tol_mode=TOL_REL, restart=None, maxit=1000):
         """rhs_host, x_host: contiguous float64 CPU tensors (pinned for speed) or numpy arrays."""
         st = Stats()
-
-        def hp(a):
-            try:
-                return ctypes.c_void_p(a.data_ptr())
-            except AttributeError:
-                return a.ctypes.data_as(ctypes.c_void_p)
-
-        rc = _check(self.lib.stgmg_solve_host(self.h, hp(rhs_host), hp(x_host), float(tol if tol else self.cfg["rtol"]),
+        n = self._n[-1]
+        rc = _check(self.lib.stgmg_solve_host(self.h, _host_ptr(rhs_host, n), _host_ptr(x_host, n),
+                                              float(tol if tol else self.cfg["rtol"]),
                                               tol_mode, int(restart or self.cfg["restart"]), int(maxit),
                                               ctypes.byref(st)), "stgmg_solve_host")
         out = st.as_dict()
@@ -304,27 +349,27 @@ class Solver:
         return out
 
     def slab_rhs(self, load, x_prev, rhs):
-        lp = _ptr(load) if load is not None else None
-        _check(self.lib.stgmg_slab_rhs(self.h, lp, _ptr(x_prev), _ptr(rhs)), "stgmg_slab_rhs")
+        lp = self._p(load) if load is not None else None
+        _check(self.lib.stgmg_slab_rhs(self.h, lp, self._p(x_prev), self._p(rhs)), "stgmg_slab_rhs")
 
     def slab_load(self, kind, t_n, load):
         """L_n of the slab (t_n, t_n + tau] assembled on the device (LOAD_MANUFACTURED / LOAD_BEAM_TRACTION)."""
-        _check(self.lib.stgmg_slab_load(self.h, int(kind), float(t_n), _ptr(load)), "stgmg_slab_load")
+        _check(self.lib.stgmg_slab_load(self.h, int(kind), float(t_n), self._p(load)), "stgmg_slab_load")
 
     def initial_state(self, kind, t0, x):
         """x = 0 except the last Radau block = interpolated initial data (reading A20)."""
-        _check(self.lib.stgmg_initial_state(self.h, int(kind), float(t0), _ptr(x)), "stgmg_initial_state")
+        _check(self.lib.stgmg_initial_state(self.h, int(kind), float(t0), self._p(x)), "stgmg_initial_state")
 
     def energy(self, x):
         """A_gamma(U,U) + <rho V,V> + <c0 P,P> of the last Radau block of x (host float)."""
         e = ctypes.c_double()
-        _check(self.lib.stgmg_energy(self.h, _ptr(x), ctypes.byref(e)), "stgmg_energy")
+        _check(self.lib.stgmg_energy(self.h, self._p(x), ctypes.byref(e)), "stgmg_energy")
         return e.value
 
     def goal_quantities(self, x, face):
         """SURVEY N1 / Eq:DefGQ: (b_u, b_p) = (int_face u.n, int_face p) of the last Radau block of x."""
         bu, bp = ctypes.c_double(), ctypes.c_double()
-        _check(self.lib.stgmg_goal_quantities(self.h, _ptr(x), int(face), ctypes.byref(bu), ctypes.byref(bp)),
+        _check(self.lib.stgmg_goal_quantities(self.h, self._p(x), int(face), ctypes.byref(bu), ctypes.byref(bp)),
                "stgmg_goal_quantities")
         return bu.value, bp.value
 

@@ -103,3 +103,30 @@ def test_setup_rejects_invalid_arguments(case):
 def test_setup_rejects_bad_level_count():
     assert _setup_rc(lambda m, o, p: None, levels=0)[0] == -1
     assert _setup_rc(lambda m, o, p: None, levels=17)[0] == -1
+
+
+def test_partition_plan_even_split_feeds_agglomeration():
+    """stgmg_partition_plan (host-only): a split level owns an even number >= 4 of cells per rank, so rank q's fine
+    cells coarsen onto exactly the coarse cells [q oc, (q+1) oc) (agglomerate(); 40 cells, 4 levels,
+    2 ranks used to split the 10-cell level into 5 + 5 with oc = 2).  Windows tile the global level."""
+    from paper_2303_06742_b200.stgmg import partition_plan
+    from stgmg_inputs import config
+    cfg = config(4)
+    cases = [(40, 4, 2), (256, 6, 8), (256, 6, 2), (48, 4, 3), (24, 3, 2), (96, 5, 4)]
+    for nx, levels, P in cases:
+        cfg = dict(cfg, cells=(nx, 4, 4), levels=levels)
+        splits = []
+        for lev in range(levels):
+            plans = [partition_plan(cfg, lev, q, P) for q in range(P)]
+            split = plans[0]["split"]
+            assert all(p["split"] == split for p in plans)
+            n = nx >> (levels - 1 - lev)
+            if split:
+                own = [p["c1"] - p["c0"] for p in plans]
+                assert own == [n // P] * P and (n // P) % 2 == 0 and n // P >= 4, (nx, levels, P, lev, own)
+                assert [p["w0"] + p["c0"] for p in plans] == [q * (n // P) for q in range(P)]
+            splits.append(split)
+        # split levels form a suffix (fine end) of the hierarchy, never level 0
+        assert splits[0] == 0 and splits == sorted(splits)
+    cfg = dict(cfg, cells=(40, 4, 4), levels=4)
+    assert [partition_plan(cfg, l, 0, 2)["split"] for l in range(4)] == [0, 0, 1, 1]

@@ -153,3 +153,48 @@ def test_single_level_is_a_direct_solve():
     assert st["converged"] and st["iterations"] == 1
     assert np.linalg.norm(to_np(x) - xd) <= 1e-9 * np.linalg.norm(xd)
     s.close()
+
+
+def test_level_seconds_filled(pair):
+    """stgmg_stats.level_seconds (SPEC SolveStats per-level smoother timings): positive on every level
+    that runs its own work (the folded sub-cycle, if any, is booked on the fold level), zero above the hierarchy, and
+    their sum below the solve's own device time (the V-cycles are part of it)."""
+    import torch
+    cfg, s, H = pair
+    b = to_gpu(uniform_load(H.fine.N, 95))
+    x = torch.zeros(H.fine.N, dtype=torch.float64, device="cuda")
+    st = s.solve(b, x, tol=cfg["rtol"], restart=cfg["restart"])
+    st = s.solve(b, torch.zeros_like(x), tol=cfg["rtol"], restart=cfg["restart"])
+    ls = st["level_seconds"]
+    lo = s.fold_level()
+    L = cfg["levels"]
+    assert all(ls[l] > 0 for l in range(lo, L)), ls
+    assert all(ls[l] == 0 for l in range(L, 16)) and all(ls[l] == 0 for l in range(0, lo)), ls
+    assert sum(ls) < 1.5 * st["seconds"], (sum(ls), st["seconds"])
+
+
+def test_binding_rejects_bad_buffers(pair):
+    """The binding validates every pointer before the ABI call: wrong length, dtype, device, layout."""
+    import torch
+    cfg, s, H = pair
+    N = H.fine.N
+    good = torch.zeros(N, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        s.vcycle(torch.zeros(N - 1, dtype=torch.float64, device="cuda"), good)
+    with pytest.raises(TypeError):
+        s.vcycle(torch.zeros(N, dtype=torch.float32, device="cuda"), good)
+    with pytest.raises(TypeError):
+        s.vcycle(torch.zeros(N, dtype=torch.float64), good)
+    with pytest.raises(TypeError):
+        s.vcycle(torch.zeros(2 * N, dtype=torch.float64, device="cuda")[::2], good)
+    with pytest.raises(ValueError):
+        s.apply(good, torch.zeros(s.size(0), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        s.restrict(1, torch.zeros(s.size(1), dtype=torch.float64, device="cuda"),
+                   torch.zeros(s.size(1), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        s.solve_host(np.zeros(N), np.zeros(N - 3))
+    with pytest.raises(TypeError):
+        s.solve_host(np.zeros(N), np.zeros(N, dtype=np.float32))
+    with pytest.raises(TypeError):
+        s.solve_host(np.zeros(N), good)
