@@ -19,6 +19,7 @@ Modules
   transfer   prolongation by interpolation, restriction = transpose
   vanka      vertex patches, A_P, equilibrated inverses, Algorithm 1
   mg         V-cycle
+  lshape     3D L-shape benchmark: Q_r^d / P_{r-1}^disc, SIP B_gamma, directional BCs
   gmres      flexible GMRES(m), right preconditioned
   loads      load functionals, slab RHS, initial data, manufactured solutions
   errors     space-time error norms for the Tab:3 / Tab:App1 pins
