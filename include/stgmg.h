@@ -59,7 +59,8 @@ enum { STGMG_SMOOTH_ADDITIVE = 0 /* Alg. 1 with averaging, P:L488-524 (default) 
 enum { STGMG_FORM_DSA = 0 /* Problem 3.1 (Eq:DPQ_A0): p-equation couples v (default) */,
        STGMG_FORM_DS = 1 /* Problem B.1: p-equation couples d_t u through T, slab RHS
                             adds -chi_b(-1) C U^{n-1} (stgmg_slab_rhs) */ };
-enum { STGMG_LOAD_MANUFACTURED = 0, STGMG_LOAD_BEAM_TRACTION = 1 };   /* stgmg_slab_load */
+enum { STGMG_LOAD_MANUFACTURED = 0, STGMG_LOAD_BEAM_TRACTION = 1,   /* stgmg_slab_load */
+       STGMG_LOAD_LSHAPE_TRACTION = 2 /* Sec. 5.2 traction on the L-shape (stgmg_setup_lshape handles only) */ };
 enum { STGMG_COMM_NCCL = 0 /* nccl_comm is an ncclComm_t */,
        STGMG_COMM_LOOPBACK = 1 /* nccl_comm is an in-process hub (N emulated ranks on one GPU; tests) */ };
 
@@ -113,6 +114,23 @@ typedef struct {
  * Errors: EINVAL (parameters), ENOMEM, ECUDA, ESINGULAR, ECOVER, ENOTSUP. */
 int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, const stgmg_params* params,
                 stgmg_handle** out);
+
+/* the 3D L-shaped benchmark of Sec. 5.2 with the Q_r^d / P_{r-1}^disc pair
+ * (Def:VhQh P:L130-148; B_gamma = the symmetric interior penalty option of Def:B; directional conditions
+ * Eq:BCd P:L757-781).  Domain ([0,1] x [0,.5] U [0,.5] x [.5,1]) x [0,.5] with 2^ref_fine cells per cube edge on the
+ * fine level; levels = ref_fine - ref_coarse + 1 (Table 4: coarse level ref_1).  Boundary parts as DESIGN.md
+ * readings N3-R1/R2: u = 0 on y = 0; directional on x = 0 and z = 0, .5; traction t_N on y = 1 (x < .5); free on
+ * x = 1 and the re-entrant faces; p = 0 on y = 1 (x < .5), no flux elsewhere.  params: rho, alpha, c0, lambda, mu, K,
+ * tau, gamma_a, gamma_b (gamma = gamma_b of the SIP term), omega, jmax, stream (mesh, bc, hF_mode, smoother,
+ * formulation and nranks are not used: single GPU, Alg. 1, Problem 3.1).  Level operators are assembled (CSR) on the
+ * host at setup from element integrals; every patch has its own explicit inverse (K4 on the device).  Vector layout per
+ * Radau node: V_0..V_2, U_0..U_2 on the active Q_r nodes (lexicographic over the (2 r 2^ref + 1)^2 (r 2^ref + 1) node
+ * grid, x fastest), then P (dim P_{r-1} monomials per active cell, cells lexicographic).  All other entry points
+ * accept the handle except stgmg_energy / stgmg_level_work / stgmg_kernel_work / stgmg_time_kernel (ENOTSUP);
+ * stgmg_slab_load takes STGMG_LOAD_LSHAPE_TRACTION, stgmg_goal_quantities face 1 (Gamma_m, Eq:DefGQ).
+ * Errors: EINVAL, ENOTSUP (r, k, nranks > 1, smoother / formulation variants), ENOMEM, ECUDA, ESINGULAR, ECOVER. */
+int stgmg_setup_lshape(int ref_fine, int levels, const stgmg_order* order, const stgmg_params* params,
+                       stgmg_handle** out);
 
 /* Number of slab DoFs N_l of a level (0 = coarse .. levels-1 = fine).  Multi-GPU: the DoFs of the rank's x-window
  * (owned cells plus 3 ghost cells per interior side); vectors passed to the library use this local numbering. */

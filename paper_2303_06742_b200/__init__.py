@@ -4,6 +4,6 @@ The product is libstgmg.so (C ABI: include/stgmg.h, CUDA sources: csrc/).  ``Sol
 PyTorch is only used for device memory and streams.  There is no CPU fallback.
 """
 from .build import build, LIB
-from .stgmg import Solver, StgmgError, load_library, SIGNATURES, TOL_REL, TOL_ABS
+from .stgmg import Solver, LShapeSolver, StgmgError, load_library, SIGNATURES, TOL_REL, TOL_ABS
 
-__all__ = ["build", "LIB", "Solver", "StgmgError", "load_library", "SIGNATURES", "TOL_REL", "TOL_ABS"]
+__all__ = ["build", "LIB", "Solver", "LShapeSolver", "StgmgError", "load_library", "SIGNATURES", "TOL_REL", "TOL_ABS"]

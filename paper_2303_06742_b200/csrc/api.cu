@@ -369,6 +369,14 @@ struct LevelData {
   int n_exp_blocks = 0;
   int2* colbase = nullptr;      // per patch column (class-major): gather bases (bq, bp)
   bool exp_fused = false;       // STGMG_EXPAND_FUSED=1: the push-form gather_expand instead
+  // unstructured level (SURVEY N3, L-shape): CSR operator / transfers / averaging table above, plus one explicit
+  // inverse per vertex patch (K2u, csrc/lshape.cu)
+  bool unstr = false;
+  int* pz = nullptr;            // concatenated Z(P)
+  long long* pzoff = nullptr;   // start of Z(P) and of y_P
+  int* pcp = nullptr;           // C_P
+  double* pinv = nullptr;       // npatch x plda x plda, row-major
+  int plda = 0, pmax = 0;
 };
 
 struct stgmg_handle {
@@ -433,6 +441,13 @@ struct stgmg_handle {
   bool graphable = true;
   bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; large 2D elements)
   int nsm = 148;                   // SMs of the device (tile balancing)
+  // the 3D L-shaped benchmark (stgmg_setup_lshape); levels are unstructured (LevelData::unstr)
+  bool lshape = false;
+  int ls_nq = 0, ls_np = 0;
+  int *J_rp = nullptr, *J_ci = nullptr, J_lpr = 32;   // slab-RHS coupling F = L + J X_{n-1}
+  double* J_v = nullptr;
+  double *ls_fN = nullptr, *ls_wu = nullptr, *ls_wp = nullptr;
+  double ls_that[kMaxK1] = {};     // right Radau nodes on [-1, 1]
   // per-level share of one V-cycle (stgmg_stats.level_seconds): events at entry / before the recursion / after it /
   // exit of every level, recorded by one eager (not graph-launched) V-cycle after the first solve
   bool lvprof = false, lev_ready = false;
@@ -696,6 +711,16 @@ static int residual_expand(stgmg_handle* h, int l, const double* b, const double
 static int sweep(stgmg_handle* h, int l, const double* b, double* d, bool zero_start) {
   if (h->prm.smoother == STGMG_SMOOTH_COLORED_MULT) return sweep_colored(h, l, b, d, zero_start);
   LevelData& L = h->lev[l];
+  if (L.unstr) {   // L-shape level: CSR residual, per-patch inverses (K2u), averaging table
+    const double* rin = b;
+    if (!zero_start) {
+      CK(residual(h, l, b, d, L.r));
+      rin = L.r;
+    }
+    CKE(launch_patch_gemv((int)L.npatch, L.pmax, L.pz, L.pzoff, L.pcp, L.pinv, L.plda, rin, L.Y, h->s));
+    h->launches += 1;
+    return average_level(h, l, zero_start, d);
+  }
   if (L.dense) {
     CK(residual_expand(h, l, b, zero_start ? nullptr : d));
     CKE(launch_patch_gemm_dense(L.g, L.k2var, L.cls_dev, L.tiles_dev, L.ntiles, L.inv_dev, L.lda, L.Rexp, L.Y, L.ldy,
@@ -786,6 +811,7 @@ static int profile_levels(stgmg_handle* h) {
 // e_i.  Chosen as the finest replicated level l >= 1 with n_l^2 doubles <= STGMG_FOLD_MB (64 MB by default; 0 = off).
 static int build_fold(stgmg_handle* h) {
   NvtxRange nv("stgmg setup: fold");
+  if (h->lshape) return 0;   // unstructured levels: no fold
   long long budget = 64ll << 20;
   if (const char* ev = std::getenv("STGMG_FOLD_MB")) budget = std::atoll(ev) << 20;
   h->fold_lv = 0;
@@ -1656,15 +1682,41 @@ extern "C" {
 
 const char* stgmg_last_error(void) { return g_last_error.c_str(); }
 
-int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, const stgmg_params* params,
-                stgmg_handle** out) {
-  NvtxRange nv("stgmg_setup");
-  if (!mesh || !order || !params || !out) { set_error("null argument"); return STGMG_EINVAL; }
-  const int d = mesh->dim, r = order->r, k = order->k;
-  if ((d != 2 && d != 3) || r < 2 || r > 3 || k < 0 || k > 3 || levels < 1 || levels > 16) {
-    set_error("invalid dim / order / levels (d in {2,3}, 2 <= r <= 3, 0 <= k <= 3)");
-    return STGMG_EINVAL;
+// Setup steps shared by every hierarchy: Krylov / reduction workspace, events, the folded coarse sub-cycle, the
+// V-cycle graph.
+static int finish_setup(stgmg_handle* h) {
+  const long long Nf = h->lev[h->L - 1].g.N;
+  CK(dalloc(h, &h->w, (size_t)Nf));
+  CK(dalloc(h, &h->rv, (size_t)Nf));
+  CK(dalloc(h, &h->stage_rhs, (size_t)Nf));
+  CK(dalloc(h, &h->stage_x, (size_t)Nf));
+  CK(dalloc(h, &h->rhs_int, (size_t)Nf));
+  CK(dalloc(h, &h->scal, 16));
+  CK(dalloc(h, &h->partials, 2048));
+  CK(dalloc(h, &h->counter, 4));
+  CKE(cudaMemset(h->counter, 0, 4 * sizeof(unsigned)));
+  CKE(cudaMallocHost(&h->pinned, 16 * sizeof(double)));
+  CKE(cudaEventCreate(&h->e0));
+  CKE(cudaEventCreate(&h->e1));
+  CK(build_fold(h));
+  if (const char* ev = std::getenv("STGMG_STEP_GRAPHS")) h->step_graphs = std::atoi(ev) != 0;
+  if (std::getenv("STGMG_PROFILE_SOLVE")) {
+    h->prof = true;
+    for (auto& e : h->pev) CKE(cudaEventCreate(&e));
   }
+  if (const char* ev = std::getenv("STGMG_SOLVE_GRAPH")) {   // experiment, see cyc_off
+    h->cyc_off = std::atoi(ev) == 0;
+    h->cyc_inline = std::atoi(ev) == 2;
+  }
+  CK(dalloc(h, &h->ctl, 2));
+  if (h->graphable) CK(capture_vcycle(h));
+  CKE(cudaStreamSynchronize(h->s));
+  return 0;
+}
+
+// Material / discretisation parameters: rho, c0, tau, mu, alpha > 0, lambda >= 0, K symmetric positive
+// definite (Eq:PosDefK, Cholesky of the d x d block).
+static int check_params(int d, const stgmg_params* params) {
   if (!(params->rho > 0) || !(params->c0 > 0) || !(params->tau > 0) || !(params->mu > 0) || params->lambda < 0 ||
       !(params->alpha > 0)) {
     set_error("rho, c0, tau, mu, alpha must be > 0 and lambda >= 0 (P:L52)");
@@ -1690,6 +1742,19 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       }
     }
   }
+  return 0;
+}
+
+int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, const stgmg_params* params,
+                stgmg_handle** out) {
+  NvtxRange nv("stgmg_setup");
+  if (!mesh || !order || !params || !out) { set_error("null argument"); return STGMG_EINVAL; }
+  const int d = mesh->dim, r = order->r, k = order->k;
+  if ((d != 2 && d != 3) || r < 2 || r > 3 || k < 0 || k > 3 || levels < 1 || levels > 16) {
+    set_error("invalid dim / order / levels (d in {2,3}, 2 <= r <= 3, 0 <= k <= 3)");
+    return STGMG_EINVAL;
+  }
+  CK(check_params(d, params));
   for (int a = 0; a < d; ++a)
     if (mesh->cells[a] < 1 || mesh->cells[a] % (1 << (levels - 1)) != 0 || !(mesh->hi[a] > mesh->lo[a])) {
       set_error("cells must be divisible by 2^(levels-1) and the box non-degenerate");
@@ -1902,32 +1967,175 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     CK(build_transfer(h.get(), l));
     CK(build_small(h.get(), l));
   }
-  const long long Nf = h->lev[levels - 1].g.N;
-  CK(dalloc(h.get(), &h->w, (size_t)Nf));
-  CK(dalloc(h.get(), &h->rv, (size_t)Nf));
-  CK(dalloc(h.get(), &h->stage_rhs, (size_t)Nf));
-  CK(dalloc(h.get(), &h->stage_x, (size_t)Nf));
-  CK(dalloc(h.get(), &h->rhs_int, (size_t)Nf));
-  CK(dalloc(h.get(), &h->scal, 16));
-  CK(dalloc(h.get(), &h->partials, 2048));
-  CK(dalloc(h.get(), &h->counter, 4));
-  CKE(cudaMemset(h->counter, 0, 4 * sizeof(unsigned)));
-  CKE(cudaMallocHost(&h->pinned, 16 * sizeof(double)));
-  CKE(cudaEventCreate(&h->e0));
-  CKE(cudaEventCreate(&h->e1));
-  CK(build_fold(h.get()));
-  if (const char* ev = std::getenv("STGMG_STEP_GRAPHS")) h->step_graphs = std::atoi(ev) != 0;
-  if (std::getenv("STGMG_PROFILE_SOLVE")) {
-    h->prof = true;
-    for (auto& e : h->pev) CKE(cudaEventCreate(&e));
+  CK(finish_setup(h.get()));
+  *out = h.release();
+  return 0;
+}
+
+// ------------------------------------------------------------------ the 3D L-shaped benchmark ----
+static HostCsr to_host_csr(const LsHostCsr& m) {
+  HostCsr c;
+  c.rp = m.rp;
+  c.ci = m.ci;
+  c.v = m.v;
+  return c;
+}
+
+static HostCsr transpose_csr(const LsHostCsr& m, long long ncols) {
+  HostCsr t;
+  t.rp.assign(ncols + 1, 0);
+  for (int c : m.ci) t.rp[c + 1] += 1;
+  for (long long i = 0; i < ncols; ++i) t.rp[i + 1] += t.rp[i];
+  t.ci.resize(m.ci.size());
+  t.v.resize(m.v.size());
+  std::vector<int> pos(t.rp.begin(), t.rp.end() - 1);
+  const long long nrows = (long long)m.rp.size() - 1;
+  for (long long r = 0; r < nrows; ++r)      // rows ascending: columns of the transpose come out ascending
+    for (int e = m.rp[r]; e < m.rp[r + 1]; ++e) {
+      const int c = m.ci[e];
+      t.ci[pos[c]] = (int)r;
+      t.v[pos[c]] = m.v[e];
+      ++pos[c];
+    }
+  return t;
+}
+
+// Batched equilibrated explicit inverses (K4) of n matrices already in mats (row-major, lda).
+static int invert_batch(stgmg_handle* h, double* mats, int n, int nmax, const int* n_each_dev, int lda,
+                        const char* what) {
+  int *perm = nullptr, *status = nullptr;
+  double *colk = nullptr, *scale = nullptr;
+  CKE(cudaMalloc(&perm, sizeof(int) * (size_t)n * lda));
+  CKE(cudaMalloc(&status, sizeof(int) * (size_t)n));
+  CKE(cudaMalloc(&colk, sizeof(double) * (size_t)n * lda));
+  CKE(cudaMalloc(&scale, sizeof(double) * (size_t)n * lda));
+  CKE(cudaMemsetAsync(status, 0, sizeof(int) * (size_t)n, h->s));
+  if (gauss_jordan_inverse(mats, n, nmax, n_each_dev, lda, perm, colk, scale, status, h->s)) {
+    set_error(std::string(what) + ": gauss_jordan_inverse launch failed");
+    return STGMG_ECUDA;
   }
-  if (const char* ev = std::getenv("STGMG_SOLVE_GRAPH")) {   // experiment, see cyc_off
-    h->cyc_off = std::atoi(ev) == 0;
-    h->cyc_inline = std::atoi(ev) == 2;
-  }
-  CK(dalloc(h.get(), &h->ctl, 2));
-  if (h->graphable) CK(capture_vcycle(h.get()));
+  std::vector<int> st(n);
+  CKE(cudaMemcpyAsync(st.data(), status, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost, h->s));
   CKE(cudaStreamSynchronize(h->s));
+  cudaFree(perm);
+  cudaFree(status);
+  cudaFree(colk);
+  cudaFree(scale);
+  for (int i = 0; i < n; ++i)
+    if (st[i] != 0) {
+      set_error(std::string(what) + ": singular matrix " + std::to_string(i) + " (pivot " + std::to_string(st[i]) +
+                ")");
+      return STGMG_ESINGULAR;
+    }
+  return 0;
+}
+
+int stgmg_setup_lshape(int ref_fine, int levels, const stgmg_order* order, const stgmg_params* params,
+                       stgmg_handle** out) {
+  NvtxRange nv("stgmg_setup_lshape");
+  if (!order || !params || !out) { set_error("null argument"); return STGMG_EINVAL; }
+  const int r = order->r, k = order->k;
+  if (r < 2 || r > 3 || k < 0 || k > 3 || levels < 1 || levels > 8 || ref_fine < levels - 1 || ref_fine > 7) {
+    set_error("L-shape: need 2 <= r <= 3, 0 <= k <= 3, 1 <= levels <= ref_fine + 1, ref_fine <= 7");
+    return STGMG_EINVAL;
+  }
+  CK(check_params(3, params));
+  if (params->nranks > 1 || params->smoother != STGMG_SMOOTH_ADDITIVE || params->formulation != STGMG_FORM_DSA) {
+    set_error("L-shape: single GPU, Algorithm 1 (additive) and Problem 3.1 only");
+    return STGMG_ENOTSUP;
+  }
+  auto h = std::make_unique<stgmg_handle>();
+  h->lshape = true;
+  h->d = 3; h->r = r; h->k = k; h->k1 = k + 1; h->L = levels;
+  h->prm = *params;
+  if (h->prm.omega <= 0) h->prm.omega = 0.7;
+  if (h->prm.jmax <= 0) h->prm.jmax = 4;
+  if (params->stream) {
+    h->s = (cudaStream_t)params->stream;
+  } else {
+    CKE(cudaStreamCreateWithFlags(&h->s, cudaStreamDefault));
+    h->own_stream = true;
+  }
+  h->c = make_consts(3, r, k, h->prm);
+  {
+    std::vector<double> t, w;
+    radau(k, t, w);
+    for (int b = 0; b <= k; ++b) h->ls_that[b] = t[b];
+  }
+  LsHost host;
+  {
+    NvtxRange nv2("stgmg setup: L-shape host assembly");
+    std::string err;
+    const int rc = lshape_build_host(ref_fine - levels + 1, levels, r, k, h->c, host, err);
+    if (rc) { set_error(err); return rc; }
+  }
+  h->lev.resize(levels);
+  for (int l = 0; l < levels; ++l) {
+    LevelData& Lv = h->lev[l];
+    const LsLevelHost& Hl = host.lev[l];
+    std::memset(&Lv.g, 0, sizeof(Lv.g));
+    Lv.g.d = 3;
+    Lv.g.nq = Hl.nq;
+    Lv.g.np = Hl.np;
+    Lv.g.R = 3LL * Hl.nq;
+    Lv.g.S = Hl.np;
+    Lv.g.block = 6LL * Hl.nq + Hl.np;
+    Lv.g.N = Hl.N;
+    Lv.unstr = l >= 1;
+    const long long N = Hl.N;
+    CK(dalloc(h.get(), &Lv.b, (size_t)N));
+    CK(dalloc(h.get(), &Lv.d, (size_t)N));
+    CK(dalloc(h.get(), &Lv.r, (size_t)N));
+    CKE(cudaMemset(Lv.b, 0, sizeof(double) * N));
+    CKE(cudaMemset(Lv.d, 0, sizeof(double) * N));
+    CKE(cudaMemset(Lv.r, 0, sizeof(double) * N));
+    const HostCsr A = to_host_csr(Hl.A);
+    Lv.A_lpr = lanes_for(A);
+    CK(upload_csr(h.get(), A, &Lv.A_rp, &Lv.A_ci, &Lv.A_v));
+    if (l == 0) continue;
+    const HostCsr P = to_host_csr(Hl.P);
+    const HostCsr R = transpose_csr(Hl.P, host.lev[l - 1].N);
+    Lv.P_lpr = lanes_for(P);
+    Lv.R_lpr = lanes_for(R);
+    CK(upload_csr(h.get(), P, &Lv.P_rp, &Lv.P_ci, &Lv.P_v));
+    CK(upload_csr(h.get(), R, &Lv.R_rp, &Lv.R_ci, &Lv.R_v));
+    Lv.npatch = (long long)Hl.pcp.size();
+    Lv.pmax = Hl.maxcp;
+    Lv.maxcp = Hl.maxcp;
+    Lv.plda = Hl.maxcp;
+    CK(upload(h.get(), &Lv.pz, Hl.pz));
+    CK(upload(h.get(), &Lv.pzoff, Hl.pzoff));
+    CK(upload(h.get(), &Lv.pcp, Hl.pcp));
+    CK(upload(h.get(), &Lv.k3tab, Hl.k3tab));
+    CK(dalloc(h.get(), &Lv.Y, (size_t)Hl.ysize));
+    CKE(cudaMemset(Lv.Y, 0, sizeof(double) * Hl.ysize));
+    // per-patch A_P extracted from the CSR operator, equilibrated explicit inverses (K4)
+    CK(dalloc(h.get(), &Lv.pinv, (size_t)Lv.npatch * Lv.plda * Lv.plda));
+    CKE(launch_csr_extract_patches(Lv.A_rp, Lv.A_ci, Lv.A_v, Lv.pz, Lv.pzoff, Lv.pcp, 0, (int)Lv.npatch, Lv.pinv,
+                                   Lv.plda, h->s));
+    CK(invert_batch(h.get(), Lv.pinv, (int)Lv.npatch, Lv.pmax, Lv.pcp, Lv.plda, "L-shape patch inverse"));
+  }
+  {   // coarse direct solve: equilibrated explicit inverse of A_0
+    NvtxRange nv3("stgmg setup: coarse inverse");
+    LevelData& L0 = h->lev[0];
+    h->n0 = (int)L0.g.N;
+    CK(dalloc(h.get(), &h->A0inv, (size_t)h->n0 * h->n0));
+    CKE(launch_csr_to_dense(h->n0, L0.A_rp, L0.A_ci, L0.A_v, h->A0inv, h->s));
+    int* n0dev = nullptr;
+    CK(upload(h.get(), &n0dev, std::vector<int>{h->n0}));
+    CK(invert_batch(h.get(), h->A0inv, 1, h->n0, n0dev, h->n0, "L-shape coarse inverse"));
+  }
+  {
+    const HostCsr J = to_host_csr(host.J);
+    h->J_lpr = lanes_for(J);
+    CK(upload_csr(h.get(), J, &h->J_rp, &h->J_ci, &h->J_v));
+    CK(upload(h.get(), &h->ls_fN, host.fN));
+    CK(upload(h.get(), &h->ls_wu, host.wu));
+    CK(upload(h.get(), &h->ls_wp, host.wp));
+    h->ls_nq = host.lev[levels - 1].nq;
+    h->ls_np = host.lev[levels - 1].np;
+  }
+  CK(finish_setup(h.get()));
   *out = h.release();
   return 0;
 }
@@ -2017,6 +2225,17 @@ int stgmg_vcycle(stgmg_handle* h, const double* b, double* x) {
 }
 
 int stgmg_slab_load(stgmg_handle* h, int kind, double t_n, double* load) {
+  if (h && load && h->lshape) {   // Sec. 5.2: chi_b rows = theta_b sin(8 pi t_{n,b}) (-<t_N, chi>)
+    if (kind != STGMG_LOAD_LSHAPE_TRACTION) { set_error("L-shape handle: kind must be LSHAPE_TRACTION"); return STGMG_EINVAL; }
+    double coef[kMaxK1] = {};
+    for (int b = 0; b < h->k1; ++b)
+      coef[b] = h->c.theta[b] * std::sin(8.0 * M_PI * (t_n + 0.5 * h->prm.tau * (1.0 + h->ls_that[b])));
+    const LevelGeom& g = h->lev[h->L - 1].g;
+    CKE(launch_lshape_load(g.N, g.block, g.R, h->k1, h->ls_fN, coef, load, h->s));
+    h->launches = 1;
+    return sync_if_own(h);
+  }
+  if (h && h->lshape) { set_error("bad argument"); return STGMG_EINVAL; }
   if (!h || !load || (kind != STGMG_LOAD_MANUFACTURED && kind != STGMG_LOAD_BEAM_TRACTION)) {
     set_error("bad argument");
     return STGMG_EINVAL;
@@ -2033,7 +2252,12 @@ int stgmg_slab_load(stgmg_handle* h, int kind, double t_n, double* load) {
 }
 
 int stgmg_initial_state(stgmg_handle* h, int kind, double t0, double* x) {
-  if (!h || !x || (kind != STGMG_LOAD_MANUFACTURED && kind != STGMG_LOAD_BEAM_TRACTION)) {
+  if (h && x && h->lshape && kind == STGMG_LOAD_LSHAPE_TRACTION) {   // Sec. 5.2 starts at rest (reading N3-R8)
+    CKE(cudaMemsetAsync(x, 0, sizeof(double) * h->lev[h->L - 1].g.N, h->s));
+    h->launches = 0;
+    return sync_if_own(h);
+  }
+  if (!h || !x || h->lshape || (kind != STGMG_LOAD_MANUFACTURED && kind != STGMG_LOAD_BEAM_TRACTION)) {
     set_error("bad argument");
     return STGMG_EINVAL;
   }
@@ -2047,6 +2271,18 @@ int stgmg_initial_state(stgmg_handle* h, int kind, double t0, double* x) {
 // block of x) over a whole box face; owned face cells of this rank, summed over the ranks.
 int stgmg_goal_quantities(stgmg_handle* h, const double* x, int face, double* bu, double* bp) {
   if (!h || !x || !bu || !bp || face < 0 || face >= 2 * h->d) { set_error("bad argument"); return STGMG_EINVAL; }
+  if (h->lshape) {   // Eq:DefGQ on Gamma_m = {1} x (0,.5) x (0,.5) (the x+ face of the L-shape)
+    if (face != 1) { set_error("L-shape: the goal face is Gamma_m (face 1, x = 1)"); return STGMG_EINVAL; }
+    const LevelGeom& g = h->lev[h->L - 1].g;
+    const long long ob = (long long)h->k * g.block;
+    CKE(launch_lshape_goal(x, ob + g.R, ob + 2 * g.R, h->ls_nq, h->ls_np, h->ls_wu, h->ls_wp, h->scal + 10, h->s));
+    h->launches = 1;
+    CKE(cudaMemcpyAsync(h->pinned + 10, h->scal + 10, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->s));
+    CKE(cudaStreamSynchronize(h->s));
+    *bu = h->pinned[10];
+    *bp = h->pinned[11];
+    return 0;
+  }
   const LevelData& F = h->lev[h->L - 1];
   const LevelGeom& g = F.g;
   const int a = face >> 1, side = face & 1;
@@ -2085,6 +2321,11 @@ int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, do
   if (!h || !x_prev || !rhs) { set_error("bad argument"); return STGMG_EINVAL; }
   const LevelGeom& g = h->lev[h->L - 1].g;
   h->launches = 0;
+  if (h->lshape) {   // F_n = L_n + J X_{n-1} with the assembled coupling (one SpMV)
+    CKE(launch_csr_spmv((int)g.N, h->J_lpr, h->J_rp, h->J_ci, h->J_v, x_prev, load, rhs, 1.0, 1.0, h->s));
+    h->launches = 1;
+    return sync_if_own(h);
+  }
   CK(apply_geom(h, g, h->cj_dev, x_prev, rhs, load, 1.0, 1.0));
   return sync_if_own(h);
 }
@@ -2113,6 +2354,7 @@ static int dot(stgmg_handle* h, double* w, const double* vprev, const double* hp
 // Two operator applies with selector constants on placed copies of that block, two owned-DoF inner products.
 int stgmg_energy(stgmg_handle* h, const double* x, double* energy) {
   if (!h || !x || !energy) { set_error("bad argument"); return STGMG_EINVAL; }
+  if (h->lshape) { set_error("stgmg_energy: not available for the L-shape"); return STGMG_ENOTSUP; }
   const int Lf = h->L - 1;
   const LevelGeom& g = h->lev[Lf].g;
   double *Y = h->w, *O = h->rv, *Zt = h->stage_rhs;
@@ -2433,6 +2675,7 @@ int stgmg_solve_host(stgmg_handle* h, const double* rhs_host, double* x_host, do
 }
 
 int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double* k2_bytes, double* k1_bytes) {
+  if (h && h->lshape) { set_error("not available for the L-shape"); return STGMG_ENOTSUP; }
   if (!h || level < 0 || level >= h->L) { set_error("bad level"); return STGMG_EINVAL; }
   const LevelData& Lv = h->lev[level];
   double fl = 0.0, sumcp = 0.0, invb = 0.0;
@@ -2448,6 +2691,7 @@ int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double*
 }
 
 int stgmg_kernel_work(const stgmg_handle* h, int kind, int level, double* flops, double* bytes) {
+  if (h && h->lshape) { set_error("not available for the L-shape"); return STGMG_ENOTSUP; }
   if (!h || level < 0 || level >= h->L || !flops || !bytes) { set_error("bad argument"); return STGMG_EINVAL; }
   const LevelData& Lv = h->lev[level];
   const double N = (double)Lv.g.N;
@@ -2475,6 +2719,7 @@ int stgmg_kernel_work(const stgmg_handle* h, int kind, int level, double* flops,
 }
 
 int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms) {
+  if (h && h->lshape) { set_error("not available for the L-shape"); return STGMG_ENOTSUP; }
   if (!h || level < 0 || level >= h->L || reps < 1 || !avg_ms) { set_error("bad argument"); return STGMG_EINVAL; }
   if ((kind == 0 || kind == 2 || kind == 6 || kind == 7) && level < 1) {
     set_error("smoother kernels need level >= 1");

@@ -205,4 +205,36 @@ cudaError_t launch_prolong_add(const LevelGeom& fine, const LevelGeom& coarse, i
 // K6: y = A x dense (coarse solve, row-major lda).
 cudaError_t launch_gemv(const double* A, int n, int lda, const double* x, double* y, cudaStream_t s);
 
+// ---- the 3D L-shaped benchmark (csrc/lshape.cu) ----
+struct LsHostCsr {
+  std::vector<int> rp, ci;
+  std::vector<double> v;
+};
+struct LsLevelHost {                  // one level of the L-shape hierarchy, assembled on the host at setup
+  int ref = 0, nq = 0, np = 0, ncell = 0, maxcp = 0;
+  long long N = 0, ysize = 0;
+  LsHostCsr A;                        // slab operator A_l (N x N)
+  LsHostCsr P;                        // prolongation level l-1 -> l (rows: this level); l >= 1
+  std::vector<int> pz, pcp;           // vertex patches: concatenated DoF lists Z(P), sizes C_P
+  std::vector<long long> pzoff;       // start of Z(P) in pz (= start of y_P in the patch results)
+  std::vector<int> k3tab;             // averaging table, 27 x N (Y offsets, lexicographic patches, -1 = none)
+};
+struct LsHost {
+  std::vector<LsLevelHost> lev;
+  LsHostCsr J;                        // slab-RHS coupling F = L + J X_{n-1} (fine level)
+  std::vector<double> fN;             // -<t_N, chi> per unit sin(8 pi t), U components (3 nq), fine level
+  std::vector<double> wu, wp;         // goal weights on Gamma_m: U_x nodes (nq), P DoFs (np)
+};
+int lshape_build_host(int ref_coarse, int levels, int r, int k, const OpConsts& oc, LsHost& out, std::string& err);
+cudaError_t launch_csr_extract_patches(const int* rp, const int* ci, const double* v, const int* pz,
+                                       const long long* pzoff, const int* pcp, int p0, int np, double* out, int lda,
+                                       cudaStream_t s);
+cudaError_t launch_patch_gemv(int npatch, int maxcp, const int* pz, const long long* pzoff, const int* pcp,
+                              const double* inv, int lda, const double* r, double* Y, cudaStream_t s);
+cudaError_t launch_csr_to_dense(int n, const int* rp, const int* ci, const double* v, double* out, cudaStream_t s);
+cudaError_t launch_lshape_load(long long N, long long block, long long R, int k1, const double* fN, const double* coef,
+                               double* L, cudaStream_t s);
+cudaError_t launch_lshape_goal(const double* x, long long ou, long long op, int nq, int np, const double* wu,
+                               const double* wp, double* out, cudaStream_t s);
+
 }  // namespace stgmg

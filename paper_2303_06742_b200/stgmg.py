@@ -14,7 +14,7 @@ TOL_REL, TOL_ABS = 0, 1
 BC_DIRICHLET, BC_NEUMANN = 0, 1
 HF_MEASURE, HF_EDGE = 0, 1
 SMOOTH_ADDITIVE, SMOOTH_COLORED_MULT, SMOOTH_ELEMENT, SMOOTH_OVERWRITE = 0, 1, 2, 3
-LOAD_MANUFACTURED, LOAD_BEAM_TRACTION = 0, 1
+LOAD_MANUFACTURED, LOAD_BEAM_TRACTION, LOAD_LSHAPE_TRACTION = 0, 1, 2
 FORM_DSA, FORM_DS = 0, 1
 
 
@@ -52,6 +52,8 @@ _P = ctypes.c_void_p
 SIGNATURES = {
     "stgmg_setup": (ctypes.c_int, [ctypes.POINTER(Mesh), ctypes.c_int, ctypes.POINTER(Order), ctypes.POINTER(Params),
                                    ctypes.POINTER(_P)]),
+    "stgmg_setup_lshape": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(Order), ctypes.POINTER(Params),
+                                          ctypes.POINTER(_P)]),
     "stgmg_local_size": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]),
     "stgmg_apply_operator": (ctypes.c_int, [_P, ctypes.c_int, _P, _P]),
     "stgmg_residual": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P]),
@@ -401,3 +403,39 @@ class Solver:
 
     def fold_level(self):
         return int(self.lib.stgmg_fold_level(self.h))
+
+
+class LShapeSolver(Solver):
+    """The 3D L-shaped benchmark of Sec. 5.2 (stgmg_setup_lshape): Q_r^3 / P_{r-1}^disc on the 3-cube
+    L-shape with 2^ref_fine cells per cube edge, levels ref_fine - levels + 1 .. ref_fine.  params: dict with rho,
+    alpha, c0, lam, mu, K (9 entries), gamma_a, gamma_b (< 0: defaults of P:L209-211)."""
+
+    def __init__(self, ref_fine, levels, r, k, tau, params, stream=None, omega=0.7, jmax=4):
+        import torch
+        if not torch.cuda.is_available():
+            raise StgmgError("no CUDA device: the stgmg product path has no CPU fallback")
+        self.lib = load_library()
+        self.cfg = dict(rtol=1e-8, restart=30, levels=levels, lshape=True)
+        o = Order(int(r), int(k))
+        p = Params()
+        p.rho, p.alpha, p.c0, p.lambda_, p.mu = params["rho"], params["alpha"], params["c0"], params["lam"], params["mu"]
+        for i in range(9):
+            p.K[i] = float(params["K"][i])
+        p.tau = float(tau)
+        p.gamma_a = float(params.get("gamma_a", -1.0))
+        p.gamma_b = float(params.get("gamma_b", -1.0))
+        p.omega, p.jmax = omega, jmax
+        p.nranks, p.rank = 1, 0
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        p.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        self.levels = int(levels)
+        h = ctypes.c_void_p()
+        _check(self.lib.stgmg_setup_lshape(int(ref_fine), self.levels, ctypes.byref(o), ctypes.byref(p),
+                                           ctypes.byref(h)), "stgmg_setup_lshape")
+        self.h = h
+        self.device = self.stream.device
+        self._n = []
+        for lev in range(self.levels):
+            n = ctypes.c_int64()
+            _check(self.lib.stgmg_local_size(self.h, lev, ctypes.byref(n)), "stgmg_local_size")
+            self._n.append(n.value)
