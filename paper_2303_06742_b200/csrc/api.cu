@@ -334,6 +334,11 @@ struct LevelData {
   int entiles = 0, elda = 0, ek2var = 0;
   int* erelidx_dev = nullptr;
   double* E_dev = nullptr;
+  // K1 as factored element GEMMs (csrc/op_fgemm.cu): tiles {type, first cell, cells} and fragment-major operands
+  bool fg = false;
+  int4* fg_tiles = nullptr;
+  int fg_ntiles = 0;
+  FgemmDev fgm;
   // x-slab domain decomposition; a replicated level has part = false, w0 = 0, gnx = n[0]
   bool part = false, has_left = false, has_right = false;
   int gnx = 0, w0 = 0, c0 = 0, c1 = 0;   // global cells along x, window start (global cell), owned cells (local)
@@ -440,6 +445,7 @@ struct stgmg_handle {
   unsigned char* mask = nullptr;   // owned fine-level DoFs (Krylov inner products)
   bool graphable = true;
   bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; large 2D elements)
+  bool fg_on = true;               // K1 element GEMM in the factored form (STGMG_K1_FGEMM=0: the full element matrix)
   int nsm = 148;                   // SMs of the device (tile balancing)
   // the 3D L-shaped benchmark (stgmg_setup_lshape); levels are unstructured (LevelData::unstr)
   bool lshape = false;
@@ -556,6 +562,21 @@ static int apply_geom(stgmg_handle* h, const LevelGeom& g, const OpConsts* cdev,
   return 0;
 }
 
+// Element results Ycell[vertex(K + 1)][e] of the element-matrix route of K1: the factored element GEMMs (op_fgemm)
+// or the full slab element matrix as a grouped GEMM.
+// Returns the leading dimension the node gathers take (0: cell-fastest Y[e][cell], ne: Y[vertex(K + 1)][e]).
+static int element_results(stgmg_handle* h, LevelData& Lv, const double* x, int* ldpm) {
+  const int ne = (int)elem_dofs(h);
+  *ldpm = Lv.fg ? 0 : ne;
+  if (Lv.fg)
+    CKE(launch_op_fgemm(Lv.g, h->r, h->k1, Lv.fg_tiles, Lv.fg_ntiles, Lv.ecls_dev, Lv.erelidx_dev, Lv.fgm, h->c, x,
+                        h->Ycell, h->s));
+  else
+    CKE(launch_patch_gemm(Lv.g, h->r, Lv.ek2var, Lv.ecls_dev, Lv.etiles_dev, Lv.entiles, Lv.erelidx_dev, Lv.E_dev,
+                          Lv.elda, x, h->Ycell, ne, h->s));
+  return 0;
+}
+
 // y = beta * base + alpha * A_l x on hierarchy level l (the runtime operator apply, K1).
 static int apply_level(stgmg_handle* h, int l, const double* x, double* y, const double* base, double alpha,
                        double beta) {
@@ -567,10 +588,9 @@ static int apply_level(stgmg_handle* h, int l, const double* x, double* y, const
   }
   if (!h->op_gemm) return apply_geom(h, h->lev[l].g, h->c_dev, x, y, base, alpha, beta);
   LevelData& Lv = h->lev[l];
-  const int ne = (int)elem_dofs(h);
-  CKE(launch_patch_gemm(Lv.g, h->r, Lv.ek2var, Lv.ecls_dev, Lv.etiles_dev, Lv.entiles, Lv.erelidx_dev, Lv.E_dev,
-                        Lv.elda, x, h->Ycell, ne, h->s));
-  CKE(launch_op_gather(Lv.g, h->r, h->k1, h->Ycell, base, y, alpha, beta, 1, 0, 0, h->s, ne));
+  int ldpm = 0;
+  CK(element_results(h, Lv, x, &ldpm));
+  CKE(launch_op_gather(Lv.g, h->r, h->k1, h->Ycell, base, y, alpha, beta, 1, 0, 0, h->s, ldpm));
   h->launches += 2;
   return 0;
 }
@@ -699,10 +719,9 @@ static int residual_expand(stgmg_handle* h, int l, const double* b, const double
     CKE(launch_op2d_cells(h->r, h->k1, L.g, h->c_dev, d, h->Yc, 1, 0, ycs, h->s));
     CKE(launch_gather_expand(L.g, h->r, h->k1, h->Yc, b, -1.0, 1.0, 0, L.cls_dev, L.Rexp, h->s));
   } else {
-    const int ne = (int)elem_dofs(h);
-    CKE(launch_patch_gemm(L.g, h->r, L.ek2var, L.ecls_dev, L.etiles_dev, L.entiles, L.erelidx_dev, L.E_dev, L.elda, d,
-                          h->Ycell, ne, h->s));
-    CKE(launch_gather_expand(L.g, h->r, h->k1, h->Ycell, b, -1.0, 1.0, ne, L.cls_dev, L.Rexp, h->s));
+    int ldpm = 0;
+    CK(element_results(h, L, d, &ldpm));
+    CKE(launch_gather_expand(L.g, h->r, h->k1, h->Ycell, b, -1.0, 1.0, ldpm, L.cls_dev, L.Rexp, h->s));
   }
   h->launches += 2;
   return 0;
@@ -1300,6 +1319,35 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
   CKE(launch_extract_elem(Ycb, ycs, ne, nt, reps_dev, mdofs_dev, E_rm, Lv.elda, h->s));
   if (gemm) CKE(launch_chunk_swizzle(E_rm, Lv.E_dev, nt, Lv.elda, h->s));
   CKE(cudaStreamSynchronize(h->s));
+  // factored form (op_fgemm.cu) on the levels where it wins (measured: cfg4/cfg3 3D levels with >= 4096 cells, the
+  // 2D Q3 levels with >= 16384 cells; on smaller levels one CTA per 32 cells leaves the GPU idle)
+  const long long ncl = Lv.ncell_global ? Lv.ncell_global : cell_count(g);
+  if (gemm && h->fg_on && h->c.ds == 0.0 && ncl >= (d == 3 ? 4096 : 16384)) {
+    std::vector<double> Eh((size_t)nt * Lv.elda * Lv.elda);
+    CKE(cudaMemcpy(Eh.data(), E_rm, sizeof(double) * Eh.size(), cudaMemcpyDeviceToHost));
+    FgemmData fd;
+    if (fgemm_build_any(d, r, k1, Eh, nt, Lv.elda, h->c, fd) == 0) {
+      std::vector<int4> tl;
+      const int nc = fgemm_cells_per_tile();
+      for (int t = 0; t < nt; ++t)
+        for (int c0 = 0; c0 < Lv.ecls[t].ncols; c0 += nc)
+          tl.push_back(make_int4(t, c0, std::min(nc, Lv.ecls[t].ncols - c0), 0));
+      double *a1 = nullptr, *a2 = nullptr, *a3 = nullptr, *ap = nullptr;
+      CK(upload(h, &a1, fd.A1));
+      CK(upload(h, &a2, fd.A2));
+      CK(upload(h, &a3, fd.A3));
+      CK(upload(h, &ap, fd.AP));
+      CK(upload(h, &Lv.fg_tiles, tl));
+      Lv.fg_ntiles = (int)tl.size();
+      Lv.fgm.A1 = a1;
+      Lv.fgm.A2 = a2;
+      Lv.fgm.A3 = a3;
+      Lv.fgm.AP = ap;
+      Lv.fgm.a2stride = fd.a2stride;
+      Lv.fgm.a3stride = fd.a3stride;
+      Lv.fg = true;
+    }
+  }
   if (Ehost) {
     Ehost->resize((size_t)nt * Lv.elda * Lv.elda);
     CKE(cudaMemcpy(Ehost->data(), E_rm, sizeof(double) * Ehost->size(), cudaMemcpyDeviceToHost));
@@ -1952,6 +2000,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     // 2D: the register kernel on small elements (cfg1, 80 DoFs: K1 9.5 vs 13.8 us), the element GEMM on large ones
     // (cfg2, r = 3, k = 2, 219 DoFs: fine-level K1 357 -> 303 us, V-cycle 27.0 -> 26.0 ms)
     h->op_gemm = d == 3 || elem_dofs(h.get()) >= 128;
+    if (const char* ev = std::getenv("STGMG_K1_FGEMM")) h->fg_on = std::atoi(ev) != 0;
     if (d == 2)
       if (const char* ev = std::getenv("STGMG_OP2D_GEMM")) h->op_gemm = std::atoi(ev) != 0;
     if (h->op_gemm) {

@@ -237,4 +237,20 @@ cudaError_t launch_lshape_load(long long N, long long block, long long R, int k1
 cudaError_t launch_lshape_goal(const double* x, long long ou, long long op, int nq, int np, const double* wu,
                                const double* wp, double* out, cudaStream_t s);
 
+// ---- K1 as factored element GEMMs (csrc/op_fgemm.cu) ----
+struct FgemmData {                    // fragment-major A operands (host)
+  std::vector<double> A1, A2, A3, AP; // mass (shared), [A_gamma | C^T] and [-C | B_gamma] per cell type, M_c (shared)
+  long long a2stride = 0, a3stride = 0;
+};
+struct FgemmDev {
+  const double *A1 = nullptr, *A2 = nullptr, *A3 = nullptr, *AP = nullptr;
+  long long a2stride = 0, a3stride = 0;
+};
+int fgemm_build_any(int d, int r, int k1, const std::vector<double>& E, int ntypes, int lda, const OpConsts& c,
+                    FgemmData& out);
+int fgemm_cells_per_tile();
+cudaError_t launch_op_fgemm(const LevelGeom& g, int r, int k1, const int4* tiles, int ntiles, const PatchClass* ecls,
+                            const int* relidx, const FgemmDev& m, const OpConsts& c, const double* x, double* Y,
+                            cudaStream_t s);   // Y[element DoF][cell] (cell-fastest)
+
 }  // namespace stgmg
