@@ -1762,6 +1762,22 @@ static int finish_setup(stgmg_handle* h) {
   return 0;
 }
 
+// STGMG_SETUP_TIMES=1: host wall time of each setup phase (device synchronised) on stderr.
+extern "C++" {
+template <class F>
+static int timed(const char* what, int level, F f) {
+  static const bool on = std::getenv("STGMG_SETUP_TIMES") != nullptr;
+  if (!on) return f();
+  cudaDeviceSynchronize();
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = f();
+  cudaDeviceSynchronize();
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  std::fprintf(stderr, "stgmg setup: %-15s level %2d  %9.1f ms\n", what, level, ms);
+  return rc;
+}
+}
+
 // Material / discretisation parameters: rho, c0, tau, mu, alpha > 0, lambda >= 0, K symmetric positive
 // definite (Eq:PosDefK, Cholesky of the d x d block).
 static int check_params(int d, const stgmg_params* params) {
@@ -2007,16 +2023,16 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       long long nv = 1;
       for (int a = 0; a < 3; ++a) nv *= h->lev[levels - 1].g.n[a] + 1;
       CK(dalloc(h.get(), &h->Ycell, (size_t)(nv * elem_dofs(h.get()))));
-      for (int l = 0; l < levels; ++l) CK(build_cells(h.get(), l, true));
+      for (int l = 0; l < levels; ++l) CK(timed("build_cells", l, [&] { return build_cells(h.get(), l, true); }));
     }
   }
-  CK(build_coarse(h.get()));
+  CK(timed("build_coarse", 0, [&] { return build_coarse(h.get()); }));
   for (int l = 1; l < levels; ++l) {
-    CK(build_patches(h.get(), l));
-    CK(build_transfer(h.get(), l));
-    CK(build_small(h.get(), l));
+    CK(timed("build_patches", l, [&] { return build_patches(h.get(), l); }));
+    CK(timed("build_transfer", l, [&] { return build_transfer(h.get(), l); }));
+    CK(timed("build_small", l, [&] { return build_small(h.get(), l); }));
   }
-  CK(finish_setup(h.get()));
+  CK(timed("finish_setup", -1, [&] { return finish_setup(h.get()); }));
   *out = h.release();
   return 0;
 }

@@ -1146,14 +1146,190 @@ __global__ void gj_colperm(double* mats, int lda, const int* n_each, const int* 
   }
 }
 
+// ---- blocked Gauss–Jordan (K4 on the FP64 tensor pipe) ----
+// The same in-place Gauss–Jordan with partial pivoting (max |a|, ties -> lowest row) as gj_pivot / gj_elim, in
+// column panels of GJB_NB pivots: the panel kernel runs the NB elimination steps on the panel columns only (L2
+// resident) and records the composite row permutation pi; the NB steps act on every other column c as
+//   M[:, c] <- M[pi(:), c] + W M[pi(panel rows), c],   W = (panel result) - I[:, panel],
+// (the in-place panel column k0 + j ends as the product of the steps' elementary matrices applied to e_{k0+j}), a
+// rank-NB update done by gjb_trailing with DMMA out of place (ping-pong buffers).  Memory traffic per pivot drops by
+// NB: the unblocked rank-1 updates stream every matrix once per pivot (3D levels: 125 x 1568^2 doubles, 1554 times).
+constexpr int GJB_NB = 32, GJB_BM = 64, GJB_BN = 64;
+
+__global__ void __launch_bounds__(512) gjb_panel(double* mats, int lda, const int* n_each, int k0, int* perm, int* pi,
+                                                 double* colk, int* status) {
+  const int c = blockIdx.x;
+  const int n = n_each[c];
+  if (k0 >= n || status[c] != 0) return;
+  double* A = mats + (long long)c * lda * lda;
+  int* pm = perm + (long long)c * lda;
+  int* pc = pi + (long long)c * lda;
+  double* ck = colk + (long long)c * lda;
+  const int nbe = min(GJB_NB, n - k0);
+  __shared__ double bv[512];
+  __shared__ int bi[512];
+  for (int i = k0 + threadIdx.x; i < n; i += blockDim.x) pc[i] = i;
+  __syncthreads();
+  for (int j = 0; j < nbe; ++j) {
+    const int k = k0 + j;
+    double best = -1.0;
+    int bidx = n;
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+      const double v = fabs(A[(long long)i * lda + k]);
+      if (v > best || (v == best && i < bidx)) { best = v; bidx = i; }
+    }
+    bv[threadIdx.x] = best;
+    bi[threadIdx.x] = bidx;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+      if (threadIdx.x < st) {
+        const double v2 = bv[threadIdx.x + st];
+        const int i2 = bi[threadIdx.x + st];
+        if (v2 > bv[threadIdx.x] || (v2 == bv[threadIdx.x] && i2 < bi[threadIdx.x])) {
+          bv[threadIdx.x] = v2;
+          bi[threadIdx.x] = i2;
+        }
+      }
+      __syncthreads();
+    }
+    const int p = bi[0];
+    if (bv[0] <= 0.0) {
+      if (threadIdx.x == 0) status[c] = k + 1;
+      return;
+    }
+    if (p != k) {   // swap the panel rows and the permutation entries
+      for (int q = threadIdx.x; q < nbe; q += blockDim.x) {
+        const double t = A[(long long)k * lda + k0 + q];
+        A[(long long)k * lda + k0 + q] = A[(long long)p * lda + k0 + q];
+        A[(long long)p * lda + k0 + q] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = pc[k];
+        pc[k] = pc[p];
+        pc[p] = t;
+      }
+    }
+    if (threadIdx.x == 0) pm[k] = p;
+    __syncthreads();
+    const double piv = A[(long long)k * lda + k];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ck[i] = A[(long long)i * lda + k];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) A[(long long)i * lda + k] = (i == k) ? 1.0 : 0.0;
+    __syncthreads();
+    const double ip = 1.0 / piv;
+    for (int q = threadIdx.x; q < nbe; q += blockDim.x) A[(long long)k * lda + k0 + q] *= ip;
+    __syncthreads();
+    for (long long e = threadIdx.x; e < (long long)n * nbe; e += blockDim.x) {
+      const int i = (int)(e / nbe), q = (int)(e % nbe);
+      if (i == k) continue;
+      const double f = ck[i];
+      if (f != 0.0) A[(long long)i * lda + k0 + q] = fma(-f, A[(long long)k * lda + k0 + q], A[(long long)i * lda + k0 + q]);
+    }
+    __syncthreads();
+  }
+}
+
+// out[i][c] = in[i][c] on the panel columns, padding and rows / columns >= n; otherwise
+// in[pi(i)][c] + sum_j W[i][j] in[pi(k0 + j)][c] with W[i][j] = in[i][k0 + j] - delta_{i, k0+j} (DMMA m8n8k4).
+__global__ void __launch_bounds__(256) gjb_trailing(const double* __restrict__ in, double* __restrict__ out, int lda,
+                                                    const int* n_each, int k0, const int* __restrict__ pi,
+                                                    const int* status) {
+  const int c = blockIdx.z;
+  const int n = n_each[c];
+  const double* A = in + (long long)c * lda * lda;
+  double* O = out + (long long)c * lda * lda;
+  const int r0 = blockIdx.y * GJB_BM, c0 = blockIdx.x * GJB_BN;
+  const bool active = k0 < n && status[c] == 0;
+  const int nbe = active ? min(GJB_NB, n - k0) : 0;
+  const int* pc = pi + (long long)c * lda;
+  __shared__ double Ws[GJB_BM][GJB_NB + 1];
+  __shared__ double Ts[GJB_NB][GJB_BN + 4];
+  __shared__ int prow[GJB_BM];
+  for (int e = threadIdx.x; e < GJB_BM * GJB_NB; e += blockDim.x) {
+    const int i = e / GJB_NB, j = e % GJB_NB, row = r0 + i;
+    double w = 0.0;
+    if (j < nbe && row < n) w = A[(long long)row * lda + k0 + j] - (row == k0 + j ? 1.0 : 0.0);
+    Ws[i][j] = w;
+  }
+  for (int e = threadIdx.x; e < GJB_NB * GJB_BN; e += blockDim.x) {
+    const int j = e / GJB_BN, q = e % GJB_BN, col = c0 + q;
+    double t = 0.0;
+    if (j < nbe && col < lda) t = A[(long long)pc[k0 + j] * lda + col];
+    Ts[j][q] = t;
+  }
+  for (int i = threadIdx.x; i < GJB_BM; i += blockDim.x) {
+    const int row = r0 + i;
+    prow[i] = (active && row >= k0 && row < n) ? pc[row] : row;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < GJB_NB / 4; ++ks) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) af[a] = Ws[wm + 8 * a + (lane >> 2)][4 * ks + (lane & 3)];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bf[b] = Ts[4 * ks + (lane & 3)][wn + 8 * b + (lane >> 2)];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                     : "d"(af[a]), "d"(bf[b]));
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = wm + 8 * a + (lane >> 2), row = r0 + i;
+        const int col = c0 + wn + 8 * b + 2 * (lane & 3) + e;
+        if (row >= lda || col >= lda) continue;
+        double v;
+        if (!active || row >= n || col >= n || (col >= k0 && col < k0 + nbe)) v = A[(long long)row * lda + col];
+        else v = A[(long long)prow[i] * lda + col] + acc[a][b][e];
+        O[(long long)row * lda + col] = v;
+      }
+}
+
 // Batched in-place inverse of nmat matrices (row-major, lda) of sizes n_each (device array).  Returns 0 or the
-// negative CUDA error; status[c] != 0 marks a singular matrix (checked by the caller after a sync).
+// negative CUDA error; status[c] != 0 marks a singular matrix (checked by the caller after a sync).  Matrices of
+// >= 128 rows take the blocked form (STGMG_GJ_UNBLOCKED=1: always the rank-1 form).
 int gauss_jordan_inverse(double* mats, int nmat, int n_max, const int* n_each, int lda, int* perm, double* colk,
                          double* scale, int* status, cudaStream_t s) {
   gj_equilibrate<<<nmat, 256, 0, s>>>(mats, lda, n_each, scale, 1, status);
-  for (int k = 0; k < n_max; ++k) {
-    gj_pivot<<<nmat, 1024, 0, s>>>(mats, lda, n_each, k, perm, colk, status);
-    gj_elim<<<dim3((n_max + 7) / 8, nmat), 256, 0, s>>>(mats, lda, n_each, k, colk, status);
+  static const bool unblocked = std::getenv("STGMG_GJ_UNBLOCKED") != nullptr;
+  double* buf = nullptr;
+  int* pi = nullptr;
+  if (!unblocked && n_max >= 128 &&
+      cudaMalloc(&buf, sizeof(double) * (size_t)nmat * lda * lda) == cudaSuccess &&
+      cudaMalloc(&pi, sizeof(int) * (size_t)nmat * lda) == cudaSuccess) {
+    double *cur = mats, *nxt = buf;
+    const dim3 tg((lda + GJB_BN - 1) / GJB_BN, (lda + GJB_BM - 1) / GJB_BM, nmat);
+    for (int k0 = 0; k0 < n_max; k0 += GJB_NB) {
+      gjb_panel<<<nmat, 512, 0, s>>>(cur, lda, n_each, k0, perm, pi, colk, status);
+      gjb_trailing<<<tg, 256, 0, s>>>(cur, nxt, lda, n_each, k0, pi, status);
+      std::swap(cur, nxt);
+    }
+    if (cur != mats) cudaMemcpyAsync(mats, cur, sizeof(double) * (size_t)nmat * lda * lda, cudaMemcpyDeviceToDevice, s);
+    cudaStreamSynchronize(s);
+    cudaFree(buf);
+    cudaFree(pi);
+  } else {
+    if (buf) cudaFree(buf);
+    cudaGetLastError();
+    for (int k = 0; k < n_max; ++k) {
+      gj_pivot<<<nmat, 1024, 0, s>>>(mats, lda, n_each, k, perm, colk, status);
+      gj_elim<<<dim3((n_max + 7) / 8, nmat), 256, 0, s>>>(mats, lda, n_each, k, colk, status);
+    }
   }
   gj_colperm<<<nmat, 256, 0, s>>>(mats, lda, n_each, perm);
   gj_equilibrate<<<nmat, 256, 0, s>>>(mats, lda, n_each, scale, 0, status);
