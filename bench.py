@@ -194,11 +194,26 @@ def cpu_baseline(cfg):
         return {"value": None, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle",
                 "sample": "not run: %s" % e}
     N = H.fine.N
-    return {"value": N / (dt * S) / 1e6, "unit": "MDoF*iter/s", "cores": blas_threads(), "kind": "oracle",
-            "sample": "one fine-level Alg. 1 sweep of slab 1 of %s (residual, all patch solves, averaging): %.2f s; "
-                      "GMRES iteration extrapolated as %.2f sweeps (V-cycle K2 flops / fine-sweep K2 flops); oracle "
-                      "setup %.1f s excluded" % (cfg["name"], dt, S, t_setup),
-            "host": host_info()}
+    cores = blas_threads()
+    single = None
+    try:   # the same oracle on ONE thread: one of 8 x-slabs of the patches, scaled to a full sweep
+        from threadpoolctl import threadpool_limits
+        nx = H.fine.n[0]
+        nslab = 8 if nx >= 16 else 1
+        with threadpool_limits(1):
+            t1 = time.perf_counter()
+            sm.partial_sweep(b, d, 0, nx // nslab)
+            dt1 = (time.perf_counter() - t1) * nslab
+        single = {"value": N / (dt1 * S) / 1e6, "cores": 1,
+                  "sample": "fine-level sweep restricted to the first of %d x-slabs of patches, x %d: %.2f s per "
+                            "sweep" % (nslab, nslab, dt1)}
+    except Exception as e:   # threadpoolctl missing: report the all-core number only
+        single = {"value": None, "cores": 1, "sample": "not run: %s" % e}
+    return {"value": N / (dt * S) / 1e6, "unit": "MDoF*iter/s", "cores": cores, "kind": "oracle",
+            "sample": "one fine-level Alg. 1 sweep of slab 1 of %s (residual, all patch solves, averaging): %.2f s on "
+                      "%d BLAS threads; GMRES iteration extrapolated as %.2f sweeps (V-cycle K2 flops / fine-sweep K2 "
+                      "flops); oracle setup %.1f s excluded" % (cfg["name"], dt, cores, S, t_setup),
+            "single_thread": single, "host": host_info()}
 
 
 def run_reference(args):
