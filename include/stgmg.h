@@ -62,7 +62,8 @@ enum { STGMG_FORM_DSA = 0 /* Problem 3.1 (Eq:DPQ_A0): p-equation cou
 enum { STGMG_LOAD_MANUFACTURED = 0, STGMG_LOAD_BEAM_TRACTION = 1,   /* stgmg_slab_load */
        STGMG_LOAD_LSHAPE_TRACTION = 2 /* Sec. 5.2 traction on the L-shape (stgmg_setup_lshape handles only) */ };
 enum { STGMG_COMM_NCCL = 0 /* nccl_comm is an ncclComm_t */,
-       STGMG_COMM_LOOPBACK = 1 /* nccl_comm is an in-process hub (N emulated ranks on one GPU; tests) */ };
+       STGMG_COMM_LOOPBACK = 1 /* nccl_comm is an in-process hub (N emulated ranks on one GPU; tests) */,
+       STGMG_COMM_SHM = 2 /* nccl_comm is a stgmg_shm_comm_create communicator (one process per rank) */ };
 
 /* Structured box, fine level (nested quad/hex levels, h_l = h_{l-1}/2). */
 typedef struct {
@@ -212,6 +213,15 @@ int stgmg_nccl_comm_destroy(void* comm);
  * each with its own handle and stream; the host synchronises at every exchange). */
 void* stgmg_loopback_hub_create(int nranks);
 void stgmg_loopback_hub_destroy(void* hub);
+
+/* Process-separated shared-memory communicator (comm_kind STGMG_COMM_SHM): one PROCESS per rank (as under torchrun),
+ * on one GPU or several, without NCCL.  Messages are staged through a POSIX shared-memory segment /<name> (rank 0
+ * creates and finally unlinks it; the others attach, waiting up to ~20 s) with a mailbox of cap_doubles doubles per
+ * message slot; a sense-reversing barrier on process-shared atomics orders the exchanges (host-synchronised, not
+ * graph-capturable).  Every rank passes the same name, nranks and cap; comm_out is owned by the caller, who destroys it
+ * (collectively) after the handle.  Errors: -1 bad argument, -4 (ENCCL) segment not created / attached. */
+int stgmg_shm_comm_create(const char* name, int nranks, int rank, int64_t cap_doubles, void** comm_out);
+int stgmg_shm_comm_destroy(void* comm);
 
 /* Diagnostics: number of patch classes on level l, their sizes C_P and the number of kernels launched by
  * the last stgmg_solve (for the bench's gpu_launches field). */

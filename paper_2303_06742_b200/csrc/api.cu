@@ -1847,7 +1847,8 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
   h->rank = nranks > 1 ? params->rank : 0;
   if (nranks > 1) {
     h->tr = params->comm_kind == STGMG_COMM_LOOPBACK ? make_loopback_transport(params->nccl_comm, h->rank)
-                                                    : make_nccl_transport(params->nccl_comm, h->rank, nranks);
+            : params->comm_kind == STGMG_COMM_SHM    ? make_shm_transport(params->nccl_comm)
+                                                     : make_nccl_transport(params->nccl_comm, h->rank, nranks);
     if (!h->tr) return STGMG_ENCCL;
     h->graphable = h->tr->graph_capturable();
   }
@@ -2913,6 +2914,10 @@ int stgmg_nccl_comm_create(const unsigned char id[128], int nranks, int rank, vo
   return nccl_comm_create(id, nranks, rank, comm_out);
 }
 int stgmg_nccl_comm_destroy(void* comm) { return nccl_comm_destroy(comm); }
+int stgmg_shm_comm_create(const char* name, int nranks, int rank, int64_t cap_doubles, void** comm_out) {
+  return shm_comm_create(name, nranks, rank, (long long)cap_doubles, comm_out);
+}
+int stgmg_shm_comm_destroy(void* comm) { return shm_comm_destroy(comm); }
 void* stgmg_loopback_hub_create(int nranks) { return loopback_hub_create(nranks); }
 void stgmg_loopback_hub_destroy(void* hub) { loopback_hub_destroy(hub); }
 

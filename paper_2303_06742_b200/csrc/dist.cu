@@ -5,12 +5,22 @@
 //   * transports: NCCL (ncclSend/ncclRecv to the x-neighbours, ncclAllReduce for dot products, ncclAllGather for
 //     the agglomerated coarse levels), loaded with dlopen so that single-GPU use needs no NCCL; and an in-process
 //     loopback transport (N emulated ranks on one GPU, one host thread each; the host synchronises at every
-//     exchange, no kernel ever waits on another rank) used by the multi-rank parity tests.
+//     exchange, no kernel ever waits on another rank) used by the multi-rank parity tests; and a PROCESS-separated
+//     shared-memory transport (one process per rank, host-staged messages in a POSIX shared-memory segment, a
+//     sense-reversing barrier on process-shared atomics) that runs the per-rank bootstrap and handles exactly as
+//     under torchrun, on one GPU or several, without NCCL.
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "dist.cuh"
@@ -275,5 +285,164 @@ struct LoopbackTransport : Transport {
 void* loopback_hub_create(int n) { return new LoopbackHub(n); }
 void loopback_hub_destroy(void* h) { delete (LoopbackHub*)h; }
 Transport* make_loopback_transport(void* hub, int rank) { return new LoopbackTransport((LoopbackHub*)hub, rank); }
+
+// ------------------------------------------------------------------------ shared memory (process ranks) ------
+// Segment layout: header {magic, nranks, slot doubles, arrived, generation}, then per rank a mailbox of
+// 3 slots (left halo, right halo, allgather) of `cap` doubles each and 16 doubles of reduction scratch.
+struct ShmHeader {
+  std::atomic<long long> magic;
+  int nranks;
+  long long cap;
+  std::atomic<int> arrived;
+  std::atomic<long long> generation;
+  std::atomic<int> attached;
+};
+
+struct ShmComm {
+  int rank = 0, nranks = 1;
+  long long cap = 0;
+  size_t bytes = 0;
+  void* base = nullptr;
+  ShmHeader* hdr = nullptr;
+  double* data = nullptr;
+  char name[128] = {0};
+  bool owner = false;
+  double* slot(int q, int k) { return data + ((size_t)q * 3 + k) * (size_t)cap; }
+  double* red(int q) { return data + (size_t)nranks * 3 * (size_t)cap + (size_t)q * 16; }
+  void barrier() {
+    const long long gen = hdr->generation.load(std::memory_order_acquire);
+    if (hdr->arrived.fetch_add(1, std::memory_order_acq_rel) + 1 == nranks) {
+      hdr->arrived.store(0, std::memory_order_relaxed);
+      hdr->generation.store(gen + 1, std::memory_order_release);
+    } else {
+      while (hdr->generation.load(std::memory_order_acquire) == gen) sched_yield();
+    }
+  }
+};
+
+static constexpr long long kShmMagic = 0x73746d676d73686dLL;
+
+int shm_comm_create(const char* name, int nranks, int rank, long long cap_doubles, void** out) {
+  if (!name || !out || nranks < 1 || rank < 0 || rank >= nranks || cap_doubles < 1 || std::strlen(name) > 100) {
+    set_error("shm comm: bad argument");
+    return -1;
+  }
+  auto* c = new ShmComm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->cap = cap_doubles;
+  std::snprintf(c->name, sizeof(c->name), "/%s", name[0] == '/' ? name + 1 : name);
+  c->bytes = sizeof(ShmHeader) + 64 + sizeof(double) * ((size_t)nranks * 3 * (size_t)cap_doubles + (size_t)nranks * 16);
+  int fd = -1;
+  if (rank == 0) {
+    fd = shm_open(c->name, O_CREAT | O_RDWR, 0600);
+    if (fd >= 0 && ftruncate(fd, (off_t)c->bytes) != 0) { close(fd); fd = -1; }
+    c->owner = true;
+  } else {
+    for (int it = 0; it < 20000 && fd < 0; ++it) {   // rank 0 creates the segment; wait up to ~20 s
+      fd = shm_open(c->name, O_RDWR, 0600);
+      if (fd < 0) usleep(1000);
+    }
+  }
+  if (fd < 0) { set_error(std::string("shm comm: shm_open failed for ") + c->name); delete c; return -4; }
+  for (int it = 0; it < 20000; ++it) {   // the segment may not be sized yet
+    struct stat st;
+    if (fstat(fd, &st) == 0 && (size_t)st.st_size >= c->bytes) break;
+    usleep(1000);
+  }
+  c->base = mmap(nullptr, c->bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (c->base == MAP_FAILED) { set_error("shm comm: mmap failed"); delete c; return -4; }
+  c->hdr = reinterpret_cast<ShmHeader*>(c->base);
+  c->data = reinterpret_cast<double*>(reinterpret_cast<char*>(c->base) + ((sizeof(ShmHeader) + 63) / 64) * 64);
+  if (rank == 0) {
+    c->hdr->nranks = nranks;
+    c->hdr->cap = cap_doubles;
+    c->hdr->arrived.store(0);
+    c->hdr->generation.store(0);
+    c->hdr->attached.store(0);
+    c->hdr->magic.store(kShmMagic, std::memory_order_release);
+  } else {
+    for (int it = 0; it < 20000 && c->hdr->magic.load(std::memory_order_acquire) != kShmMagic; ++it) usleep(1000);
+    if (c->hdr->magic.load() != kShmMagic || c->hdr->nranks != nranks || c->hdr->cap != cap_doubles) {
+      set_error("shm comm: segment not initialised or ranks / capacity disagree");
+      munmap(c->base, c->bytes);
+      delete c;
+      return -4;
+    }
+  }
+  // pinned host staging for the DMA copies (optional: pageable copies work too)
+  cudaHostRegister(c->data, c->bytes - ((char*)c->data - (char*)c->base), cudaHostRegisterDefault);
+  cudaGetLastError();
+  c->hdr->attached.fetch_add(1);
+  c->barrier();   // every rank attached before any exchange
+  *out = c;
+  return 0;
+}
+
+int shm_comm_destroy(void* comm) {
+  auto* c = (ShmComm*)comm;
+  if (!c) return 0;
+  c->barrier();
+  cudaHostUnregister(c->data);
+  cudaGetLastError();
+  munmap(c->base, c->bytes);
+  if (c->owner) shm_unlink(c->name);
+  delete c;
+  return 0;
+}
+
+struct ShmTransport : Transport {
+  ShmComm* c;
+  explicit ShmTransport(ShmComm* comm) : c(comm) { rank = comm->rank; nranks = comm->nranks; }
+  bool graph_capturable() const override { return false; }
+  int check(long long n) {
+    if (n > c->cap) { set_error("shm transport: message of " + std::to_string(n) + " doubles exceeds the slot"); return -4; }
+    return 0;
+  }
+  int halo(const double* sl, long long nsl, const double* sr, long long nsr, double* rl, long long nrl, double* rr,
+           long long nrr, cudaStream_t s) override {
+    if (check(nsl) || check(nsr) || check(nrl) || check(nrr)) return -4;
+    if (nsl && cudaMemcpyAsync(c->slot(rank, 0), sl, sizeof(double) * nsl, cudaMemcpyDeviceToHost, s)) return -3;
+    if (nsr && cudaMemcpyAsync(c->slot(rank, 1), sr, sizeof(double) * nsr, cudaMemcpyDeviceToHost, s)) return -3;
+    if (cudaStreamSynchronize(s) != cudaSuccess) { set_error("shm transport: stream sync"); return -3; }
+    c->barrier();
+    if (nrl && cudaMemcpyAsync(rl, c->slot(rank - 1, 1), sizeof(double) * nrl, cudaMemcpyHostToDevice, s)) return -3;
+    if (nrr && cudaMemcpyAsync(rr, c->slot(rank + 1, 0), sizeof(double) * nrr, cudaMemcpyHostToDevice, s)) return -3;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return -3;
+    c->barrier();   // the neighbours' slots may be reused only after both reads
+    return 0;
+  }
+  int allreduce_sum(double* v, int n, cudaStream_t s) override {
+    if (n > 16) { set_error("shm allreduce: n > 16"); return -1; }
+    double loc[16];
+    if (cudaMemcpyAsync(loc, v, sizeof(double) * n, cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s)) return -3;
+    std::memcpy(c->red(rank), loc, sizeof(double) * n);
+    c->barrier();
+    for (int i = 0; i < n; ++i) {
+      double t = 0.0;
+      for (int q = 0; q < nranks; ++q) t += c->red(q)[i];   // fixed rank order: identical on every rank
+      loc[i] = t;
+    }
+    c->barrier();
+    if (cudaMemcpyAsync(v, loc, sizeof(double) * n, cudaMemcpyHostToDevice, s) || cudaStreamSynchronize(s)) return -3;
+    return 0;
+  }
+  int allgather(const double* send, long long n, double* recv, cudaStream_t s) override {
+    if (check(n)) return -4;
+    if (cudaMemcpyAsync(c->slot(rank, 2), send, sizeof(double) * n, cudaMemcpyDeviceToHost, s) ||
+        cudaStreamSynchronize(s))
+      return -3;
+    c->barrier();
+    for (int q = 0; q < nranks; ++q)
+      if (cudaMemcpyAsync(recv + (long long)q * n, c->slot(q, 2), sizeof(double) * n, cudaMemcpyHostToDevice, s))
+        return -3;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return -3;
+    c->barrier();
+    return 0;
+  }
+};
+
+Transport* make_shm_transport(void* comm) { return comm ? new ShmTransport((ShmComm*)comm) : nullptr; }
 
 }  // namespace stgmg

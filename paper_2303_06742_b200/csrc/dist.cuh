@@ -20,6 +20,9 @@ Transport* make_nccl_transport(void* comm, int rank, int nranks);
 void* loopback_hub_create(int n);
 void loopback_hub_destroy(void* hub);
 Transport* make_loopback_transport(void* hub, int rank);
+Transport* make_shm_transport(void* comm);
+int shm_comm_create(const char* name, int nranks, int rank, long long cap_doubles, void** out);
+int shm_comm_destroy(void* comm);
 int nccl_unique_id(unsigned char out[128]);
 int nccl_comm_create(const unsigned char id[128], int nranks, int rank, void** comm);
 int nccl_comm_destroy(void* comm);

@@ -89,6 +89,9 @@ SIGNATURES = {
     "stgmg_nccl_comm_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
     "stgmg_nccl_comm_destroy": (ctypes.c_int, [_P]),
     "stgmg_loopback_hub_create": (_P, [ctypes.c_int]),
+    "stgmg_shm_comm_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                             ctypes.POINTER(_P)]),
+    "stgmg_shm_comm_destroy": (ctypes.c_int, [_P]),
     "stgmg_loopback_hub_destroy": (None, [_P]),
 }
 
@@ -162,7 +165,7 @@ def _host_ptr(a, n):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-COMM_NCCL, COMM_LOOPBACK = 0, 1
+COMM_NCCL, COMM_LOOPBACK, COMM_SHM = 0, 1, 2
 
 
 def make_mesh(cfg):
@@ -232,6 +235,19 @@ def nccl_comm_create(uid, nranks, rank):
 
 def nccl_comm_destroy(comm):
     load_library().stgmg_nccl_comm_destroy(comm)
+
+
+def shm_comm_create(name, nranks, rank, cap_doubles=1 << 22):
+    """Process-separated shared-memory communicator (one process per rank; stgmg_shm_comm_create)."""
+    lib = load_library()
+    comm = ctypes.c_void_p()
+    _check(lib.stgmg_shm_comm_create(name.encode(), int(nranks), int(rank), int(cap_doubles), ctypes.byref(comm)),
+           "stgmg_shm_comm_create")
+    return comm
+
+
+def shm_comm_destroy(comm):
+    load_library().stgmg_shm_comm_destroy(comm)
 
 
 def loopback_hub(nranks):
