@@ -122,7 +122,8 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
  * fine level; levels = ref_fine - ref_coarse + 1 (Table 4: coarse level ref_1).  Boundary parts as DESIGN.md
  * readings N3-R1/R2: u = 0 on y = 0; directional on x = 0 and z = 0, .5; traction t_N on y = 1 (x < .5); free on
  * x = 1 and the re-entrant faces; p = 0 on y = 1 (x < .5), no flux elsewhere.  params: rho, alpha, c0, lambda, mu, K,
- * tau, gamma_a, gamma_b (gamma = gamma_b of the SIP term), omega, jmax, stream (mesh, bc, hF_mode, smoother,
+ * tau, gamma_a, gamma_b (gamma = gamma_b of the SIP term), hF_mode (penalty length of the Nitsche, directional and
+ * SIP terms: cell measure h^3 by default, reading A6; STGMG_HF_EDGE: h), omega, jmax, stream (mesh, bc, smoother,
  * formulation and nranks are not used: single GPU, Alg. 1, Problem 3.1).  Level operators are assembled (CSR) on the
  * host at setup from element integrals; every patch has its own explicit inverse (K4 on the device).  Vector layout per
  * Radau node: V_0..V_2, U_0..U_2 on the active Q_r nodes (lexicographic over the (2 r 2^ref + 1)^2 (r 2^ref + 1) node
@@ -244,9 +245,10 @@ int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double*
 int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms);
 
 /* Algorithmic work of one launch of stgmg_time_kernel's kind on level l (SURVEY §8(d) "Binding roofline"):
- * kind 0 (K2): flops 2 sum_P C_P^2, bytes 16 sum_P C_P + 8 sum_classes C_P^2; kind 1 (K1, y = A x): 16 N_l bytes;
+ * kind 0 (K2): flops 2 sum_P C_P^2, bytes 16 sum_P C_P + 8 sum_classes C_P^2; kind 1 (K1, y = A x): 16 N_l bytes
+ * and the sum-factorised flop count (k+1) n_cells [(6d^2+5d) 2 (r+1)^(d+1) + c_pt (r+1)^d], c_pt = 60 (2D) / 100 (3D);
  * kind 2 (K3): 16 N_l + 8 sum_P C_P bytes (read Y, read and write d; 1/p is structural); kind 7 (K5 restrict +
- * prolong-add): 24 N_l + 16 N_{l-1} bytes; kind 8 (K7 fused MGS pass): 32 N bytes.  flops = 0 for the HBM kinds.
+ * prolong-add): 24 N_l + 16 N_{l-1} bytes; kind 8 (K7 fused MGS pass): 32 N bytes.  flops = 0 for kinds 2, 7, 8.
  * EINVAL for other kinds. */
 int stgmg_kernel_work(const stgmg_handle* h, int kind, int level, double* flops, double* bytes);
 

@@ -179,7 +179,12 @@ class LForms:
         self.exps = p_exponents(r - 1)
         self.vol = float(np.prod(self.h))
         # |K|_d, also the SIP average on a uniform mesh (R4); hF_fixed: frozen h_F (Galerkin-identity pin only)
-        self.hF = float(params["hF_fixed"]) if params.get("hF_fixed") is not None else self.vol
+        if params.get("hF_fixed") is not None:
+            self.hF = float(params["hF_fixed"])
+        else:   # |K|_d (reading A6), or the edge length with hF_mode = 1 (the flag of the structured path)
+            self.hF = float(self.h[0]) if params.get("hF_mode", 0) == 1 else self.vol
+        # penalty length of the directional faces: h_F (reading R4), or the literal h of a^d_gamma (hF_mode = 2)
+        self.hD = float(self.h[0]) if params.get("hF_mode", 0) in (1, 2) else self.hF
         self.K = np.asarray(params["K"], dtype=np.float64).reshape(3, 3)
 
     def _pts(self, face=None):
@@ -221,7 +226,7 @@ class LForms:
         Vf = self.ef._vec_val(phq)
         _, sig = self.ef._stress(Gf)
         sn = np.einsum("Iqab,b->Iqa", sig, n)               # sigma(psi_I) n
-        pen = self.p["gamma_a"] / self.hF
+        pen = self.p["gamma_a"] / (self.hF if kind == U_DIRICHLET else self.hD)
         vn = np.einsum("Jqa,a->Jq", Vf, n)                    # psi_J . n
         if kind == U_DIRICHLET:
             A = (-np.einsum("Jqa,Iqa,q->IJ", sn, Vf, w) - np.einsum("Jqa,Iqa,q->IJ", Vf, sn, w)

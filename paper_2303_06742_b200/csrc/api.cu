@@ -376,6 +376,7 @@ struct LevelData {
   bool exp_fused = false;       // STGMG_EXPAND_FUSED=1: the push-form gather_expand instead
   // unstructured level (SURVEY N3, L-shape): CSR operator / transfers / averaging table above, plus one explicit
   // inverse per vertex patch (K2u, csrc/lshape.cu)
+  double* rtmp = nullptr;       // intermediates of the separable restriction (levels with >= 1M DoFs)
   bool unstr = false;
   int* pz = nullptr;            // concatenated Z(P)
   long long* pzoff = nullptr;   // start of Z(P) and of y_P
@@ -644,8 +645,12 @@ static int restrict_level(stgmg_handle* h, int l, const double* rf, double* bc) 
   LevelData& Lv = h->lev[l];
   if (Lv.R_rp)
     CKE(launch_csr_spmv((int)h->lev[l - 1].g.N, Lv.R_lpr, Lv.R_rp, Lv.R_ci, Lv.R_v, rf, nullptr, bc, 1.0, 0.0, h->s));
-  else
+  else if (Lv.rtmp) {   // large levels: axis-by-axis restriction (coalesced passes)
+    CKE(launch_restrict_sep(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, rf, bc, Lv.rtmp, h->s));
+    h->launches += h->d - 1;
+  } else {
     CKE(launch_restrict(Lv.g, h->lev[l - 1].g, h->k1, Lv.tt, rf, bc, h->s));
+  }
   h->launches += 1;
   return 0;
 }
@@ -1434,6 +1439,10 @@ static int build_transfer(stgmg_handle* h, int l) {
       T = Interp1D{rpf, cif, vf, rpc, cic, vc};
     }
   }
+  // separable restriction on levels with >= 1M DoFs (its intermediates hold < N_l doubles); STGMG_RESTRICT_SEP=0: off
+  const char* sep_env = std::getenv("STGMG_RESTRICT_SEP");
+  const bool sep_off = sep_env && std::atoi(sep_env) == 0;
+  if (!sep_off && F.g.N >= 1000000 && !F.R_rp) CK(dalloc(h, &F.rtmp, (size_t)F.g.N));
   return 0;
 }
 
@@ -2132,7 +2141,7 @@ int stgmg_setup_lshape(int ref_fine, int levels, const stgmg_order* order, const
   {
     NvtxRange nv2("stgmg setup: L-shape host assembly");
     std::string err;
-    const int rc = lshape_build_host(ref_fine - levels + 1, levels, r, k, h->c, host, err);
+    const int rc = lshape_build_host(ref_fine - levels + 1, levels, r, k, h->c, params->hF_mode, host, err);
     if (rc) { set_error(err); return rc; }
   }
   h->lev.resize(levels);
@@ -2770,7 +2779,16 @@ int stgmg_kernel_work(const stgmg_handle* h, int kind, int level, double* flops,
   *flops = 0.0;
   switch (kind) {
     case 0: *flops = fl2; *bytes = 16.0 * sumcp + invb; break;                 // K2
-    case 1: *bytes = 16.0 * N; break;                                          // K1: read x, write y
+    case 1: {   // K1: read x, write y; flops = SURVEY §8(d)'s sum-factorised count (the algorithmic work, not the
+                // padded factored-GEMM flops the kernel issues): (k+1) n_cells [(6d^2+5d) 2 (r+1)^(d+1) + c_pt (r+1)^d]
+      *bytes = 16.0 * N;
+      const int d = h->d, r1 = h->r + 1;
+      double nc = 1.0, rp = 1.0;
+      for (int a = 0; a < d; ++a) { nc *= Lv.g.n[a]; rp *= r1; }
+      const double cpt = d == 3 ? 100.0 : 60.0;
+      *flops = (double)h->k1 * nc * ((6.0 * d * d + 5.0 * d) * 2.0 * rp * r1 + cpt * rp);
+      break;
+    }
     case 2: *bytes = 16.0 * N + 8.0 * sumcp; break;                            // K3: read Y, read + write d
     case 7: {                                                                  // K5: restrict + prolong-add
       if (level < 1) { set_error("kind 7 needs level >= 1"); return STGMG_EINVAL; }

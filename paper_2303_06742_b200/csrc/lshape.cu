@@ -226,7 +226,7 @@ struct ElemMats {
 
 struct Forms {
   int r = 2;
-  double h = 1.0, hF = 1.0;
+  double h = 1.0, hF = 1.0, hD = 1.0;   // hD: penalty length of the directional faces
   double lam = 1, mu = 1, alpha = 1, rho = 1, c0 = 1, ga = 1, gb = 1, K[3][3] = {{0}};
   std::vector<double> nd;
   Exps ex;
@@ -284,7 +284,7 @@ struct Forms {
     const int fa = f / 2;
     const double n[3] = {fa == 0 ? (f % 2 ? 1.0 : -1.0) : 0.0, fa == 1 ? (f % 2 ? 1.0 : -1.0) : 0.0,
                          fa == 2 ? (f % 2 ? 1.0 : -1.0) : 0.0};
-    const double pen = ga / hF;
+    const double pen = ga / (kind == 0 ? hF : hD);
     const Quad Q = face_quad(r + 1, h, f);
     for (size_t q = 0; q < Q.w.size(); ++q) {
       const double xh[3] = {Q.x[q][0], Q.x[q][1], Q.x[q][2]};
@@ -466,7 +466,9 @@ struct LGrid {
 
 }  // namespace
 
-int lshape_build_host(int ref_coarse, int levels, int r, int k, const OpConsts& oc, LsHost& out, std::string& err) {
+int lshape_build_host(int ref_coarse, int levels, int r, int k, const OpConsts& oc, int hf_mode, LsHost& out,
+                      std::string& err) {
+  const bool hf_edge = hf_mode == 1;
   if (r != 2 && r != 3) { err = "L-shape: r must be 2 or 3"; return STGMG_ENOTSUP; }
   if (k < 0 || k + 1 > kMaxK1) { err = "L-shape: k out of range"; return STGMG_ENOTSUP; }
   const int k1 = k + 1;
@@ -489,7 +491,9 @@ int lshape_build_host(int ref_coarse, int levels, int r, int k, const OpConsts& 
     Forms F;
     F.r = r;
     F.h = g.h;
-    F.hF = g.h * g.h * g.h;   // |K|_d (reading A6 / N3-R4); the SIP average on a uniform mesh
+    // |K|_d (reading A6 / N3-R4; the SIP average on a uniform mesh), or the edge length h (STGMG_HF_EDGE)
+    F.hF = hf_edge ? g.h : g.h * g.h * g.h;
+    F.hD = (hf_edge || hf_mode == 2) ? g.h : F.hF;   // mode 2: a^d_gamma with the literal h^-1 of P:L778
     F.lam = oc.lam;
     F.mu = oc.mu;
     F.alpha = oc.alpha;

@@ -202,6 +202,8 @@ cudaError_t launch_restrict(const LevelGeom& fine, const LevelGeom& coarse, int 
                             const double* rf, double* bc, cudaStream_t s);
 cudaError_t launch_prolong_add(const LevelGeom& fine, const LevelGeom& coarse, int k1, const TransferTables& t,
                                const double* dc, double* df, cudaStream_t s);
+cudaError_t launch_restrict_sep(const LevelGeom& fine, const LevelGeom& coarse, int k1, const TransferTables& t,
+                                const double* rf, double* bc, double* tmp, cudaStream_t s);
 // K6: y = A x dense (coarse solve, row-major lda).
 cudaError_t launch_gemv(const double* A, int n, int lda, const double* x, double* y, cudaStream_t s);
 
@@ -225,7 +227,8 @@ struct LsHost {
   std::vector<double> fN;             // -<t_N, chi> per unit sin(8 pi t), U components (3 nq), fine level
   std::vector<double> wu, wp;         // goal weights on Gamma_m: U_x nodes (nq), P DoFs (np)
 };
-int lshape_build_host(int ref_coarse, int levels, int r, int k, const OpConsts& oc, LsHost& out, std::string& err);
+int lshape_build_host(int ref_coarse, int levels, int r, int k, const OpConsts& oc, int hf_mode, LsHost& out,
+                      std::string& err);
 cudaError_t launch_csr_extract_patches(const int* rp, const int* ci, const double* v, const int* pz,
                                        const long long* pzoff, const int* pcp, int p0, int np, double* out, int lda,
                                        cudaStream_t s);

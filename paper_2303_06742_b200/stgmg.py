@@ -426,7 +426,7 @@ class LShapeSolver(Solver):
     L-shape with 2^ref_fine cells per cube edge, levels ref_fine - levels + 1 .. ref_fine.  params: dict with rho,
     alpha, c0, lam, mu, K (9 entries), gamma_a, gamma_b (< 0: defaults of P:L209-211)."""
 
-    def __init__(self, ref_fine, levels, r, k, tau, params, stream=None, omega=0.7, jmax=4):
+    def __init__(self, ref_fine, levels, r, k, tau, params, stream=None, omega=0.7, jmax=4, hF_mode=HF_MEASURE):
         import torch
         if not torch.cuda.is_available():
             raise StgmgError("no CUDA device: the stgmg product path has no CPU fallback")
@@ -441,6 +441,7 @@ class LShapeSolver(Solver):
         p.gamma_a = float(params.get("gamma_a", -1.0))
         p.gamma_b = float(params.get("gamma_b", -1.0))
         p.omega, p.jmax = omega, jmax
+        p.hF_mode = int(hF_mode)
         p.nranks, p.rank = 1, 0
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         p.stream = ctypes.c_void_p(self.stream.cuda_stream)

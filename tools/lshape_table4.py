@@ -35,10 +35,11 @@ ap.add_argument("--E", type=float, default=20000.0)
 ap.add_argument("--tol", type=float, default=1e-8)
 ap.add_argument("--abs", action="store_true")
 ap.add_argument("--T", type=float, default=4.0)
+ap.add_argument("--hf", default="measure", choices=["measure", "edge", "dir_edge"])
 a = ap.parse_args()
 tau = 0.01
 t0 = time.perf_counter()
-s = LShapeSolver(a.ref, a.ref - a.coarse + 1, a.r, a.k, tau, params(a.r, a.E))
+s = LShapeSolver(a.ref, a.ref - a.coarse + 1, a.r, a.k, tau, params(a.r, a.E), hF_mode={"measure": 0, "edge": 1, "dir_edge": 2}[a.hf])
 setup = time.perf_counter() - t0
 N = s.size()
 X = torch.zeros(N, dtype=torch.float64, device="cuda")
@@ -56,7 +57,7 @@ for n in range(nsl):
     X.copy_(x)
     goal.append(s.goal_quantities(X, 1))
 g = np.array(goal)
-print(json.dumps(dict(ref=a.ref, coarse=a.coarse, k=a.k, r=a.r, E=a.E, dofs=N, tol=a.tol, tol_mode="abs" if a.abs else "rel",
+print(json.dumps(dict(ref=a.ref, coarse=a.coarse, k=a.k, r=a.r, E=a.E, hF=a.hf, dofs=N, tol=a.tol, tol_mode="abs" if a.abs else "rel",
                       slabs=nsl, avg_its=float(np.mean(its)), min_its=int(min(its)), max_its=int(max(its)),
                       converged=int(sum(conv)), bu=[float(g[:, 0].min()), float(g[:, 0].max())],
                       bp=[float(g[:, 1].min()), float(g[:, 1].max())], s_per_slab=float(np.median(secs)),
