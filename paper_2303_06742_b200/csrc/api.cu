@@ -376,7 +376,7 @@ struct LevelData {
   bool exp_fused = false;       // STGMG_EXPAND_FUSED=1: the push-form gather_expand instead
   // unstructured level (SURVEY N3, L-shape): CSR operator / transfers / averaging table above, plus one explicit
   // inverse per vertex patch (K2u, csrc/lshape.cu)
-  double* rtmp = nullptr;       // intermediates of the separable restriction (levels with >= 1M DoFs)
+  double* rtmp = nullptr;       // intermediates of the separable restriction (levels with >= 200k DoFs)
   bool unstr = false;
   int* pz = nullptr;            // concatenated Z(P)
   long long* pzoff = nullptr;   // start of Z(P) and of y_P
@@ -928,7 +928,17 @@ std::vector<TileDesc> stgmg::balanced_tiles(const std::vector<int>& cp, const st
       }
     }
   }
-  std::stable_sort(groups.begin(), groups.end(), [](const Group& a, const Group& b) { return a.w > b.w; });
+  // heaviest first (load balance over the resident slots); among equal weights, column-tile major: the row blocks
+  // (m0) of one column tile run back to back, so its B operand (the expanded residual, GBs on the fine 3D levels)
+  // comes from DRAM once and from L2 for the other row blocks (ncu, cfg4 fine K2D: 48.2 GB DRAM per launch with
+  // m0-major order, 6.3x the algorithmic bytes).  Order only: every tile computes the same sums.
+  std::stable_sort(groups.begin(), groups.end(), [](const Group& a, const Group& b) {
+    if (a.w != b.w) return a.w > b.w;
+    const TileDesc &x = a.t.front(), &y = b.t.front();
+    if (x.cls != y.cls) return x.cls < y.cls;
+    if (x.n0 != y.n0) return x.n0 < y.n0;
+    return x.m0 < y.m0;
+  });
   std::vector<TileDesc> out;
   for (const auto& gq : groups)
     for (const auto& t : gq.t) out.push_back(t);
@@ -1439,10 +1449,11 @@ static int build_transfer(stgmg_handle* h, int l) {
       T = Interp1D{rpf, cif, vf, rpc, cic, vc};
     }
   }
-  // separable restriction on levels with >= 1M DoFs (its intermediates hold < N_l doubles); STGMG_RESTRICT_SEP=0: off
+  // separable restriction on levels with >= 200k DoFs (its intermediates hold < N_l doubles); STGMG_RESTRICT_SEP=0:
+  // off
   const char* sep_env = std::getenv("STGMG_RESTRICT_SEP");
   const bool sep_off = sep_env && std::atoi(sep_env) == 0;
-  if (!sep_off && F.g.N >= 1000000 && !F.R_rp) CK(dalloc(h, &F.rtmp, (size_t)F.g.N));
+  if (!sep_off && F.g.N >= 200000 && F.g.N < (1LL << 31)) CK(dalloc(h, &F.rtmp, (size_t)F.g.N));
   return 0;
 }
 

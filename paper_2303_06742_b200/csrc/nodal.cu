@@ -562,34 +562,39 @@ __global__ void __launch_bounds__(256) restrict_pass_kernel(const double* __rest
                                                             double* __restrict__ out, SepDims dout, int axis,
                                                             Interp1D tq, Interp1D tp) {
   pdl_trigger();
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)K1 * dout.blk) return;
-  const int m = (int)(idx / dout.blk);
-  const long long rem = idx - (long long)m * dout.blk;
-  const bool pres = rem >= 2 * D * dout.nq;
-  const int slot = pres ? 2 * D : (int)(rem / dout.nq);
-  long long node = pres ? rem - 2 * D * dout.nq : rem - (long long)slot * dout.nq;
+  // 32-bit index arithmetic (every level vector here has < 2^31 entries; 64-bit divisions dominated the first
+  // version of this kernel)
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int blk = (int)dout.blk, nq = (int)dout.nq;
+  if (idx >= K1 * blk) return;
+  const int m = idx / blk;
+  const int rem = idx - m * blk;
+  const bool pres = rem >= 2 * D * nq;
+  const int slot = pres ? 2 * D : rem / nq;
+  int node = pres ? rem - 2 * D * nq : rem - slot * nq;
   const int* od = pres ? dout.p : dout.q;
   const int* id = pres ? di.p : di.q;
   int c[3] = {0, 0, 0};
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    c[a] = (int)(node % od[a]);
-    node /= od[a];
+  for (int a = 0; a < D - 1; ++a) {
+    const int q = node / od[a];
+    c[a] = node - q * od[a];
+    node = q;
   }
-  long long base = 0, st = 1, sa = 1;   // input offset without the contracted axis; stride of that axis
+  c[D - 1] = node;
+  int base = 0, st = 1, sa = 1;   // input offset without the contracted axis; stride of that axis
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     if (a == axis) sa = st;
-    else base += (long long)c[a] * st;
+    else base += c[a] * st;
     st *= id[a];
   }
   const Interp1D& T = pres ? tp : tq;
   const double* src = in + (long long)m * di.blk + (pres ? 2 * D * di.nq : (long long)slot * di.nq) + base;
+  const int lo = __ldg(T.rp_c + c[axis]), hi = __ldg(T.rp_c + c[axis] + 1);
   pdl_wait();
-  const int lo = T.rp_c[c[axis]], hi = T.rp_c[c[axis] + 1];
   double acc = 0.0;
-  for (int e = lo; e < hi; ++e) acc = fma(T.v_c[e], __ldg(src + (long long)T.ci_c[e] * sa), acc);
+  for (int e = lo; e < hi; ++e) acc = fma(__ldg(T.v_c + e), __ldg(src + __ldg(T.ci_c + e) * sa), acc);
   out[idx] = acc;
 }
 

@@ -1,4 +1,4 @@
-"""The axis-by-axis restriction (nodal.cu restrict_pass_kernel, levels with >= 1M DoFs) against the per-coarse-node
+"""The axis-by-axis restriction (nodal.cu restrict_pass_kernel, levels with >= 200k DoFs) against the per-coarse-node
 gather form (STGMG_RESTRICT_SEP=0) on the full cfg3 and cfg2 fine levels (-m gpu): b_c = P^T r_f in both;
 only the summation order differs (1e-14 relative).  The V-cycle parity at full size (test_gpu_fullsize*.py) covers it
 against the oracle."""
