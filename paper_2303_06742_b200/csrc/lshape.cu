@@ -493,6 +493,10 @@ int lshape_build_host(int ref_coarse, int levels, int r, int k, const OpConsts& 
     F.h = g.h;
     // |K|_d (reading A6 / N3-R4; the SIP average on a uniform mesh), or the edge length h (STGMG_HF_EDGE)
     F.hF = hf_edge ? g.h : g.h * g.h * g.h;
+    if (hf_mode == 3) {   // mode 3: the FINE level's |K|_d on every level (coarse operators = Galerkin products, pin L5)
+      const double hf = G[levels - 1].h;
+      F.hF = hf * hf * hf;
+    }
     F.hD = (hf_edge || hf_mode == 2) ? g.h : F.hF;   // mode 2: a^d_gamma with the literal h^-1 of P:L778
     F.lam = oc.lam;
     F.mu = oc.mu;

@@ -21,6 +21,8 @@
 // 8 (w % MB) .. +8 of G1 and G2 for the 32 cells in two passes of 16 (A fragments pre-arranged fragment-major in
 // global memory: one coalesced 256-byte load per k-step), and G3 / GP tasks (8 cells, all Radau nodes) follow on the
 // first warps.
+#include <algorithm>
+#include <cstdlib>
 #include <functional>
 
 #include "op_common.cuh"
@@ -79,23 +81,12 @@ struct FgMix {   // temporal constants of the epilogue (T[b][a], theta_b)
   double th[kMaxK1];
 };
 
-template <int D, int R, int K1>
-__global__ void __launch_bounds__(FG<D, R, K1>::NT * 32, 2) op_fgemm_kernel(
-    LevelGeom g, const int4* __restrict__ tiles, const PatchClass* __restrict__ ecls, const int* __restrict__ relidx,
-    const double* __restrict__ A1, const double* __restrict__ A2, const double* __restrict__ A3,
-    const double* __restrict__ AP, long long a2stride, long long a3stride, FgMix mix, const double* __restrict__ x,
-    double* __restrict__ Y, long long ncell) {
-  using F = FG<D, R, K1>;
-  pdl_trigger();
-  extern __shared__ double smem[];
-  double* XE = smem;
-  long long* qb = reinterpret_cast<long long*>(XE + (size_t)F::XR * F::XS);
-  long long* pb = qb + F::NC;
-  long long* pl = pb + F::NC;   // lexicographic cell index (column of Y)
-  const int4 td = tiles[blockIdx.x];   // type, first cell of the type's box (lexicographic), cells, -
-  const PatchClass& pc = ecls[td.x];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < F::NC) {   // cell of column j: box of the type (vlo = cell + 1 per axis), x fastest
+// Column bases of a tile (threads < NC): lowest Q_r / Q_{r-1} node of each cell and its lexicographic index.
+template <int D, int R>
+__device__ __forceinline__ void fg_bases(const LevelGeom& g, const PatchClass& pc, int4 td, long long* qb,
+                                         long long* pb, long long* pl) {
+  constexpr int NC = 32;
+  if (threadIdx.x < NC) {   // cell of column j: box of the type (vlo = cell + 1 per axis), x fastest
     const int j = threadIdx.x;
     long long q = 0, p = 0, v = 0, vs = 1;
     if (j < td.z) {
@@ -113,54 +104,35 @@ __global__ void __launch_bounds__(FG<D, R, K1>::NT * 32, 2) op_fgemm_kernel(
     pb[j] = p;
     pl[j] = v;
   }
-  __syncthreads();
-  pdl_wait();
-  // gather the element inputs: XE[a RA + slot NQK + node][cell] (zero rows pad each slot block); GU elements per
-  // thread and round with all their loads issued before the stores (the loop was bound by one load in flight)
-  const int* rel = relidx + pc.rel_off;
-  constexpr int GU = 8, TOT = F::XR * F::NC;
-  const int nthr = blockDim.x;
-  for (int base = threadIdx.x; base < TOT; base += GU * nthr) {
-    long long src[GU];
-    int dst[GU];
-#pragma unroll
-    for (int u = 0; u < GU; ++u) {
-      const int idx = base + u * nthr;
-      src[u] = -1;
-      dst[u] = -1;
-      if (idx < TOT) {
-        const int row = idx / F::NC, col = idx % F::NC;
-        const int a = row / F::RA, rr = row % F::RA;
-        int e = -1;
-        if (rr < 2 * D * F::NQK) {
-          const int slot = rr / F::NQK, j = rr % F::NQK;
-          if (j < F::NQ) e = a * F::NE1 + slot * F::NQ + j;
-        } else {
-          const int j = rr - 2 * D * F::NQK;
-          if (j < F::NP) e = a * F::NE1 + 2 * D * F::NQ + j;
-        }
-        dst[u] = row * F::XS + col;
-        if (e >= 0 && col < td.z) {
-          const int code = __ldg(rel + e);
-          src[u] = (code >> 1) + ((code & 1) ? pb[col] : qb[col]);
-        }
-      }
-    }
-    double v[GU];
-#pragma unroll
-    for (int u = 0; u < GU; ++u) v[u] = src[u] >= 0 ? __ldg(x + src[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < GU; ++u)
-      if (dst[u] >= 0) XE[dst[u]] = v[u];
+}
+
+// Element DoF e of XE row `row` (-1 for the zero rows that pad each slot block to a multiple of 4).
+template <int D, int R, int K1>
+__device__ __forceinline__ int fg_row_elem(int row) {
+  using F = FG<D, R, K1>;
+  const int a = row / F::RA, rr = row % F::RA;
+  if (rr < 2 * D * F::NQK) {
+    const int slot = rr / F::NQK, j = rr % F::NQK;
+    return j < F::NQ ? a * F::NE1 + slot * F::NQ + j : -1;
   }
-  __syncthreads();
+  const int j = rr - 2 * D * F::NQK;
+  return j < F::NP ? a * F::NE1 + 2 * D * F::NQ + j : -1;
+}
+
+// The G1 / G2 / G3 GEMMs of one tile from its gathered inputs XE and the epilogue (mixing with T, theta; stores).
+template <int D, int R, int K1, int HN>
+__device__ __forceinline__ void fg_compute(const double* XE, const long long* pl, int4 td, const double* __restrict__ A1,
+                                           const double* __restrict__ A2, const double* __restrict__ A3,
+                                           const double* __restrict__ AP, long long a2stride, long long a3stride,
+                                           const FgMix& mix, double* __restrict__ Y, long long ncell) {
+  using F = FG<D, R, K1>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kl = lane & 3, nl = lane >> 2;
   const double* Bl = XE + kl * F::XS + nl;   // this lane's B element: row k0 + kl, column n0 + nl
   if (warp < F::NT) {
     const int c = warp / F::MB, i = warp % F::MB;
     const double* a2 = A2 + td.x * a2stride + (long long)(c * F::MB + i) * F::KS2 * 32 + lane;
     const double* a1 = A1 + (long long)i * F::KS1 * 32 + lane;
-    constexpr int HN = 2;   // n8 blocks per pass (16 cells): keeps the accumulators within ~80 registers
 #pragma unroll 1
     for (int h = 0; h < F::NC / 8; h += HN) {
       // G2: AU_a for rows 8i.. of component c, columns (a, cell)
@@ -259,6 +231,116 @@ __global__ void __launch_bounds__(FG<D, R, K1>::NT * 32, 2) op_fgemm_kernel(
   }
 }
 
+template <int D, int R, int K1>
+__global__ void __launch_bounds__(FG<D, R, K1>::NT * 32, 2) op_fgemm_kernel(
+    LevelGeom g, const int4* __restrict__ tiles, const PatchClass* __restrict__ ecls, const int* __restrict__ relidx,
+    const double* __restrict__ A1, const double* __restrict__ A2, const double* __restrict__ A3,
+    const double* __restrict__ AP, long long a2stride, long long a3stride, FgMix mix, const double* __restrict__ x,
+    double* __restrict__ Y, long long ncell) {
+  using F = FG<D, R, K1>;
+  pdl_trigger();
+  extern __shared__ double smem[];
+  double* XE = smem;
+  long long* qb = reinterpret_cast<long long*>(XE + (size_t)F::XR * F::XS);
+  long long* pb = qb + F::NC;
+  long long* pl = pb + F::NC;   // lexicographic cell index (column of Y)
+  const int4 td = tiles[blockIdx.x];   // type, first cell of the type's box (lexicographic), cells, -
+  const PatchClass& pc = ecls[td.x];
+  fg_bases<D, R>(g, pc, td, qb, pb, pl);
+  __syncthreads();
+  pdl_wait();
+  // gather the element inputs: XE[a RA + slot NQK + node][cell]; GU elements per thread and round with all their
+  // loads issued before the stores (the loop was bound by one load in flight)
+  const int* rel = relidx + pc.rel_off;
+  constexpr int GU = 8, TOT = F::XR * F::NC;
+  const int nthr = blockDim.x;
+  for (int base = threadIdx.x; base < TOT; base += GU * nthr) {
+    long long src[GU];
+    int dst[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int idx = base + u * nthr;
+      src[u] = -1;
+      dst[u] = -1;
+      if (idx < TOT) {
+        const int row = idx / F::NC, col = idx % F::NC;
+        const int e = fg_row_elem<D, R, K1>(row);
+        dst[u] = row * F::XS + col;
+        if (e >= 0 && col < td.z) {
+          const int code = __ldg(rel + e);
+          src[u] = (code >> 1) + ((code & 1) ? pb[col] : qb[col]);
+        }
+      }
+    }
+    double v[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) v[u] = src[u] >= 0 ? __ldg(x + src[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < GU; ++u)
+      if (dst[u] >= 0) XE[dst[u]] = v[u];
+  }
+  __syncthreads();
+  fg_compute<D, R, K1, 2>(XE, pl, td, A1, A2, A3, AP, a2stride, a3stride, mix, Y, ncell);
+}
+
+// Persistent form (STGMG_K1_PERSIST=1): one CTA per SM walks the tiles with a double-buffered input stage — the
+// next tile's element inputs are gathered by 8-byte cp.async into the other buffer while the current tile's GEMMs
+// run, so the gather latency is hidden behind the DMMA work instead of behind a second co-resident CTA.
+__device__ __forceinline__ void fg_cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int D, int R, int K1>
+__global__ void __launch_bounds__(FG<D, R, K1>::NT * 32, 1) op_fgemm_persist_kernel(
+    LevelGeom g, const int4* __restrict__ tiles, int ntiles, const PatchClass* __restrict__ ecls,
+    const int* __restrict__ relidx, const double* __restrict__ A1, const double* __restrict__ A2,
+    const double* __restrict__ A3, const double* __restrict__ AP, long long a2stride, long long a3stride, FgMix mix,
+    const double* __restrict__ x, double* __restrict__ Y, long long ncell) {
+  using F = FG<D, R, K1>;
+  extern __shared__ double smem[];
+  double* XEb[2] = {smem, smem + (size_t)F::XR * F::XS};
+  long long* meta = reinterpret_cast<long long*>(smem + 2 * (size_t)F::XR * F::XS);   // [buf][qb | pb | pl][NC]
+  pdl_trigger();
+  pdl_wait();
+  auto stage = [&](int t, int b) {   // bases, then the asynchronous gather of tile t into buffer b
+    const int4 td = tiles[t];
+    const PatchClass& pc = ecls[td.x];
+    long long* qb = meta + (size_t)b * 3 * F::NC;
+    fg_bases<D, R>(g, pc, td, qb, qb + F::NC, qb + 2 * F::NC);
+    __syncthreads();
+    const int* rel = relidx + pc.rel_off;
+    double* XE = XEb[b];
+    for (int idx = threadIdx.x; idx < F::XR * F::NC; idx += blockDim.x) {
+      const int row = idx / F::NC, col = idx % F::NC;
+      const int e = fg_row_elem<D, R, K1>(row);
+      double* dst = XE + row * F::XS + col;
+      if (e >= 0 && col < td.z) {
+        const int code = __ldg(rel + e);
+        fg_cp_async8(dst, x + (code >> 1) + ((code & 1) ? qb[F::NC + col] : qb[col]));
+      } else {
+        *dst = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int t = blockIdx.x, b = 0;
+  if (t < ntiles) stage(t, 0);
+  for (; t < ntiles; t += gridDim.x, b ^= 1) {
+    const int tn = t + gridDim.x;
+    if (tn < ntiles) {
+      stage(tn, b ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    fg_compute<D, R, K1, 4>(XEb[b], meta + (size_t)b * 3 * F::NC + 2 * F::NC, tiles[t], A1, A2, A3, AP, a2stride,
+                            a3stride, mix, Y, ncell);
+    __syncthreads();   // buffer b is refilled by the stage of the next iteration
+  }
+}
+
 // ------------------------------------------------------------------------------------------- host side -----
 // Fragment-major copy of a row-major (rows x cols) block M into out[(mb * ksteps + ks) * 32 + lane] = the m8n8k4 A
 // fragment element (row 8 mb + lane / 4, k 4 ks + lane % 4) of the padded matrix; the column map kcol (padded k ->
@@ -349,6 +431,19 @@ static cudaError_t launch_fg(const LevelGeom& g, const int4* tiles, int ntiles, 
   for (int b = 0; b < kMaxK1; ++b) {
     mix.th[b] = c.theta[b];
     for (int a = 0; a < kMaxK1; ++a) mix.T[b][a] = c.T[b][a];
+  }
+  static const bool persist = std::getenv("STGMG_K1_PERSIST") && std::atoi(std::getenv("STGMG_K1_PERSIST")) != 0;
+  if (persist) {
+    const size_t smem = 2 * sizeof(double) * (size_t)F::XR * F::XS + 2 * 3 * sizeof(long long) * F::NC;
+    static PerDeviceOnce attrp;
+    attrp.run([smem] {
+      cudaFuncSetAttribute(op_fgemm_persist_kernel<D, R, K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return launch_pdl(op_fgemm_persist_kernel<D, R, K1>, dim3(std::min(ntiles, nsm)), dim3(F::NT * 32), smem, s, g,
+                      tiles, ntiles, ecls, relidx, m.A1, m.A2, m.A3, m.AP, m.a2stride, m.a3stride, mix, x, Y, ncell);
   }
   return launch_pdl(op_fgemm_kernel<D, R, K1>, dim3(ntiles), dim3(F::NT * 32), F::SMEM, s, g, tiles, ecls, relidx,
                     m.A1, m.A2, m.A3, m.AP, m.a2stride, m.a3stride, mix, x, Y, ncell);
