@@ -141,16 +141,34 @@ def test_P15_dof_counts():
 
 
 # ---------------------------------------------------------------- P4: Tab:3 --------------------------
-@pytest.mark.parametrize("level", [0, 1])
-def test_P4_table3_reproduction(level):
-    """P4: PAPER Tab:3 (P:L711-712, P:L737-738) printed errors, Q5/Q4, k=2, Eq. 5.3, within 2 %."""
-    gold = json.load(open(os.path.join(GOLD, "tab3.json")))
+@pytest.fixture(scope="module")
+def tab3_runs():
+    """The oracle's Tab:3 marches (Q5/Q4, k = 2, Eq. 5.3, 4x4 cells, interval length 1) at tau0 / 2^0..2^3."""
     lam, mu = lame(100.0, 0.35)
     params = dict(rho=1.0, alpha=0.9, c0=0.01, lam=lam, mu=mu, K=[1, 0, 0, 1])
     lev = Level(2, [4, 4], [0, 0], [1, 1], r=5, k=2)
-    res = march_errors(lev, params, manufactured_eq53(params), 0.0, 1.0, 50 * 2 ** level)
+    sol = manufactured_eq53(params)
+    return [march_errors(lev, params, sol, 0.0, 1.0, 50 * 2 ** level) for level in range(4)]
+
+
+@pytest.mark.parametrize("level", [0, 1, 2, 3])
+def test_P4_table3_reproduction(level, tab3_runs):
+    """P4: PAPER Tab:3 (P:L711-714, P:L737-740) printed errors, Q5/Q4, k=2, Eq. 5.3, within 2 %."""
+    gold = json.load(open(os.path.join(GOLD, "tab3.json")))
+    res = tab3_runs[level]
     assert np.allclose(res["L2"], gold["L2"][str(level)], rtol=0.02, atol=0)
     assert np.allclose(res["linf_tn"], gold["linf_tn"][str(level)], rtol=0.02, atol=0)
+
+
+def test_P4_table3_eoc(tab3_runs):
+    """P4: the printed EOC columns of Tab:3 (order 2k+1 = 5 in the time nodes, k+1 = 3 in
+    L2(L2) for grad u and v, the pre-asymptotic pressure rates 4.13 / 4.77 / 4.09) within +-0.1."""
+    gold = json.load(open(os.path.join(GOLD, "tab3.json")))
+    for key, gkey in (("L2", "eoc_L2"), ("linf_tn", "eoc_linf_tn")):
+        e = np.array([r[key] for r in tab3_runs])
+        eoc = np.log2(e[:-1] / e[1:])
+        for lvl in (1, 2, 3):
+            assert np.all(np.abs(eoc[lvl - 1] - np.array(gold[gkey][str(lvl)])) <= 0.1), (key, lvl, eoc[lvl - 1])
 
 
 # ---------------------------------------------------------------- P5: Tab:App1 rates (k = 3) ---------
