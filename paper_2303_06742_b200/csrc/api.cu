@@ -376,7 +376,7 @@ struct LevelData {
   bool exp_fused = false;       // STGMG_EXPAND_FUSED=1: the push-form gather_expand instead
   // unstructured level (SURVEY N3, L-shape): CSR operator / transfers / averaging table above, plus one explicit
   // inverse per vertex patch (K2u, csrc/lshape.cu)
-  double* rtmp = nullptr;       // intermediates of the separable restriction (levels with >= 200k DoFs)
+  double* rtmp = nullptr;       // intermediates of the separable restriction (levels with 200k..16M DoFs)
   bool unstr = false;
   int* pz = nullptr;            // concatenated Z(P)
   long long* pzoff = nullptr;   // start of Z(P) and of y_P
@@ -1431,7 +1431,7 @@ static int build_transfer(stgmg_handle* h, int l) {
     for (int pres = 0; pres < 2; ++pres) {
       Interp1D& T = pres ? F.tt.p[a] : F.tt.q[a];
       if (a >= h->d) {
-        T = Interp1D{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        T = Interp1D{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
         continue;
       }
       const int deg = pres ? h->r - 1 : h->r;
@@ -1446,14 +1446,17 @@ static int build_transfer(stgmg_handle* h, int l) {
       CK(upload(h, &rpc, ih.rp_c));
       CK(upload(h, &cic, ih.ci_c));
       CK(upload(h, &vc, ih.v_c));
-      T = Interp1D{rpf, cif, vf, rpc, cic, vc};
+      T = Interp1D{rpf, cif, vf, rpc, cic, vc, (int)ih.ci_c.size()};
     }
   }
-  // separable restriction on levels with >= 200k DoFs (its intermediates hold < N_l doubles); STGMG_RESTRICT_SEP=0:
-  // off
+  // separable restriction on levels with 200k..16M DoFs (its intermediates hold < N_l doubles);
+  // STGMG_RESTRICT_SEP=0: off
   const char* sep_env = std::getenv("STGMG_RESTRICT_SEP");
   const bool sep_off = sep_env && std::atoi(sep_env) == 0;
-  if (!sep_off && F.g.N >= 200000 && F.g.N < (1LL << 31)) CK(dalloc(h, &F.rtmp, (size_t)F.g.N));
+  // measured (R+P, one B200): cfg2 fine (7.9M) 368 -> 156 us, cfg3 level 3 (441k) 80 -> 31 us, cfg3 fine (3.4M)
+  // 97 -> 81 us, but cfg4 fine (26.6M) 489 -> 542 us (its first pass is latency-bound on the table chain): the gather
+  // form stays on levels above 16M DoFs
+  if (!sep_off && F.g.N >= 200000 && F.g.N < 16000000) CK(dalloc(h, &F.rtmp, (size_t)F.g.N));
   return 0;
 }
 

@@ -37,6 +37,10 @@ __global__ void __launch_bounds__(128) avg_nodal_kernel(LevelGeom g, const doubl
   const int nq = (int)g.nq, np = (int)g.np;
   if (t >= nq + np) return;
   const bool pres = t >= nq;
+  // one (Radau node m, field slot) per grid row: the per-node thread with all 2d K1 slots needed 208 registers
+  // (8 warps per SM, ncu: 12 % of the warp slots active)
+  const int m = blockIdx.y / (2 * D), sl = blockIdx.y % (2 * D);
+  if (pres && sl > 0) return;
   const int node = pres ? t - nq : t;
   int idx[3];
   node_coords<D>(node, pres ? g.pn : g.qn, idx);
@@ -64,7 +68,7 @@ __global__ void __launch_bounds__(128) avg_nodal_kernel(LevelGeom g, const doubl
     }
   }
   // per candidate patch: offset of (m = 0, slot 0) of this node in Y, slot stride nQ, Radau stride blk
-  int off[NPMAX], sq[NPMAX], sb[NPMAX];
+  int off[NPMAX];
   const int vs1 = g.n[0] + 1, vs2 = (g.n[0] + 1) * (g.n[1] + 1);
 #pragma unroll
   for (int i3 = 0; i3 < (D == 3 ? 3 : 1); ++i3)
@@ -86,57 +90,30 @@ __global__ void __launch_bounds__(128) avg_nodal_kernel(LevelGeom g, const doubl
           nQ *= qb;
           nP *= pb;
         }
-        off[s] = ok ? plin * ldy + loc + (pres ? 2 * D * nQ : 0) : -1;
-        sq[s] = nQ;
-        sb[s] = 2 * D * nQ + nP;
+        // Y offset of (m, slot sl, this node) in patch s (int: npatch * ldy < 2^31 on every level)
+        off[s] = ok ? plin * ldy + loc + (pres ? 2 * D * nQ : sl * nQ) + m * (2 * D * nQ + nP) : -1;
       }
   int p = 1;
 #pragma unroll
   for (int a = 0; a < D; ++a) p *= cnt[a];
-  const long long blockN = g.block;
-  const long long node_off = pres ? 2 * g.R + node : (long long)node;
-  const double* Yv[NPMAX];
-#pragma unroll
-  for (int s = 0; s < NPMAX; ++s) Yv[s] = Y + (off[s] >= 0 ? off[s] : 0);   // absent patch: any valid address
-  const int nsl = pres ? 1 : 2 * D;
+  const long long mu = (long long)m * g.block + (pres ? 2 * g.R + node : (long long)sl * g.nq + node);
   // omega / p_mu (reading A17: d + omega * (sum_P y_P) / p_mu); N2(iii) overwrite: the last patch's y, p = 1
   const double wp = overwrite ? omega : omega / (double)p;
   pdl_wait();
-  // loads first (unconditional, so that they issue back to back), then the fixed-order sums
-  constexpr int SLB = D == 3 ? 1 : 2 * D;   // slots loaded per batch (register budget)
+  double v[NPMAX];
 #pragma unroll
-  for (int m = 0; m < K1; ++m) {
+  for (int s = 0; s < NPMAX; ++s) v[s] = __ldg(Y + (off[s] >= 0 ? off[s] : 0));   // absent patch: any valid address
+  const double dold = zero_init ? 0.0 : dvec[mu];
+  double z = 0.0;
+  if (overwrite) {
 #pragma unroll
-    for (int sl0 = 0; sl0 < 2 * D; sl0 += SLB) {
-      if (sl0 >= nsl) break;
-      double v[SLB][NPMAX];
+    for (int s = 0; s < NPMAX; ++s) z = off[s] >= 0 ? v[s] : z;   // last patch (lexicographic) wins
+  } else {
 #pragma unroll
-      for (int j = 0; j < SLB; ++j)
-#pragma unroll
-        for (int s = 0; s < NPMAX; ++s) v[j][s] = __ldg(Yv[s] + m * sb[s] + (sl0 + j) * sq[s]);
-      double dold[SLB];
-#pragma unroll
-      for (int j = 0; j < SLB; ++j) {
-        const long long mu = m * blockN + node_off + (pres ? 0 : (long long)(sl0 + j < nsl ? sl0 + j : 0) * g.nq);
-        dold[j] = zero_init ? 0.0 : dvec[mu];
-      }
-#pragma unroll
-      for (int j = 0; j < SLB; ++j) {
-        if (sl0 + j >= nsl) break;
-        double z = 0.0;
-        if (overwrite) {
-#pragma unroll
-          for (int s = 0; s < NPMAX; ++s) z = off[s] >= 0 ? v[j][s] : z;   // last patch (lexicographic) wins
-        } else {
-#pragma unroll
-          for (int s = 0; s < NPMAX; ++s) z += off[s] >= 0 ? v[j][s] : 0.0;
-        }
-        const long long mu = m * blockN + node_off + (pres ? 0 : (long long)(sl0 + j) * g.nq);
-        const double upd = z * wp;
-        dvec[mu] = zero_init ? upd : dold[j] + upd;
-      }
-    }
+    for (int s = 0; s < NPMAX; ++s) z += off[s] >= 0 ? v[s] : 0.0;
   }
+  const double upd = z * wp;
+  dvec[mu] = zero_init ? upd : dold + upd;
 }
 
 // ------------------------------------------------------------------------------------------------ K1b -------
@@ -678,8 +655,8 @@ static inline unsigned node_blocks(const LevelGeom& g) { return (unsigned)((g.nq
 cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double* Y, int ldy, double omega,
                                  int zero_init, double* dvec, cudaStream_t s, int overwrite) {
   STGMG_DRK(g.d, r, k1,
-            return launch_pdl(avg_nodal_kernel<D_, R_, K_>, dim3(node_blocks(g)), dim3(128), 0, s, g, Y, ldy, omega,
-                              zero_init, dvec, overwrite));
+            return launch_pdl(avg_nodal_kernel<D_, R_, K_>, dim3(node_blocks(g), K_ * 2 * D_), dim3(128), 0, s, g, Y,
+                              ldy, omega, zero_init, dvec, overwrite));
   return cudaErrorNotSupported;
 }
 

@@ -196,6 +196,7 @@ int gauss_jordan_inverse(double* mats, int nmat, int n_max, const int* n_each, i
 struct Interp1D {              // CSR tables of the 1D prolongation for one axis and degree (device)
   const int* rp_f; const int* ci_f; const double* v_f;   // rows = fine nodes
   const int* rp_c; const int* ci_c; const double* v_c;   // rows = coarse nodes (transpose)
+  int nz_c;                                               // nonzeros of the coarse-row table
 };
 struct TransferTables { Interp1D q[3], p[3]; };
 cudaError_t launch_restrict(const LevelGeom& fine, const LevelGeom& coarse, int k1, const TransferTables& t,
