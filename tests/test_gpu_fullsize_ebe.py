@@ -1,11 +1,13 @@
-"""Full-size parity of the whole solver at BASELINE sizes (configs 2 and 3; -m gpu), against the element-by-element
+"""Full-size parity of the whole solver at BASELINE sizes (configs 2, 3 and the bench workload 4; -m gpu), against the
+element-by-element
 oracle (oracle/ebe.py: the assembled oracle's definitions without a global matrix, pinned against it in
 tests/test_oracle_ebe.py).  North-star tolerances, on the bench's launch configuration (single GPU, default kernels):
   * one V-cycle:     ||d_gpu - d_orc|| / ||d_orc|| <= 1e-8
   * FGMRES solve:    iterations +-1, ||x_gpu - x_orc|| / ||x_orc|| <= 1e-8,
                      ||r_gpu - r_orc|| / ||b|| <= 1e-10 with each side's own r = b - A x
 Right-hand sides: the configs' slab-1 F_1 (cfg3: manufactured loads + interpolated initial data, assembled by the
-oracle; the device's own F_1 is compared with it too; cfg2: the seed-2 U[-1,1) load, reading A21).
+oracle; cfg4: the beam traction (reading A23) from a zero state; the device's own F_1 is compared with both; cfg2: the
+seed-2 U[-1,1) load, reading A21).
 The oracle runs on the host's cores (minutes); one module-scoped oracle solve per config.
 """
 import numpy as np
@@ -21,7 +23,7 @@ def rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-@pytest.fixture(scope="module", params=[3, 2], ids=["cfg3", "cfg2"])
+@pytest.fixture(scope="module", params=[3, 2, 4], ids=["cfg3", "cfg2", "cfg4"])
 def case(request):
     import torch
     from threadpoolctl import threadpool_limits
@@ -43,17 +45,19 @@ def case(request):
 
 
 def test_fullsize_rhs(case):
-    """The device's slab-1 right-hand side (on-device loads + K8) equals the oracle's (cfg3)."""
+    """The device's slab-1 right-hand side (on-device loads + K8) equals the oracle's (cfg3, cfg4)."""
     import torch
     cfg, s, b = case["cfg"], case["s"], case["b"]
-    if cfg["load"] != "manufactured":
+    if cfg["load"] not in ("manufactured", "beam"):
         pytest.skip("random load: the vector is an input")
-    from paper_2303_06742_b200.stgmg import LOAD_MANUFACTURED
+    from paper_2303_06742_b200.stgmg import LOAD_MANUFACTURED, LOAD_BEAM_TRACTION
+    kind = LOAD_MANUFACTURED if cfg["load"] == "manufactured" else LOAD_BEAM_TRACTION
     N = s.size()
     X0 = torch.zeros(N, dtype=torch.float64, device="cuda")
     L, F = torch.zeros_like(X0), torch.zeros_like(X0)
-    s.initial_state(LOAD_MANUFACTURED, 0.0, X0)
-    s.slab_load(LOAD_MANUFACTURED, 0.0, L)
+    if kind == LOAD_MANUFACTURED:
+        s.initial_state(LOAD_MANUFACTURED, 0.0, X0)
+    s.slab_load(kind, 0.0, L)
     s.slab_rhs(L, X0, F)
     torch.cuda.synchronize()
     assert rel(to_np(F), b) < 1e-12, rel(to_np(F), b)
