@@ -129,7 +129,8 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
  * host at setup from element integrals; every patch has its own explicit inverse (K4 on the device).  Vector layout per
  * Radau node: V_0..V_2, U_0..U_2 on the active Q_r nodes (lexicographic over the (2 r 2^ref + 1)^2 (r 2^ref + 1) node
  * grid, x fastest), then P (dim P_{r-1} monomials per active cell, cells lexicographic).  All other entry points
- * accept the handle except stgmg_energy / stgmg_level_work / stgmg_kernel_work / stgmg_time_kernel (ENOTSUP);
+ * accept the handle except stgmg_energy / stgmg_level_work (ENOTSUP); stgmg_time_kernel takes kinds 0 (K2u, the
+ * per-patch inverse GEMV), 1, 2, 3, 6 and stgmg_kernel_work kind 0 (8 sum C_P^2 + 16 sum C_P bytes, 2 sum C_P^2 flops);
  * stgmg_slab_load takes STGMG_LOAD_LSHAPE_TRACTION, stgmg_goal_quantities face 1 (Gamma_m, Eq:DefGQ).
  * Errors: EINVAL, ENOTSUP (r, k, nranks > 1, smoother / formulation variants), ENOMEM, ECUDA, ESINGULAR, ECOVER. */
 int stgmg_setup_lshape(int ref_fine, int levels, const stgmg_order* order, const stgmg_params* params,

@@ -2780,8 +2780,17 @@ int stgmg_level_work(const stgmg_handle* h, int level, double* k2_flops, double*
 }
 
 int stgmg_kernel_work(const stgmg_handle* h, int kind, int level, double* flops, double* bytes) {
-  if (h && h->lshape) { set_error("not available for the L-shape"); return STGMG_ENOTSUP; }
   if (!h || level < 0 || level >= h->L || !flops || !bytes) { set_error("bad argument"); return STGMG_EINVAL; }
+  if (h->lshape) {   // K2u: one explicit inverse per patch, streamed once per sweep (HBM-bound GEMV)
+    if (kind != 0 || !h->lev[level].unstr) { set_error("L-shape: kind 0 on levels >= 1 only"); return STGMG_ENOTSUP; }
+    std::vector<int> cps(h->lev[level].npatch);
+    CKE(cudaMemcpy(cps.data(), h->lev[level].pcp, sizeof(int) * cps.size(), cudaMemcpyDeviceToHost));
+    double s2 = 0.0, s1 = 0.0;
+    for (int c : cps) { s2 += (double)c * c; s1 += c; }
+    *flops = 2.0 * s2;
+    *bytes = 8.0 * s2 + 16.0 * s1;   // the inverses (C_P^2 each) + gather r, write y
+    return 0;
+  }
   const LevelData& Lv = h->lev[level];
   const double N = (double)Lv.g.N;
   double sumcp = 0.0, fl2 = 0.0, invb = 0.0;
@@ -2817,7 +2826,10 @@ int stgmg_kernel_work(const stgmg_handle* h, int kind, int level, double* flops,
 }
 
 int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* avg_ms) {
-  if (h && h->lshape) { set_error("not available for the L-shape"); return STGMG_ENOTSUP; }
+  if (h && h->lshape && kind != 0 && kind != 1 && kind != 2 && kind != 3 && kind != 6) {
+    set_error("L-shape: kinds 0 (K2u), 1, 2, 3, 6 only");
+    return STGMG_ENOTSUP;
+  }
   if (!h || level < 0 || level >= h->L || reps < 1 || !avg_ms) { set_error("bad argument"); return STGMG_EINVAL; }
   if ((kind == 0 || kind == 2 || kind == 6 || kind == 7) && level < 1) {
     set_error("smoother kernels need level >= 1");
@@ -2831,7 +2843,9 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
   LevelData& Lv = h->lev[level];
   auto one = [&]() -> int {
     if (kind == 0) {
-      if (Lv.dense)
+      if (Lv.unstr)
+        CKE(launch_patch_gemv((int)Lv.npatch, Lv.pmax, Lv.pz, Lv.pzoff, Lv.pcp, Lv.pinv, Lv.plda, Lv.r, Lv.Y, h->s));
+      else if (Lv.dense)
         CKE(launch_patch_gemm_dense(Lv.g, Lv.k2var, Lv.cls_dev, Lv.tiles_dev, Lv.ntiles, Lv.inv_dev, Lv.lda, Lv.Rexp,
                                     Lv.Y, Lv.ldy, h->s));
       else

@@ -57,9 +57,16 @@ for n in range(nsl):
     X.copy_(x)
     goal.append(s.goal_quantities(X, 1))
 g = np.array(goal)
+# the dominant kernel: K2u (per-patch inverse GEMV) on the fine level, HBM-bound (MEASURED_PEAKS copy bandwidth)
+lf = s.levels - 1
+t2 = s.time_kernel(0, lf, reps=20)
+fl2, by2 = s.kernel_work(0, lf)
+tv = s.time_kernel(3, lf, reps=5)
+k2u = dict(avg_launch_ms=t2, bytes=by2, hbm_gbs=by2 / (t2 * 1e-3) / 1e9, hbm_frac=by2 / (t2 * 1e-3) / 1e9 / 6550.7,
+           vcycle_ms=tv)
 print(json.dumps(dict(ref=a.ref, coarse=a.coarse, k=a.k, r=a.r, E=a.E, hF=a.hf, dofs=N, tol=a.tol, tol_mode="abs" if a.abs else "rel",
                       slabs=nsl, avg_its=float(np.mean(its)), min_its=int(min(its)), max_its=int(max(its)),
                       converged=int(sum(conv)), bu=[float(g[:, 0].min()), float(g[:, 0].max())],
                       bp=[float(g[:, 1].min()), float(g[:, 1].max())], s_per_slab=float(np.median(secs)),
-                      setup_s=setup)))
+                      setup_s=setup, k2u=k2u)))
 s.close()
