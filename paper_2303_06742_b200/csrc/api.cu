@@ -949,8 +949,23 @@ std::vector<TileDesc> stgmg::balanced_tiles(const std::vector<int>& cp, const st
   return out;
 }
 
+// STGMG_SETUP_TIMES=1: sub-phase marks inside a setup phase (device synchronised), "what: ms since the last mark".
+struct SetupMarks {
+  bool on = std::getenv("STGMG_SETUP_TIMES") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, int level) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "stgmg setup:   %-28s level %2d  %9.1f ms\n", what, level,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 static int build_patches(stgmg_handle* h, int l) {
   NvtxRange nv("stgmg setup: patch classes + inverses (K4)");
+  SetupMarks sm;
   LevelData& Lv = h->lev[l];
   const LevelGeom& g = Lv.g;
   const int d = h->d, r = h->r, k1 = h->k1;
@@ -1165,6 +1180,7 @@ static int build_patches(stgmg_handle* h, int l) {
       CK(upload(h, &C.items_dev, items));
     }
   }
+  sm.mark("classes, tiles, tables", l);
   CK(dalloc(h, &Lv.Y, (size_t)Lv.npatch * Lv.ldy));
   double* inv_rm = nullptr;   // row-major inverses (setup scratch); K2 reads the chunk-major copy Lv.inv_dev
   CKE(cudaMalloc(&inv_rm, sizeof(double) * (size_t)ncls * Lv.lda * Lv.lda));
@@ -1185,6 +1201,7 @@ static int build_patches(stgmg_handle* h, int l) {
     if (Ycb) { CKE(cudaStreamSynchronize(h->s)); CKE(cudaFree(Ycb)); }
     if (rc) return rc;
   }
+  sm.mark("mini-level dense operator", l);
   int* cps_dev = nullptr;
   long long* offs_dev = nullptr;
   int* mdofs_dev = nullptr;
@@ -1199,10 +1216,12 @@ static int build_patches(stgmg_handle* h, int l) {
   CK(dalloc(h, &colk, (size_t)ncls * Lv.lda));
   CK(dalloc(h, &scale, (size_t)ncls * Lv.lda));
   CKE(cudaMemsetAsync(status, 0, sizeof(int) * ncls, h->s));
+  sm.mark("extraction", l);
   if (gauss_jordan_inverse(inv_rm, ncls, Lv.maxcp, cps_dev, Lv.lda, perm, colk, scale, status, h->s)) {
     set_error("gauss_jordan_inverse launch failed");
     return STGMG_ECUDA;
   }
+  sm.mark("Gauss-Jordan", l);
   CKE(launch_chunk_swizzle(inv_rm, Lv.inv_dev, ncls, Lv.lda, h->s));
   std::vector<int> st(ncls);
   CKE(cudaMemcpyAsync(st.data(), status, sizeof(int) * ncls, cudaMemcpyDeviceToHost, h->s));
