@@ -35,7 +35,7 @@ __device__ __forceinline__ void fg_dmma(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <int D, int R, int K1>
+template <int D, int R, int K1, int NCC = 32>
 struct FG {
   static constexpr int NQ = ipow(R + 1, D), NP = ipow(R, D);
   static constexpr int NQK = (NQ + 3) / 4 * 4;     // XE rows per Q slot (K padding, zero rows)
@@ -44,7 +44,7 @@ struct FG {
   static constexpr int NPM = (NP + 7) / 8 * 8;     // G3 / GP rows
   static constexpr int RA = 2 * D * NQK + NPK;     // XE rows per Radau node: V_0..V_{d-1}, U_0..U_{d-1}, P
   static constexpr int XR = K1 * RA;
-  static constexpr int NC = 32;                    // cells per CTA
+  static constexpr int NC = NCC;                   // cells per CTA tile
   static constexpr int XS = NC + 4;                // XE row stride (doubles)
   static constexpr int KS1 = NQK / 4, KS2 = (D * NQK + NPK) / 4, KSP = NPK / 4;
   static constexpr int KSV = D * NQK / 4;          // G3 k-steps over V (then KSP over P)
@@ -82,10 +82,9 @@ struct FgMix {   // temporal constants of the epilogue (T[b][a], theta_b)
 };
 
 // Column bases of a tile (threads < NC): lowest Q_r / Q_{r-1} node of each cell and its lexicographic index.
-template <int D, int R>
+template <int D, int R, int NC = 32>
 __device__ __forceinline__ void fg_bases(const LevelGeom& g, const PatchClass& pc, int4 td, long long* qb,
                                          long long* pb, long long* pl) {
-  constexpr int NC = 32;
   if (threadIdx.x < NC) {   // cell of column j: box of the type (vlo = cell + 1 per axis), x fastest
     const int j = threadIdx.x;
     long long q = 0, p = 0, v = 0, vs = 1;
@@ -120,12 +119,12 @@ __device__ __forceinline__ int fg_row_elem(int row) {
 }
 
 // The G1 / G2 / G3 GEMMs of one tile from its gathered inputs XE and the epilogue (mixing with T, theta; stores).
-template <int D, int R, int K1, int HN>
+template <int D, int R, int K1, int HN, int NC = 32>
 __device__ __forceinline__ void fg_compute(const double* XE, const long long* pl, int4 td, const double* __restrict__ A1,
                                            const double* __restrict__ A2, const double* __restrict__ A3,
                                            const double* __restrict__ AP, long long a2stride, long long a3stride,
                                            const FgMix& mix, double* __restrict__ Y, long long ncell) {
-  using F = FG<D, R, K1>;
+  using F = FG<D, R, K1, NC>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kl = lane & 3, nl = lane >> 2;
   const double* Bl = XE + kl * F::XS + nl;   // this lane's B element: row k0 + kl, column n0 + nl
@@ -292,22 +291,29 @@ __device__ __forceinline__ void fg_cp_async8(double* dst, const double* src) {
 }
 
 template <int D, int R, int K1>
-__global__ void __launch_bounds__(FG<D, R, K1>::NT * 32, 1) op_fgemm_persist_kernel(
+__global__ void __launch_bounds__(FG<D, R, K1, 16>::NT * 32, 2) op_fgemm_persist_kernel(
     LevelGeom g, const int4* __restrict__ tiles, int ntiles, const PatchClass* __restrict__ ecls,
     const int* __restrict__ relidx, const double* __restrict__ A1, const double* __restrict__ A2,
     const double* __restrict__ A3, const double* __restrict__ AP, long long a2stride, long long a3stride, FgMix mix,
     const double* __restrict__ x, double* __restrict__ Y, long long ncell) {
-  using F = FG<D, R, K1>;
+  // half tiles of 16 cells (two per 32-cell tile), two CTAs per SM, each double-buffered
+  using F = FG<D, R, K1, 16>;
   extern __shared__ double smem[];
   double* XEb[2] = {smem, smem + (size_t)F::XR * F::XS};
   long long* meta = reinterpret_cast<long long*>(smem + 2 * (size_t)F::XR * F::XS);   // [buf][qb | pb | pl][NC]
   pdl_trigger();
   pdl_wait();
-  auto stage = [&](int t, int b) {   // bases, then the asynchronous gather of tile t into buffer b
-    const int4 td = tiles[t];
+  const int nv = 2 * ntiles;
+  auto half = [&](int v) {
+    const int4 t = tiles[v >> 1];
+    const int h = v & 1;
+    return make_int4(t.x, t.y + 16 * h, max(0, min(16, t.z - 16 * h)), 0);
+  };
+  auto stage = [&](int v, int b) {   // bases, then the asynchronous gather of half tile v into buffer b
+    const int4 td = half(v);
     const PatchClass& pc = ecls[td.x];
     long long* qb = meta + (size_t)b * 3 * F::NC;
-    fg_bases<D, R>(g, pc, td, qb, qb + F::NC, qb + 2 * F::NC);
+    fg_bases<D, R, 16>(g, pc, td, qb, qb + F::NC, qb + 2 * F::NC);
     __syncthreads();
     const int* rel = relidx + pc.rel_off;
     double* XE = XEb[b];
@@ -324,19 +330,21 @@ __global__ void __launch_bounds__(FG<D, R, K1>::NT * 32, 1) op_fgemm_persist_ker
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  int t = blockIdx.x, b = 0;
-  if (t < ntiles) stage(t, 0);
-  for (; t < ntiles; t += gridDim.x, b ^= 1) {
-    const int tn = t + gridDim.x;
-    if (tn < ntiles) {
-      stage(tn, b ^ 1);
+  int v = blockIdx.x, b = 0;
+  if (v < nv) stage(v, 0);
+  for (; v < nv; v += gridDim.x, b ^= 1) {
+    const int vn = v + gridDim.x;
+    if (vn < nv) {
+      stage(vn, b ^ 1);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
-    fg_compute<D, R, K1, 4>(XEb[b], meta + (size_t)b * 3 * F::NC + 2 * F::NC, tiles[t], A1, A2, A3, AP, a2stride,
-                            a3stride, mix, Y, ncell);
+    const int4 td = half(v);
+    if (td.z > 0)
+      fg_compute<D, R, K1, 2, 16>(XEb[b], meta + (size_t)b * 3 * F::NC + 2 * F::NC, td, A1, A2, A3, AP, a2stride,
+                                  a3stride, mix, Y, ncell);
     __syncthreads();   // buffer b is refilled by the stage of the next iteration
   }
 }
@@ -434,7 +442,8 @@ static cudaError_t launch_fg(const LevelGeom& g, const int4* tiles, int ntiles, 
   }
   static const bool persist = std::getenv("STGMG_K1_PERSIST") && std::atoi(std::getenv("STGMG_K1_PERSIST")) != 0;
   if (persist) {
-    const size_t smem = 2 * sizeof(double) * (size_t)F::XR * F::XS + 2 * 3 * sizeof(long long) * F::NC;
+    using FH = FG<D, R, K1, 16>;
+    const size_t smem = 2 * sizeof(double) * (size_t)FH::XR * FH::XS + 2 * 3 * sizeof(long long) * FH::NC;
     static PerDeviceOnce attrp;
     attrp.run([smem] {
       cudaFuncSetAttribute(op_fgemm_persist_kernel<D, R, K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -442,7 +451,7 @@ static cudaError_t launch_fg(const LevelGeom& g, const int4* tiles, int ntiles, 
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return launch_pdl(op_fgemm_persist_kernel<D, R, K1>, dim3(std::min(ntiles, nsm)), dim3(F::NT * 32), smem, s, g,
+    return launch_pdl(op_fgemm_persist_kernel<D, R, K1>, dim3(std::min(2 * ntiles, 2 * nsm)), dim3(F::NT * 32), smem, s, g,
                       tiles, ntiles, ecls, relidx, m.A1, m.A2, m.A3, m.AP, m.a2stride, m.a3stride, mix, x, Y, ncell);
   }
   return launch_pdl(op_fgemm_kernel<D, R, K1>, dim3(ntiles), dim3(F::NT * 32), F::SMEM, s, g, tiles, ecls, relidx,
