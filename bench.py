@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of the decomposition")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "shm"],
+                    help="N > 1: the library's NCCL transport (default) or its process-separated shared-memory "
+                         "transport with a gloo process group (exercises the N-rank flow on one GPU; ranks then share "
+                         "the device and the numbers are not a scaling measurement)")
     ap.add_argument("--smoother", default="additive", choices=["additive", "colored", "element", "overwrite"],
                     help="additive = Alg. 1 (paper, default); colored = multiplicative colour-ordered Vanka (N2(i)); "
                          "element = element-wise Vanka (N2(ii)); overwrite = Alg. 1 without averaging (N2(iii))")
@@ -77,7 +81,9 @@ def workload_config(cfg, args, ws, dd):
             "rtol": cfg["rtol"], "load": load_label(cfg), "smoother": args.smoother,
             "march": "slab n of step i: t_n = (warmup + i) tau, F_n = L_n + J X_{n-1}",
             "l2": "flushed between timed steps (256 MB write, untimed); inputs > L2 (212 MB per vector at cfg4)",
-            "parallelism": ("x-slab decomposition over %d GPUs (NCCL halo exchange)" % ws) if dd else
+            "parallelism": ("x-slab decomposition over %d ranks (%s halo exchange)"
+                            % (ws, "NCCL" if getattr(args, "transport", "nccl") == "nccl"
+                               else "host shared-memory, ranks may share a GPU")) if dd else
                            ("%d replicas" % ws if ws > 1 else "single GPU")}
 
 
@@ -266,14 +272,21 @@ def run_ours(args):
     import torch
     ws, rank, lrank = dist_env()
     dd = ws > 1 and not args.replicas
+    shm = ws > 1 and args.transport == "shm"
+    gpu = (lrank % max(1, torch.cuda.device_count())) if shm else lrank
     if ws > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")   # lets the driver count the communicator's ranks
-        torch.cuda.set_device(lrank)
+        torch.cuda.set_device(gpu)
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
-    dev = torch.device("cuda", lrank if ws > 1 else 0)
+        if shm:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+    dev = torch.device("cuda", gpu if ws > 1 else 0)
+    red_dev = "cpu" if shm else dev   # gloo reduces host tensors
     from paper_2303_06742_b200 import Solver
     from paper_2303_06742_b200.stgmg import (nccl_unique_id, nccl_comm_create, nccl_comm_destroy, partition_plan,
+                                             shm_comm_create, shm_comm_destroy, COMM_NCCL, COMM_SHM,
                                              LOAD_MANUFACTURED, LOAD_BEAM_TRACTION)
     from paper_2303_06742_b200.partition import window_index
     cfg = config(args.config)
@@ -285,10 +298,18 @@ def run_ours(args):
     if dd:
         # the library's own NCCL communicator: rank 0 draws the id, torch.distributed broadcasts it (stgmg.h).
         # Any failure here raises: a decomposition that cannot be set up ends the run with a non-zero exit.
-        uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
-        torch.distributed.broadcast(uid, 0)
-        comm = nccl_comm_create(bytes(uid.cpu().tolist()), ws, rank)
-        s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm, smoother=smoother)
+        if shm:   # segment name drawn by rank 0, broadcast over the gloo group
+            import uuid
+            name = list(("stgmg_bench_" + uuid.uuid4().hex[:16]).encode()) if rank == 0 else [0] * 28
+            nt = torch.tensor(name, dtype=torch.uint8)
+            torch.distributed.broadcast(nt, 0)
+            comm = shm_comm_create(bytes(nt.tolist()).decode(), ws, rank)
+        else:
+            uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
+            torch.distributed.broadcast(uid, 0)
+            comm = nccl_comm_create(bytes(uid.cpu().tolist()), ws, rank)
+        s = Solver(cfg, stream=stream, rank=rank, nranks=ws, comm=comm, smoother=smoother,
+                   comm_kind=COMM_SHM if shm else COMM_NCCL)
     else:
         s = Solver(cfg, stream=stream, smoother=smoother)
     t_setup = time.perf_counter() - t_setup
@@ -363,8 +384,8 @@ def run_ours(args):
     t_e = time.perf_counter() - t_e0
     e_end = nvml_energy_mj(dev.index)
     clk = clocks.stop()
-    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
-    its_t = torch.tensor([float(its)], dtype=torch.float64, device=dev)
+    t_local = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    its_t = torch.tensor([float(its)], dtype=torch.float64, device=red_dev)
     energy_j = (e_end - e_start) * 1e-3 if (e_start is not None and e_end is not None) else None
     if ws > 1:
         import torch.distributed as dist
@@ -372,7 +393,7 @@ def run_ours(args):
         if not dd:                     # replicas: every rank solved its own copy
             dist.all_reduce(its_t, op=dist.ReduceOp.SUM)
         if energy_j is not None:       # board energy of every participating GPU
-            et = torch.tensor([energy_j], dtype=torch.float64, device=dev)
+            et = torch.tensor([energy_j], dtype=torch.float64, device=red_dev)
             dist.all_reduce(et, op=dist.ReduceOp.SUM)
             energy_j = float(et.item())
     t_max_s = float(t_local.item()) * 1e-3
@@ -388,7 +409,7 @@ def run_ours(args):
     fold_lv = s.fold_level()
     vc_flops = sum(2 * 4 * s.level_work(l)["k2_flops"] for l in range(max(1, fold_lv + 1), cfg["levels"]))
     fold_flops = 2.0 * float(s.size(fold_lv)) ** 2 if fold_lv else 0.0
-    job_flops = torch.tensor([vc_flops * its], dtype=torch.float64, device=dev)
+    job_flops = torch.tensor([vc_flops * its], dtype=torch.float64, device=red_dev)
     if ws > 1:
         torch.distributed.all_reduce(job_flops, op=torch.distributed.ReduceOp.SUM)
     solve_tflops = float(job_flops.item()) / t_max_s / 1e12
@@ -437,7 +458,7 @@ def run_ours(args):
     e2e_dt = time.perf_counter() - t0
     e2e_val = Nglob * e2e_its / e2e_dt / 1e6
     if ws > 1:
-        tt = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
+        tt = torch.tensor([e2e_dt], dtype=torch.float64, device=red_dev)
         import torch.distributed as dist
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_val = Nglob * e2e_its * (1 if dd else ws) / float(tt.item()) / 1e6
@@ -490,7 +511,7 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     s.close()
     if comm is not None:
-        nccl_comm_destroy(comm)
+        (shm_comm_destroy if shm else nccl_comm_destroy)(comm)
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()

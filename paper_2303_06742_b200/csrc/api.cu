@@ -2893,7 +2893,9 @@ int stgmg_time_kernel(stgmg_handle* h, int kind, int level, int reps, double* av
     return 0;
   };
   CK(one());   // warm-up
-  if (kind == 3) {   // a graph launch cannot be captured: time back-to-back graph launches
+  // a graph launch cannot be captured, and a host-synchronising transport (loopback / shared memory) cannot be
+  // captured either: time back-to-back launches instead
+  if (kind == 3 || !h->graphable) {
     CKE(cudaEventRecord(h->e0, h->s));
     for (int i = 0; i < reps; ++i) CK(one());
     CKE(cudaEventRecord(h->e1, h->s));

@@ -396,6 +396,10 @@ struct ShmTransport : Transport {
   ShmComm* c;
   explicit ShmTransport(ShmComm* comm) : c(comm) { rank = comm->rank; nranks = comm->nranks; }
   bool graph_capturable() const override { return false; }
+  int fail(const char* what) {
+    set_error(std::string("shm transport: ") + what + ": " + cudaGetErrorString(cudaGetLastError()));
+    return -3;
+  }
   int check(long long n) {
     if (n > c->cap) { set_error("shm transport: message of " + std::to_string(n) + " doubles exceeds the slot"); return -4; }
     return 0;
@@ -403,20 +407,25 @@ struct ShmTransport : Transport {
   int halo(const double* sl, long long nsl, const double* sr, long long nsr, double* rl, long long nrl, double* rr,
            long long nrr, cudaStream_t s) override {
     if (check(nsl) || check(nsr) || check(nrl) || check(nrr)) return -4;
-    if (nsl && cudaMemcpyAsync(c->slot(rank, 0), sl, sizeof(double) * nsl, cudaMemcpyDeviceToHost, s)) return -3;
-    if (nsr && cudaMemcpyAsync(c->slot(rank, 1), sr, sizeof(double) * nsr, cudaMemcpyDeviceToHost, s)) return -3;
-    if (cudaStreamSynchronize(s) != cudaSuccess) { set_error("shm transport: stream sync"); return -3; }
+    if (nsl && cudaMemcpyAsync(c->slot(rank, 0), sl, sizeof(double) * nsl, cudaMemcpyDeviceToHost, s))
+      return fail("halo copy out");
+    if (nsr && cudaMemcpyAsync(c->slot(rank, 1), sr, sizeof(double) * nsr, cudaMemcpyDeviceToHost, s))
+      return fail("halo copy out");
+    if (cudaStreamSynchronize(s) != cudaSuccess) return fail("stream sync");
     c->barrier();
-    if (nrl && cudaMemcpyAsync(rl, c->slot(rank - 1, 1), sizeof(double) * nrl, cudaMemcpyHostToDevice, s)) return -3;
-    if (nrr && cudaMemcpyAsync(rr, c->slot(rank + 1, 0), sizeof(double) * nrr, cudaMemcpyHostToDevice, s)) return -3;
-    if (cudaStreamSynchronize(s) != cudaSuccess) return -3;
+    if (nrl && cudaMemcpyAsync(rl, c->slot(rank - 1, 1), sizeof(double) * nrl, cudaMemcpyHostToDevice, s))
+      return fail("halo copy in");
+    if (nrr && cudaMemcpyAsync(rr, c->slot(rank + 1, 0), sizeof(double) * nrr, cudaMemcpyHostToDevice, s))
+      return fail("halo copy in");
+    if (cudaStreamSynchronize(s) != cudaSuccess) return fail("stream sync");
     c->barrier();   // the neighbours' slots may be reused only after both reads
     return 0;
   }
   int allreduce_sum(double* v, int n, cudaStream_t s) override {
     if (n > 16) { set_error("shm allreduce: n > 16"); return -1; }
     double loc[16];
-    if (cudaMemcpyAsync(loc, v, sizeof(double) * n, cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s)) return -3;
+    if (cudaMemcpyAsync(loc, v, sizeof(double) * n, cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+      return fail("allreduce copy out");
     std::memcpy(c->red(rank), loc, sizeof(double) * n);
     c->barrier();
     for (int i = 0; i < n; ++i) {
@@ -425,7 +434,8 @@ struct ShmTransport : Transport {
       loc[i] = t;
     }
     c->barrier();
-    if (cudaMemcpyAsync(v, loc, sizeof(double) * n, cudaMemcpyHostToDevice, s) || cudaStreamSynchronize(s)) return -3;
+    if (cudaMemcpyAsync(v, loc, sizeof(double) * n, cudaMemcpyHostToDevice, s) || cudaStreamSynchronize(s))
+      return fail("allreduce copy in");
     return 0;
   }
   int allgather(const double* send, long long n, double* recv, cudaStream_t s) override {

@@ -41,3 +41,19 @@ def test_reference_arm_line():
     d = run("--impl", "reference", "--config", "0", "--steps", "1", "--warmup", "0")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_two_rank_shm_bench():
+    """The N > 1 flow of bench.py (barriers, max-over-ranks timing, decomposition, halo exchange inside every V-cycle
+    and FGMRES dot) on the one GPU of the test box: two ranks over torchrun share cuda:0 through the host
+    shared-memory transport (STGMG_COMM_SHM).  Config 1 (64 x 64 cells, split 32 + 32)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29631", os.path.join(ROOT, "bench.py"), "--gpus", "2", "--transport", "shm",
+           "--config", "1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert "shared-memory" in d["config"]["parallelism"]
