@@ -338,6 +338,8 @@ struct LevelData {
   bool fg = false;
   int4* fg_tiles = nullptr;
   int fg_ntiles = 0;
+  int4* sf_tiles = nullptr;        // K1 tiles of the volume-only cell types on the sum-factorised kernel (op_sf3.cu)
+  int sf_ntiles = 0;
   FgemmDev fgm;
   // x-slab domain decomposition; a replicated level has part = false, w0 = 0, gnx = n[0]
   bool part = false, has_left = false, has_right = false;
@@ -446,7 +448,10 @@ struct stgmg_handle {
   unsigned char* mask = nullptr;   // owned fine-level DoFs (Krylov inner products)
   bool graphable = true;
   bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; large 2D elements)
-  bool fg_on = true;               // K1 element GEMM in the factored form (STGMG_K1_FGEMM=0: the full element matrix)
+  int fg_on = 1;                   // K1 element GEMM in the factored form (STGMG_K1_FGEMM=0: the full element matrix;
+                                   // 2: on every element-route level regardless of size, for tests)
+  int sf_on = 1;                   // 3D Q2: volume-only cell types by sum factorisation on levels with >= 128k cells
+                                   // (STGMG_K1_SF=0: all factored; 2: every factored level, for tests)
   int nsm = 148;                   // SMs of the device (tile balancing)
   // the 3D L-shaped benchmark (stgmg_setup_lshape); levels are unstructured (LevelData::unstr)
   bool lshape = false;
@@ -569,10 +574,15 @@ static int apply_geom(stgmg_handle* h, const LevelGeom& g, const OpConsts* cdev,
 static int element_results(stgmg_handle* h, LevelData& Lv, const double* x, int* ldpm) {
   const int ne = (int)elem_dofs(h);
   *ldpm = Lv.fg ? 0 : ne;
-  if (Lv.fg)
-    CKE(launch_op_fgemm(Lv.g, h->r, h->k1, Lv.fg_tiles, Lv.fg_ntiles, Lv.ecls_dev, Lv.erelidx_dev, Lv.fgm, h->c, x,
-                        h->Ycell, h->s));
-  else
+  if (Lv.fg) {
+    if (Lv.sf_ntiles) {
+      CKE(launch_op_sf3(Lv.g, h->r, h->k1, Lv.sf_tiles, Lv.sf_ntiles, Lv.ecls_dev, h->c, x, h->Ycell, h->s));
+      if (Lv.fg_ntiles) h->launches += 1;
+    }
+    if (Lv.fg_ntiles)
+      CKE(launch_op_fgemm(Lv.g, h->r, h->k1, Lv.fg_tiles, Lv.fg_ntiles, Lv.ecls_dev, Lv.erelidx_dev, Lv.fgm, h->c, x,
+                          h->Ycell, h->s));
+  } else
     CKE(launch_patch_gemm(Lv.g, h->r, Lv.ek2var, Lv.ecls_dev, Lv.etiles_dev, Lv.entiles, Lv.erelidx_dev, Lv.E_dev,
                           Lv.elda, x, h->Ycell, ne, h->s));
   return 0;
@@ -1356,22 +1366,35 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
   // factored form (op_fgemm.cu) on the levels where it wins (measured: cfg4/cfg3 3D levels with >= 4096 cells, the
   // 2D Q3 levels with >= 16384 cells; on smaller levels one CTA per 32 cells leaves the GPU idle)
   const long long ncl = Lv.ncell_global ? Lv.ncell_global : cell_count(g);
-  if (gemm && h->fg_on && h->c.ds == 0.0 && ncl >= (d == 3 ? 4096 : 16384)) {
+  if (gemm && h->fg_on && h->c.ds == 0.0 && (h->fg_on == 2 || ncl >= (d == 3 ? 4096 : 16384))) {
     std::vector<double> Eh((size_t)nt * Lv.elda * Lv.elda);
     CKE(cudaMemcpy(Eh.data(), E_rm, sizeof(double) * Eh.size(), cudaMemcpyDeviceToHost));
     FgemmData fd;
     if (fgemm_build_any(d, r, k1, Eh, nt, Lv.elda, h->c, fd) == 0) {
-      std::vector<int4> tl;
+      std::vector<int4> tl, ts;
       const int nc = fgemm_cells_per_tile();
-      for (int t = 0; t < nt; ++t)
+      for (int t = 0; t < nt; ++t) {
+        // volume-only type: every domain face its box touches is Neumann for u and p (no Nitsche terms)
+        // (measured on B200: faster than the factored GEMMs at cfg4's fine level, 262k cells, slower on 4k-33k cell
+        // levels)
+        bool vol = sf3_supported(d, r, k1) && (h->sf_on == 2 || (h->sf_on == 1 && ncl >= 131072));
+        for (int a = 0; a < d; ++a) {
+          const int c0 = Lv.ecls[t].vlo[a] - 1, c1 = c0 + Lv.ecls[t].cnt[a] - 1;
+          if (c0 == 0 && (g.bcu[2 * a] == STGMG_BC_DIRICHLET || g.bcp[2 * a] == STGMG_BC_DIRICHLET)) vol = false;
+          if (c1 == g.n[a] - 1 && (g.bcu[2 * a + 1] == STGMG_BC_DIRICHLET || g.bcp[2 * a + 1] == STGMG_BC_DIRICHLET))
+            vol = false;
+        }
         for (int c0 = 0; c0 < Lv.ecls[t].ncols; c0 += nc)
-          tl.push_back(make_int4(t, c0, std::min(nc, Lv.ecls[t].ncols - c0), 0));
+          (vol ? ts : tl).push_back(make_int4(t, c0, std::min(nc, Lv.ecls[t].ncols - c0), 0));
+      }
+      if (!ts.empty()) CK(upload(h, &Lv.sf_tiles, ts));
+      Lv.sf_ntiles = (int)ts.size();
       double *a1 = nullptr, *a2 = nullptr, *a3 = nullptr, *ap = nullptr;
       CK(upload(h, &a1, fd.A1));
       CK(upload(h, &a2, fd.A2));
       CK(upload(h, &a3, fd.A3));
       CK(upload(h, &ap, fd.AP));
-      CK(upload(h, &Lv.fg_tiles, tl));
+      if (!tl.empty()) CK(upload(h, &Lv.fg_tiles, tl));
       Lv.fg_ntiles = (int)tl.size();
       Lv.fgm.A1 = a1;
       Lv.fgm.A2 = a2;
@@ -2059,7 +2082,8 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     // 2D: the register kernel on small elements (cfg1, 80 DoFs: K1 9.5 vs 13.8 us), the element GEMM on large ones
     // (cfg2, r = 3, k = 2, 219 DoFs: fine-level K1 357 -> 303 us, V-cycle 27.0 -> 26.0 ms)
     h->op_gemm = d == 3 || elem_dofs(h.get()) >= 128;
-    if (const char* ev = std::getenv("STGMG_K1_FGEMM")) h->fg_on = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("STGMG_K1_FGEMM")) h->fg_on = std::atoi(ev);
+    if (const char* ev = std::getenv("STGMG_K1_SF")) h->sf_on = std::atoi(ev);
     if (d == 2)
       if (const char* ev = std::getenv("STGMG_OP2D_GEMM")) h->op_gemm = std::atoi(ev) != 0;
     if (h->op_gemm) {

@@ -256,5 +256,9 @@ int fgemm_cells_per_tile();
 cudaError_t launch_op_fgemm(const LevelGeom& g, int r, int k1, const int4* tiles, int ntiles, const PatchClass* ecls,
                             const int* relidx, const FgemmDev& m, const OpConsts& c, const double* x, double* Y,
                             cudaStream_t s);   // Y[element DoF][cell] (cell-fastest)
+// K1 on the volume-only cell types by sum factorisation (csrc/op_sf3.cu; 3D Q2), same tiles / Y layout as op_fgemm.
+bool sf3_supported(int d, int r, int k1);
+cudaError_t launch_op_sf3(const LevelGeom& g, int r, int k1, const int4* tiles, int ntiles, const PatchClass* ecls,
+                          const OpConsts& c, const double* x, double* Y, cudaStream_t s);
 
 }  // namespace stgmg
