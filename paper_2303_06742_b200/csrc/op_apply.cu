@@ -92,7 +92,25 @@ __global__ void __launch_bounds__(128) op_apply_kernel(LevelGeom g, const OpCons
       return off + 2 * g.R + node;
     }
   };
-  for (int i = lane; i < T::NE; i += 32) xe[i] = __ldg(x + gidx(i / T::NE1, i % T::NE1));
+  bool nz = false;
+  for (int i = lane; i < T::NE; i += 32) {
+    xe[i] = __ldg(x + gidx(i / T::NE1, i % T::NE1));
+    nz = nz || xe[i] != 0.0;
+  }
+  // A cell whose inputs are all zero contributes exactly zero (the operator is linear): skip its work.  At setup the
+  // kernel runs on batches of unit vectors (element and mini-level matrices, coarse operator), where all but the <= 2^d
+  // cells around the unit vector's node are such cells.
+  if (!__any_sync(0xffffffffu, nz)) {
+    if (Yc) {
+      long long plin = 0, vs = 1;
+      for (int a = 0; a < D; ++a) {
+        plin += (long long)(cell[a] + 1) * vs;
+        vs *= g.n[a] + 1;
+      }
+      for (int i = lane; i < T::NE; i += 32) Yc[plin * T::NE + i] = 0.0;
+    }
+    return;
+  }
   __syncwarp();
 
   const double hinv[3] = {1.0 / g.h[0], D > 1 ? 1.0 / g.h[1] : 0.0, D > 2 ? 1.0 / g.h[2] : 0.0};

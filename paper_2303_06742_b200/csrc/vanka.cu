@@ -1156,18 +1156,27 @@ __global__ void gj_colperm(double* mats, int lda, const int* n_each, const int* 
 // NB: the unblocked rank-1 updates stream every matrix once per pivot (3D levels: 125 x 1568^2 doubles, 1554 times).
 constexpr int GJB_NB = 32, GJB_BM = 64, GJB_BN = 64;
 
-__global__ void __launch_bounds__(512) gjb_panel(double* mats, int lda, const int* n_each, int k0, int* perm, int* pi,
-                                                 double* colk, int* status) {
+// One CTA per matrix.  Per step: argmax of the pivot column (block reduction), row swap on the panel columns, then ONE
+// pass over the n x nbe panel that applies the whole elementary step (column k := e_k, pivot row scaled by 1 / pivot,
+// rank-1 elimination of every other row) from the pivot column and the scaled pivot row held in shared memory, with
+// GJB_UNR independent loads in flight per thread (the L2-resident panel made every step latency-bound).
+constexpr int GJB_PT = 1024, GJB_UNR = 8;
+
+__global__ void __launch_bounds__(GJB_PT) gjb_panel(double* mats, int lda, const int* n_each, int k0, int* perm,
+                                                    int* pi, double* colk, int* status) {
   const int c = blockIdx.x;
   const int n = n_each[c];
   if (k0 >= n || status[c] != 0) return;
   double* A = mats + (long long)c * lda * lda;
   int* pm = perm + (long long)c * lda;
   int* pc = pi + (long long)c * lda;
-  double* ck = colk + (long long)c * lda;
+  extern __shared__ double gsm[];
+  double* ck = gsm;                  // pivot column (lda)
+  double* pr = ck + lda;             // scaled pivot row on the panel columns (GJB_NB)
+  __shared__ double bv[GJB_PT / 32];
+  __shared__ int bi[GJB_PT / 32];
   const int nbe = min(GJB_NB, n - k0);
-  __shared__ double bv[512];
-  __shared__ int bi[512];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = k0 + threadIdx.x; i < n; i += blockDim.x) pc[i] = i;
   __syncthreads();
   for (int j = 0; j < nbe; ++j) {
@@ -1176,22 +1185,28 @@ __global__ void __launch_bounds__(512) gjb_panel(double* mats, int lda, const in
     int bidx = n;
     for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
       const double v = fabs(A[(long long)i * lda + k]);
-      if (v > best || (v == best && i < bidx)) { best = v; bidx = i; }
+      if (v > best) { best = v; bidx = i; }   // rows ascending per thread: ties keep the lowest row
     }
-    bv[threadIdx.x] = best;
-    bi[threadIdx.x] = bidx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (v2 > best || (v2 == best && i2 < bidx)) { best = v2; bidx = i2; }
+    }
+    if (lane == 0) { bv[warp] = best; bi[warp] = bidx; }
     __syncthreads();
-    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-      if (threadIdx.x < st) {
-        const double v2 = bv[threadIdx.x + st];
-        const int i2 = bi[threadIdx.x + st];
-        if (v2 > bv[threadIdx.x] || (v2 == bv[threadIdx.x] && i2 < bi[threadIdx.x])) {
-          bv[threadIdx.x] = v2;
-          bi[threadIdx.x] = i2;
-        }
+    if (warp == 0) {
+      best = lane < GJB_PT / 32 ? bv[lane] : -1.0;
+      bidx = lane < GJB_PT / 32 ? bi[lane] : n;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (v2 > best || (v2 == best && i2 < bidx)) { best = v2; bidx = i2; }
       }
-      __syncthreads();
+      if (lane == 0) { bv[0] = best; bi[0] = bidx; }
     }
+    __syncthreads();
     const int p = bi[0];
     if (bv[0] <= 0.0) {
       if (threadIdx.x == 0) status[c] = k + 1;
@@ -1211,19 +1226,32 @@ __global__ void __launch_bounds__(512) gjb_panel(double* mats, int lda, const in
     }
     if (threadIdx.x == 0) pm[k] = p;
     __syncthreads();
-    const double piv = A[(long long)k * lda + k];
     for (int i = threadIdx.x; i < n; i += blockDim.x) ck[i] = A[(long long)i * lda + k];
+    if (threadIdx.x < nbe) {
+      const double ip = 1.0 / A[(long long)k * lda + k];
+      pr[threadIdx.x] = (threadIdx.x == j ? 1.0 : A[(long long)k * lda + k0 + threadIdx.x]) * ip;
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) A[(long long)i * lda + k] = (i == k) ? 1.0 : 0.0;
-    __syncthreads();
-    const double ip = 1.0 / piv;
-    for (int q = threadIdx.x; q < nbe; q += blockDim.x) A[(long long)k * lda + k0 + q] *= ip;
-    __syncthreads();
-    for (long long e = threadIdx.x; e < (long long)n * nbe; e += blockDim.x) {
-      const int i = (int)(e / nbe), q = (int)(e % nbe);
-      if (i == k) continue;
-      const double f = ck[i];
-      if (f != 0.0) A[(long long)i * lda + k0 + q] = fma(-f, A[(long long)k * lda + k0 + q], A[(long long)i * lda + k0 + q]);
+    const long long tot = (long long)n * nbe;
+    for (long long e0 = threadIdx.x; e0 < tot; e0 += (long long)GJB_UNR * blockDim.x) {
+      double old[GJB_UNR];
+#pragma unroll
+      for (int u = 0; u < GJB_UNR; ++u) {
+        const long long e = e0 + (long long)u * blockDim.x;
+        old[u] = 0.0;
+        if (e < tot) {
+          const int i = (int)(e / nbe), q = (int)(e % nbe);
+          old[u] = q == j ? (i == k ? 1.0 : 0.0) : A[(long long)i * lda + k0 + q];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GJB_UNR; ++u) {
+        const long long e = e0 + (long long)u * blockDim.x;
+        if (e < tot) {
+          const int i = (int)(e / nbe), q = (int)(e % nbe);
+          A[(long long)i * lda + k0 + q] = i == k ? pr[q] : fma(-ck[i], pr[q], old[u]);
+        }
+      }
     }
     __syncthreads();
   }
@@ -1309,22 +1337,24 @@ int gauss_jordan_inverse(double* mats, int nmat, int n_max, const int* n_each, i
   static const bool unblocked = std::getenv("STGMG_GJ_UNBLOCKED") != nullptr;
   double* buf = nullptr;
   int* pi = nullptr;
-  if (!unblocked && n_max >= 128 &&
-      cudaMalloc(&buf, sizeof(double) * (size_t)nmat * lda * lda) == cudaSuccess &&
-      cudaMalloc(&pi, sizeof(int) * (size_t)nmat * lda) == cudaSuccess) {
+  const size_t psmem = sizeof(double) * ((size_t)lda + GJB_NB);   // pivot column + scaled pivot row
+  if (!unblocked && n_max >= 128 && psmem <= 200 * 1024 &&
+      cudaMallocAsync(&buf, sizeof(double) * (size_t)nmat * lda * lda, s) == cudaSuccess &&
+      cudaMallocAsync(&pi, sizeof(int) * (size_t)nmat * lda, s) == cudaSuccess) {
+    static PerDeviceOnce attr;
+    attr.run([] { cudaFuncSetAttribute(gjb_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
     double *cur = mats, *nxt = buf;
     const dim3 tg((lda + GJB_BN - 1) / GJB_BN, (lda + GJB_BM - 1) / GJB_BM, nmat);
     for (int k0 = 0; k0 < n_max; k0 += GJB_NB) {
-      gjb_panel<<<nmat, 512, 0, s>>>(cur, lda, n_each, k0, perm, pi, colk, status);
+      gjb_panel<<<nmat, GJB_PT, psmem, s>>>(cur, lda, n_each, k0, perm, pi, colk, status);
       gjb_trailing<<<tg, 256, 0, s>>>(cur, nxt, lda, n_each, k0, pi, status);
       std::swap(cur, nxt);
     }
     if (cur != mats) cudaMemcpyAsync(mats, cur, sizeof(double) * (size_t)nmat * lda * lda, cudaMemcpyDeviceToDevice, s);
-    cudaStreamSynchronize(s);
-    cudaFree(buf);
-    cudaFree(pi);
+    cudaFreeAsync(buf, s);
+    cudaFreeAsync(pi, s);
   } else {
-    if (buf) cudaFree(buf);
+    if (buf) cudaFreeAsync(buf, s);
     cudaGetLastError();
     for (int k = 0; k < n_max; ++k) {
       gj_pivot<<<nmat, 1024, 0, s>>>(mats, lda, n_each, k, perm, colk, status);
