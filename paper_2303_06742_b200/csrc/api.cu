@@ -448,6 +448,7 @@ struct stgmg_handle {
   unsigned char* mask = nullptr;   // owned fine-level DoFs (Krylov inner products)
   bool graphable = true;
   bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; large 2D elements)
+  GjScratch gj;                    // blocked Gauss–Jordan scratch, reused by every setup inverse, freed after setup
   int fg_on = 1;                   // K1 element GEMM in the factored form (STGMG_K1_FGEMM=0: the full element matrix;
                                    // 2: on every element-route level regardless of size, for tests)
   int sf_on = 1;                   // 3D Q2: volume-only cell types by sum factorisation on levels with >= 128k cells
@@ -476,6 +477,8 @@ struct stgmg_handle {
     for (auto g : vg_step)
       if (g) cudaGraphExecDestroy(g);
     for (void* p : allocs) cudaFree(p);
+    if (gj.buf) cudaFree(gj.buf);
+    if (gj.pi) cudaFree(gj.pi);
     delete tr;
     if (pinned) cudaFreeHost(pinned);
     if (e0) cudaEventDestroy(e0);
@@ -1227,7 +1230,7 @@ static int build_patches(stgmg_handle* h, int l) {
   CK(dalloc(h, &scale, (size_t)ncls * Lv.lda));
   CKE(cudaMemsetAsync(status, 0, sizeof(int) * ncls, h->s));
   sm.mark("extraction", l);
-  if (gauss_jordan_inverse(inv_rm, ncls, Lv.maxcp, cps_dev, Lv.lda, perm, colk, scale, status, h->s)) {
+  if (gauss_jordan_inverse(inv_rm, ncls, Lv.maxcp, cps_dev, Lv.lda, perm, colk, scale, status, h->s, &h->gj)) {
     set_error("gauss_jordan_inverse launch failed");
     return STGMG_ECUDA;
   }
@@ -1450,7 +1453,7 @@ static int build_coarse(stgmg_handle* h) {
   CK(dalloc(h, &colk, (size_t)N));
   CK(dalloc(h, &scale, (size_t)N));
   CKE(cudaMemsetAsync(status, 0, sizeof(int), h->s));
-  if (gauss_jordan_inverse(h->A0inv, 1, (int)N, cps_dev, (int)N, perm, colk, scale, status, h->s)) {
+  if (gauss_jordan_inverse(h->A0inv, 1, (int)N, cps_dev, (int)N, perm, colk, scale, status, h->s, &h->gj)) {
     set_error("coarse gauss_jordan_inverse launch failed");
     return STGMG_ECUDA;
   }
@@ -1798,6 +1801,12 @@ const char* stgmg_last_error(void) { return g_last_error.c_str(); }
 // Setup steps shared by every hierarchy: Krylov / reduction workspace, events, the folded coarse sub-cycle, the
 // V-cycle graph.
 static int finish_setup(stgmg_handle* h) {
+  if (h->gj.buf || h->gj.pi) {   // setup scratch of the class inverses
+    CKE(cudaStreamSynchronize(h->s));
+    if (h->gj.buf) CKE(cudaFree(h->gj.buf));
+    if (h->gj.pi) CKE(cudaFree(h->gj.pi));
+    h->gj = GjScratch();
+  }
   const long long Nf = h->lev[h->L - 1].g.N;
   CK(dalloc(h, &h->w, (size_t)Nf));
   CK(dalloc(h, &h->rv, (size_t)Nf));
@@ -1877,6 +1886,7 @@ static int check_params(int d, const stgmg_params* params) {
 int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, const stgmg_params* params,
                 stgmg_handle** out) {
   NvtxRange nv("stgmg_setup");
+  SetupMarks pm;   // STGMG_SETUP_TIMES: the allocation / constant phases before build_cells
   if (!mesh || !order || !params || !out) { set_error("null argument"); return STGMG_EINVAL; }
   const int d = mesh->dim, r = order->r, k = order->k;
   if ((d != 2 && d != 3) || r < 2 || r > 3 || k < 0 || k > 3 || levels < 1 || levels > 16) {
@@ -1988,6 +1998,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     CKE(cudaMemset(Lv.d, 0, sizeof(double) * N));
     CKE(cudaMemset(Lv.r, 0, sizeof(double) * N));
   }
+  pm.mark("handle, level vectors", -1);
   if (nranks > 1 && !h->lev[levels - 1].part) {
     set_error("multi-GPU: the fine level must split into an even number >= 4 of cells per rank along x "
               "(cells[0] % (2 nranks) == 0)");
@@ -2090,6 +2101,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
       long long nv = 1;
       for (int a = 0; a < 3; ++a) nv *= h->lev[levels - 1].g.n[a] + 1;
       CK(dalloc(h.get(), &h->Ycell, (size_t)(nv * elem_dofs(h.get()))));
+      pm.mark("constants, element buffer", -1);
       for (int l = 0; l < levels; ++l) CK(timed("build_cells", l, [&] { return build_cells(h.get(), l, true); }));
     }
   }
@@ -2142,7 +2154,7 @@ static int invert_batch(stgmg_handle* h, double* mats, int n, int nmax, const in
   CKE(cudaMalloc(&colk, sizeof(double) * (size_t)n * lda));
   CKE(cudaMalloc(&scale, sizeof(double) * (size_t)n * lda));
   CKE(cudaMemsetAsync(status, 0, sizeof(int) * (size_t)n, h->s));
-  if (gauss_jordan_inverse(mats, n, nmax, n_each_dev, lda, perm, colk, scale, status, h->s)) {
+  if (gauss_jordan_inverse(mats, n, nmax, n_each_dev, lda, perm, colk, scale, status, h->s, &h->gj)) {
     set_error(std::string(what) + ": gauss_jordan_inverse launch failed");
     return STGMG_ECUDA;
   }

@@ -190,8 +190,13 @@ cudaError_t launch_vanka_average(const LevelGeom& g, int r, int k1, const double
 cudaError_t launch_extract_patch(const LevelGeom& mini, int r, int k1, const double* Adense, long long ldA,
                                  const int* vrep, int nclass, const int* cps, const long long* rel_offs,
                                  const int* relidx_mini, double* inv, int lda, cudaStream_t s);
+struct GjScratch {                     // device scratch of the blocked Gauss–Jordan (ping-pong copy, permutations);
+  double* buf = nullptr;               // owned by the caller, grown on demand, reused across calls
+  int* pi = nullptr;
+  size_t buf_bytes = 0, pi_bytes = 0;
+};
 int gauss_jordan_inverse(double* mats, int nmat, int n_max, const int* n_each, int lda, int* perm, double* colk,
-                         double* scale, int* status, cudaStream_t s);
+                         double* scale, int* status, cudaStream_t s, GjScratch* scratch = nullptr);
 // K5: restriction / prolongation with per-axis sparse 1D interpolation tables.
 struct Interp1D {              // CSR tables of the 1D prolongation for one axis and degree (device)
   const int* rp_f; const int* ci_f; const double* v_f;   // rows = fine nodes

@@ -1154,7 +1154,10 @@ __global__ void gj_colperm(double* mats, int lda, const int* n_each, const int* 
 // (the in-place panel column k0 + j ends as the product of the steps' elementary matrices applied to e_{k0+j}), a
 // rank-NB update done by gjb_trailing with DMMA out of place (ping-pong buffers).  Memory traffic per pivot drops by
 // NB: the unblocked rank-1 updates stream every matrix once per pivot (3D levels: 125 x 1568^2 doubles, 1554 times).
-constexpr int GJB_NB = 32, GJB_BM = 64, GJB_BN = 64;
+constexpr int GJB_NB = 64, GJB_BM = 64, GJB_BN = 64;
+// shared row strides = 4 (mod 16) doubles: the m8n8k4 fragments of a half warp hit 16 distinct 8-byte bank pairs
+constexpr int GJB_WS = GJB_NB + 4, GJB_TS = GJB_BN + 4;
+constexpr size_t GJB_TSMEM = sizeof(double) * (GJB_BM * GJB_WS + GJB_NB * GJB_TS);
 
 // One CTA per matrix.  Per step: argmax of the pivot column (block reduction), row swap on the panel columns, then ONE
 // pass over the n x nbe panel that applies the whole elementary step (column k := e_k, pivot row scaled by 1 / pivot,
@@ -1232,24 +1235,23 @@ __global__ void __launch_bounds__(GJB_PT) gjb_panel(double* mats, int lda, const
       pr[threadIdx.x] = (threadIdx.x == j ? 1.0 : A[(long long)k * lda + k0 + threadIdx.x]) * ip;
     }
     __syncthreads();
-    const long long tot = (long long)n * nbe;
-    for (long long e0 = threadIdx.x; e0 < tot; e0 += (long long)GJB_UNR * blockDim.x) {
-      double old[GJB_UNR];
+    // thread = (row group, panel columns lane, lane + 32): rows i = rg, rg + GJB_PT / 32, ... (32-bit index math)
+    const int rg = warp;
+    for (int q = lane; q < nbe; q += 32) {
+      const double prq = pr[q];
+      constexpr int RS = GJB_PT / 32;
+      for (int i0 = rg; i0 < n; i0 += GJB_UNR * RS) {
+        double old[GJB_UNR];
 #pragma unroll
-      for (int u = 0; u < GJB_UNR; ++u) {
-        const long long e = e0 + (long long)u * blockDim.x;
-        old[u] = 0.0;
-        if (e < tot) {
-          const int i = (int)(e / nbe), q = (int)(e % nbe);
-          old[u] = q == j ? (i == k ? 1.0 : 0.0) : A[(long long)i * lda + k0 + q];
+        for (int u = 0; u < GJB_UNR; ++u) {
+          const int i = i0 + u * RS;
+          old[u] = 0.0;
+          if (i < n) old[u] = q == j ? (i == k ? 1.0 : 0.0) : A[(size_t)i * lda + k0 + q];
         }
-      }
 #pragma unroll
-      for (int u = 0; u < GJB_UNR; ++u) {
-        const long long e = e0 + (long long)u * blockDim.x;
-        if (e < tot) {
-          const int i = (int)(e / nbe), q = (int)(e % nbe);
-          A[(long long)i * lda + k0 + q] = i == k ? pr[q] : fma(-ck[i], pr[q], old[u]);
+        for (int u = 0; u < GJB_UNR; ++u) {
+          const int i = i0 + u * RS;
+          if (i < n) A[(size_t)i * lda + k0 + q] = i == k ? prq : fma(-ck[i], prq, old[u]);
         }
       }
     }
@@ -1259,6 +1261,8 @@ __global__ void __launch_bounds__(GJB_PT) gjb_panel(double* mats, int lda, const
 
 // out[i][c] = in[i][c] on the panel columns, padding and rows / columns >= n; otherwise
 // in[pi(i)][c] + sum_j W[i][j] in[pi(k0 + j)][c] with W[i][j] = in[i][k0 + j] - delta_{i, k0+j} (DMMA m8n8k4).
+// One CTA per 64 x 64 output tile; 8 warps in a 4 x 2 grid, warp tile 16 x 32 (2 x 4 m8n8k4 DMMA per k-step; a
+// 64 x 128 tile with 32 x 32 warp tiles, 2 CTAs per SM, measured 18 % slower).
 __global__ void __launch_bounds__(256) gjb_trailing(const double* __restrict__ in, double* __restrict__ out, int lda,
                                                     const int* n_each, int k0, const int* __restrict__ pi,
                                                     const int* status) {
@@ -1270,8 +1274,9 @@ __global__ void __launch_bounds__(256) gjb_trailing(const double* __restrict__ i
   const bool active = k0 < n && status[c] == 0;
   const int nbe = active ? min(GJB_NB, n - k0) : 0;
   const int* pc = pi + (long long)c * lda;
-  __shared__ double Ws[GJB_BM][GJB_NB + 1];
-  __shared__ double Ts[GJB_NB][GJB_BN + 4];
+  extern __shared__ double sraw[];
+  double (*Ws)[GJB_WS] = reinterpret_cast<double (*)[GJB_WS]>(sraw);
+  double (*Ts)[GJB_TS] = reinterpret_cast<double (*)[GJB_TS]>(sraw + GJB_BM * GJB_WS);
   __shared__ int prow[GJB_BM];
   for (int e = threadIdx.x; e < GJB_BM * GJB_NB; e += blockDim.x) {
     const int i = e / GJB_NB, j = e % GJB_NB, row = r0 + i;
@@ -1297,8 +1302,9 @@ __global__ void __launch_bounds__(256) gjb_trailing(const double* __restrict__ i
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll
-  for (int ks = 0; ks < GJB_NB / 4; ++ks) {
+  const int ksn = (nbe + 3) / 4;
+#pragma unroll 4
+  for (int ks = 0; ks < ksn; ++ks) {
     double af[2], bf[4];
 #pragma unroll
     for (int a = 0; a < 2; ++a) af[a] = Ws[wm + 8 * a + (lane >> 2)][4 * ks + (lane & 3)];
@@ -1332,30 +1338,49 @@ __global__ void __launch_bounds__(256) gjb_trailing(const double* __restrict__ i
 // negative CUDA error; status[c] != 0 marks a singular matrix (checked by the caller after a sync).  Matrices of
 // >= 128 rows take the blocked form (STGMG_GJ_UNBLOCKED=1: always the rank-1 form).
 int gauss_jordan_inverse(double* mats, int nmat, int n_max, const int* n_each, int lda, int* perm, double* colk,
-                         double* scale, int* status, cudaStream_t s) {
+                         double* scale, int* status, cudaStream_t s, GjScratch* scr) {
   gj_equilibrate<<<nmat, 256, 0, s>>>(mats, lda, n_each, scale, 1, status);
   static const bool unblocked = std::getenv("STGMG_GJ_UNBLOCKED") != nullptr;
-  double* buf = nullptr;
-  int* pi = nullptr;
   const size_t psmem = sizeof(double) * ((size_t)lda + GJB_NB);   // pivot column + scaled pivot row
-  if (!unblocked && n_max >= 128 && psmem <= 200 * 1024 &&
-      cudaMallocAsync(&buf, sizeof(double) * (size_t)nmat * lda * lda, s) == cudaSuccess &&
-      cudaMallocAsync(&pi, sizeof(int) * (size_t)nmat * lda, s) == cudaSuccess) {
+  const size_t need_buf = sizeof(double) * (size_t)nmat * lda * lda, need_pi = sizeof(int) * (size_t)nmat * lda;
+  GjScratch local;
+  GjScratch* sc = scr ? scr : &local;
+  bool blocked = !unblocked && n_max >= 128 && psmem <= 200 * 1024;
+  if (blocked && (sc->buf_bytes < need_buf || sc->pi_bytes < need_pi)) {   // grow the caller's scratch
+    if (sc->buf) cudaFree(sc->buf);
+    if (sc->pi) cudaFree(sc->pi);
+    sc->buf = nullptr;
+    sc->pi = nullptr;
+    sc->buf_bytes = sc->pi_bytes = 0;
+    if (cudaMalloc(&sc->buf, need_buf) == cudaSuccess && cudaMalloc(&sc->pi, need_pi) == cudaSuccess) {
+      sc->buf_bytes = need_buf;
+      sc->pi_bytes = need_pi;
+    } else {
+      cudaGetLastError();
+      blocked = false;
+    }
+  }
+  if (blocked) {
     static PerDeviceOnce attr;
-    attr.run([] { cudaFuncSetAttribute(gjb_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
-    double *cur = mats, *nxt = buf;
+    attr.run([] {
+      cudaFuncSetAttribute(gjb_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(gjb_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GJB_TSMEM);
+    });
+    double *cur = mats, *nxt = sc->buf;
+    int* pi = sc->pi;
     const dim3 tg((lda + GJB_BN - 1) / GJB_BN, (lda + GJB_BM - 1) / GJB_BM, nmat);
     for (int k0 = 0; k0 < n_max; k0 += GJB_NB) {
       gjb_panel<<<nmat, GJB_PT, psmem, s>>>(cur, lda, n_each, k0, perm, pi, colk, status);
-      gjb_trailing<<<tg, 256, 0, s>>>(cur, nxt, lda, n_each, k0, pi, status);
+      gjb_trailing<<<tg, 256, GJB_TSMEM, s>>>(cur, nxt, lda, n_each, k0, pi, status);
       std::swap(cur, nxt);
     }
     if (cur != mats) cudaMemcpyAsync(mats, cur, sizeof(double) * (size_t)nmat * lda * lda, cudaMemcpyDeviceToDevice, s);
-    cudaFreeAsync(buf, s);
-    cudaFreeAsync(pi, s);
+    if (sc == &local) {
+      cudaStreamSynchronize(s);
+      cudaFree(local.buf);
+      cudaFree(local.pi);
+    }
   } else {
-    if (buf) cudaFreeAsync(buf, s);
-    cudaGetLastError();
     for (int k = 0; k < n_max; ++k) {
       gj_pivot<<<nmat, 1024, 0, s>>>(mats, lda, n_each, k, perm, colk, status);
       gj_elim<<<dim3((n_max + 7) / 8, nmat), 256, 0, s>>>(mats, lda, n_each, k, colk, status);
