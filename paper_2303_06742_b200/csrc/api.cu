@@ -438,6 +438,7 @@ struct stgmg_handle {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   OpConsts* c_dev = nullptr;    // operator constants (device copy, read by the 2D cell kernel)
   OpConsts* cj_dev = nullptr;   // slab-RHS variant: T'_ba = chi_b(-1) delta_{a,k}, theta = 0 (K8)
+  OpConsts cj;                  // host copy (the sum-factorised K8 takes its constants by value)
   LoadConsts* lc_dev = nullptr; // on-device load assembly / initial data
   OpConsts* ce_dev = nullptr;   // discrete energy (N1, P7): [0] T = 0, theta_k = 1 ; [1] T_kk = 1, theta = 0
   double* Yc = nullptr;         // element results of the 2D cell kernel (largest level)
@@ -2044,6 +2045,7 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
     CK(dalloc(h.get(), &h->cj_dev, 1));
     CKE(cudaMemcpy(h->c_dev, &h->c, sizeof(OpConsts), cudaMemcpyHostToDevice));
     CKE(cudaMemcpy(h->cj_dev, &cj, sizeof(OpConsts), cudaMemcpyHostToDevice));
+    h->cj = cj;
     {   // energy constants: ce[0] picks theta_k (A_gamma U in the chi rows), ce[1] picks T_kk (mass rows)
       OpConsts ce[2] = {h->c, h->c};
       for (int b = 0; b < kMaxK1; ++b) {
@@ -2468,6 +2470,17 @@ int stgmg_slab_rhs(stgmg_handle* h, const double* load, const double* x_prev, do
   if (h->lshape) {   // F_n = L_n + J X_{n-1} with the assembled coupling (one SpMV)
     CKE(launch_csr_spmv((int)g.N, h->J_lpr, h->J_rp, h->J_ci, h->J_v, x_prev, load, rhs, 1.0, 1.0, h->s));
     h->launches = 1;
+    return sync_if_own(h);
+  }
+  LevelData& F = h->lev[h->L - 1];
+  if (F.fg && F.sf_ntiles && h->c.ds == 0.0) {
+    // 3D fine level with the sum-factorised K1: J X_{n-1} has theta = 0, so every term of the operator but the mass
+    // terms vanishes (the Nitsche face terms carry theta_b too) and the volume-only kernel is exact on EVERY cell
+    // type; element results into Ycell, one gather adds the load
+    CKE(launch_op_sf3(g, h->r, h->k1, F.sf_tiles, F.sf_ntiles, F.ecls_dev, h->cj, x_prev, h->Ycell, h->s));
+    if (F.fg_ntiles) CKE(launch_op_sf3(g, h->r, h->k1, F.fg_tiles, F.fg_ntiles, F.ecls_dev, h->cj, x_prev, h->Ycell, h->s));
+    CKE(launch_op_gather(g, h->r, h->k1, h->Ycell, load, rhs, 1.0, 1.0, 1, 0, 0, h->s, 0));
+    h->launches = F.fg_ntiles ? 3 : 2;
     return sync_if_own(h);
   }
   CK(apply_geom(h, g, h->cj_dev, x_prev, rhs, load, 1.0, 1.0));

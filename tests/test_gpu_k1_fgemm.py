@@ -78,3 +78,24 @@ def test_sumfact_solve_matches_oracle(i):
     assert abs(st["iterations"] - info["iterations"]) <= 1
     assert np.linalg.norm(to_np(x) - xo) <= 1e-8 * np.linalg.norm(xo)
     s.close()
+
+
+@pytest.mark.parametrize("i", [3, 4])
+def test_sumfact_slab_rhs_equals_warp_kernel(i):
+    """K8 F_n = L_n + J X_{n-1}: theta = 0 leaves only mass terms, so the sum-factorised kernel runs on
+    every cell type of the fine level; against the warp-per-cell kernel of the full element route (1e-13)."""
+    import torch
+    cfg = small_config(i)
+    s0, s2 = _solver(cfg, "0"), _solver(cfg, "2", "2")
+    n = s0.size()
+    xp = to_gpu(random_vector(n, 31))
+    load = to_gpu(random_vector(n, 32))
+    outs = []
+    for s in (s0, s2):
+        rhs = torch.zeros(n, dtype=torch.float64, device="cuda")
+        s.slab_rhs(load, xp, rhs)
+        outs.append(to_np(rhs))
+    torch.cuda.synchronize()
+    assert np.linalg.norm(outs[1] - outs[0]) <= 1e-13 * np.linalg.norm(outs[0])
+    for s in (s0, s2):
+        s.close()
