@@ -2581,7 +2581,10 @@ static int enqueue_arnoldi_step(stgmg_handle* h, int j, int m, bool cond, cudaGr
     CKE(cudaMemcpyAsync(zj, F.d, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->s));
     return arnoldi_tail(h, j, m, true, next);
   }
-  if (h->vgraph && h->step_graphs && h->nranks == 1) {
+  // per-step graphs whenever the V-cycle itself is captured: single GPU, or a graph-capturable transport (NCCL: the
+  // halo send/recv, the all-reduce of the MGS dots and the all-gather of the agglomeration are captured stream work);
+  // the host-synchronising loopback / shared-memory transports never get here (no V-cycle graph)
+  if (h->vgraph && h->step_graphs) {
     if (h->vg_step_m != m) {   // H's leading dimension is m + 1: graphs of another restart length are stale
       for (auto& g : h->vg_step)
         if (g) {
