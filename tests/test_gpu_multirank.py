@@ -19,7 +19,10 @@ from paper_2303_06742_b200.partition import window_index, scatter_owned
 pytestmark = pytest.mark.gpu
 
 CASES = [("cfg1s_2ranks", 1, 2), ("cfg2s_2ranks", 2, 2), ("cfg3s_2ranks", 3, 2), ("cfg4s_2ranks", 4, 2),
-         ("cfg4s_4ranks", 4, 4)]
+         ("cfg4s_4ranks", 4, 4), ("cfg4s_2ranks_sumfact", 4, 2)]
+# "_sumfact": the factored element GEMMs and the sum-factorised K1 (csrc/op_sf3.cu) forced onto every element-route
+# level of the windows and of the 1-GPU reference (they run only on levels >= 128k cells by default)
+SUMFACT_ENV = {"STGMG_K1_FGEMM": "2", "STGMG_K1_SF": "2"}
 
 
 def run_ranks(nranks, fn):
@@ -45,7 +48,11 @@ def run_ranks(nranks, fn):
 def ranks(request):
     import torch
     from paper_2303_06742_b200.stgmg import Solver, loopback_hub, loopback_hub_destroy, partition_plan, COMM_LOOPBACK
-    _, ci, P = request.param
+    name, ci, P = request.param
+    import os
+    saved = {k: os.environ.get(k) for k in SUMFACT_ENV}
+    if name.endswith("_sumfact"):
+        os.environ.update(SUMFACT_ENV)
     cfg = small_config(ci)
     if ci == 4:
         cfg = dict(cfg, cells=(32, 4, 4), hi=(4.0, 1.0, 1.0))
@@ -58,6 +65,11 @@ def ranks(request):
 
     solvers = run_ranks(P, make)
     single = Solver(cfg)
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
     fine = cfg["levels"] - 1
     maps = [window_index(cfg, fine, partition_plan(cfg, fine, q, P)) for q in range(P)]
     for q in range(P):
