@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(128) avg_nodal_kernel(LevelGeom g, const doubl
   pdl_wait();
   double v[NPMAX];
 #pragma unroll
-  for (int s = 0; s < NPMAX; ++s) v[s] = __ldg(Y + (off[s] >= 0 ? off[s] : 0));   // absent patch: any valid address
+  for (int s = 0; s < NPMAX; ++s) v[s] = off[s] >= 0 ? __ldg(Y + off[s]) : 0.0;   // absent patch: predicated off
   const double dold = zero_init ? 0.0 : dvec[mu];
   double z = 0.0;
   if (overwrite) {
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(128) gather_nodal_kernel(LevelGeom g, const do
     for (int sl = 0; sl < 2 * D; ++sl) {
       const long long eadd = (long long)(m * NE1 + (sl < nsl ? sl : 0) * NQE) * estride;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) v[sl][c] = __ldg(Yv[c] + eadd);
+      for (int c = 0; c < NC; ++c) v[sl][c] = off[c] >= 0 ? __ldg(Yv[c] + eadd) : 0.0;   // predicated: no request
     }
 #pragma unroll
     for (int sl = 0; sl < 2 * D; ++sl) {
