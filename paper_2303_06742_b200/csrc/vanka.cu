@@ -1263,7 +1263,12 @@ __global__ void __launch_bounds__(GJB_PT) gjb_panel(double* mats, int lda, const
 // in[pi(i)][c] + sum_j W[i][j] in[pi(k0 + j)][c] with W[i][j] = in[i][k0 + j] - delta_{i, k0+j} (DMMA m8n8k4).
 // One CTA per 64 x 64 output tile; 8 warps in a 4 x 2 grid, warp tile 16 x 32 (2 x 4 m8n8k4 DMMA per k-step; a
 // 64 x 128 tile with 32 x 32 warp tiles, 2 CTAs per SM, measured 18 % slower).
-__global__ void __launch_bounds__(256) gjb_trailing(const double* __restrict__ in, double* __restrict__ out, int lda,
+__device__ __forceinline__ void gjb_cp8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(256, 3) gjb_trailing(const double* __restrict__ in, double* __restrict__ out, int lda,
                                                     const int* n_each, int k0, const int* __restrict__ pi,
                                                     const int* status) {
   const int c = blockIdx.z;
@@ -1278,25 +1283,47 @@ __global__ void __launch_bounds__(256) gjb_trailing(const double* __restrict__ i
   double (*Ws)[GJB_WS] = reinterpret_cast<double (*)[GJB_WS]>(sraw);
   double (*Ts)[GJB_TS] = reinterpret_cast<double (*)[GJB_TS]>(sraw + GJB_BM * GJB_WS);
   __shared__ int prow[GJB_BM];
+  // operand tiles by asynchronous 8-byte copies (all of a thread's copies in flight at once); zero padding by stores
   for (int e = threadIdx.x; e < GJB_BM * GJB_NB; e += blockDim.x) {
     const int i = e / GJB_NB, j = e % GJB_NB, row = r0 + i;
-    double w = 0.0;
-    if (j < nbe && row < n) w = A[(long long)row * lda + k0 + j] - (row == k0 + j ? 1.0 : 0.0);
-    Ws[i][j] = w;
+    if (j < nbe && row < n) gjb_cp8(&Ws[i][j], A + (long long)row * lda + k0 + j);
+    else Ws[i][j] = 0.0;
   }
   for (int e = threadIdx.x; e < GJB_NB * GJB_BN; e += blockDim.x) {
     const int j = e / GJB_BN, q = e % GJB_BN, col = c0 + q;
-    double t = 0.0;
-    if (j < nbe && col < lda) t = A[(long long)pc[k0 + j] * lda + col];
-    Ts[j][q] = t;
+    if (j < nbe && col < lda) gjb_cp8(&Ts[j][q], A + (long long)pc[k0 + j] * lda + col);
+    else Ts[j][q] = 0.0;
   }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   for (int i = threadIdx.x; i < GJB_BM; i += blockDim.x) {
     const int row = r0 + i;
     prow[i] = (active && row >= k0 && row < n) ? pc[row] : row;
   }
-  __syncthreads();
+  __syncthreads();   // prow
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+  // the epilogue's base values (row-permuted input, or the unchanged input) loaded while the operands arrive
+  double base[2][4][2];
+  bool upd[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = wm + 8 * a + (lane >> 2), row = r0 + i;
+        const int col = c0 + wn + 8 * b + 2 * (lane & 3) + e;
+        upd[a][b][e] = !(!active || row >= n || col >= n || (col >= k0 && col < k0 + nbe));
+        base[a][b][e] = (row < lda && col < lda) ? A[(long long)(upd[a][b][e] ? prow[i] : row) * lda + col] : 0.0;
+      }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  // W = (panel result) - I on the panel rows
+  for (int j = threadIdx.x; j < nbe; j += blockDim.x) {
+    const int i = k0 + j - r0;
+    if (i >= 0 && i < GJB_BM) Ws[i][j] -= 1.0;
+  }
+  __syncthreads();
   double acc[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -1324,13 +1351,10 @@ __global__ void __launch_bounds__(256) gjb_trailing(const double* __restrict__ i
     for (int b = 0; b < 4; ++b)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int i = wm + 8 * a + (lane >> 2), row = r0 + i;
+        const int row = r0 + wm + 8 * a + (lane >> 2);
         const int col = c0 + wn + 8 * b + 2 * (lane & 3) + e;
         if (row >= lda || col >= lda) continue;
-        double v;
-        if (!active || row >= n || col >= n || (col >= k0 && col < k0 + nbe)) v = A[(long long)row * lda + col];
-        else v = A[(long long)prow[i] * lda + col] + acc[a][b][e];
-        O[(long long)row * lda + col] = v;
+        O[(long long)row * lda + col] = upd[a][b][e] ? base[a][b][e] + acc[a][b][e] : base[a][b][e];
       }
 }
 
