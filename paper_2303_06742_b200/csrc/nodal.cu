@@ -190,7 +190,8 @@ __global__ void __launch_bounds__(128) gather_nodal_kernel(LevelGeom g, const do
     for (int sl = 0; sl < 2 * D; ++sl) {
       const long long eadd = (long long)(m * NE1 + (sl < nsl ? sl : 0) * NQE) * estride;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) v[sl][c] = off[c] >= 0 ? __ldg(Yv[c] + eadd) : 0.0;   // predicated: no request
+      for (int c = 0; c < NC; ++c) v[sl][c] = __ldg(Yv[c] + eadd);   // absent cell: a valid address (predicating the
+                                                                      // loads measured 185 -> 205 us at cfg4 fine)
     }
 #pragma unroll
     for (int sl = 0; sl < 2 * D; ++sl) {
