@@ -124,7 +124,9 @@ int stgmg_setup(const stgmg_mesh* mesh, int levels, const stgmg_order* order, co
  * x = 1 and the re-entrant faces; p = 0 on y = 1 (x < .5), no flux elsewhere.  params: rho, alpha, c0, lambda, mu, K,
  * tau, gamma_a, gamma_b (gamma = gamma_b of the SIP term), hF_mode (penalty length of the Nitsche, directional and
  * SIP terms: cell measure h^3 by default, reading A6; STGMG_HF_EDGE: h; 2: h^3 but h for the directional faces;
- * 3: the fine level's h^3 on every level — coarse operators = Galerkin products), omega, jmax, stream (mesh, bc, smoother,
+ * 3: the fine level's h^3 on every level — coarse operators = Galerkin products; experiments on the grid robustness of
+ * Table 4: 4: h^3 for u, h for the SIP faces of p; 5: h for u, h^3 for p; 6: the face measure h^2 for
+ * both), omega, jmax, stream (mesh, bc, smoother,
  * formulation and nranks are not used: single GPU, Alg. 1, Problem 3.1).  Level operators are assembled (CSR) on the
  * host at setup from element integrals; every patch has its own explicit inverse (K4 on the device).  Vector layout per
  * Radau node: V_0..V_2, U_0..U_2 on the active Q_r nodes (lexicographic over the (2 r 2^ref + 1)^2 (r 2^ref + 1) node

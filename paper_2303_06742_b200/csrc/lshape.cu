@@ -226,7 +226,7 @@ struct ElemMats {
 
 struct Forms {
   int r = 2;
-  double h = 1.0, hF = 1.0, hD = 1.0;   // hD: penalty length of the directional faces
+  double h = 1.0, hF = 1.0, hD = 1.0, hP = 1.0;   // hD: directional faces; hP: SIP (p) faces
   double lam = 1, mu = 1, alpha = 1, rho = 1, c0 = 1, ga = 1, gb = 1, K[3][3] = {{0}};
   std::vector<double> nd;
   Exps ex;
@@ -327,7 +327,7 @@ struct Forms {
     const int fa = f / 2;
     double n[3] = {0, 0, 0};
     n[fa] = f % 2 ? 1.0 : -1.0;
-    const double pen = gb / hF;
+    const double pen = gb / hP;
     const Quad Q = face_quad(r + 1, h, f);
     for (size_t q = 0; q < Q.w.size(); ++q) {
       const double xh[3] = {Q.x[q][0], Q.x[q][1], Q.x[q][2]};
@@ -355,7 +355,7 @@ struct Forms {
       for (int j = 0; j < 2; ++j) Bf[i][j].assign(npc * npc, 0.0);
     double n[3] = {0, 0, 0};
     n[a] = 1.0;
-    const double pen = gb / hF, sg[2] = {1.0, -1.0};
+    const double pen = gb / hP, sg[2] = {1.0, -1.0};
     const Quad Qm = face_quad(r + 1, h, 2 * a + 1), Qp = face_quad(r + 1, h, 2 * a);
     for (size_t q = 0; q < Qm.w.size(); ++q) {
       const double xm[3] = {Qm.x[q][0], Qm.x[q][1], Qm.x[q][2]};
@@ -498,6 +498,12 @@ int lshape_build_host(int ref_coarse, int levels, int r, int k, const OpConsts& 
       F.hF = hf * hf * hf;
     }
     F.hD = (hf_edge || hf_mode == 2) ? g.h : F.hF;   // mode 2: a^d_gamma with the literal h^-1 of P:L778
+    F.hP = F.hF;
+    // experiments on the grid robustness of Table 4: 4 = h^3 for u, h for the SIP faces of p;
+    // 5 = h for u, h^3 for p; 6 = the face measure h^2 for both
+    if (hf_mode == 4) { F.hF = F.hD = g.h * g.h * g.h; F.hP = g.h; }
+    if (hf_mode == 5) { F.hF = F.hD = g.h; F.hP = g.h * g.h * g.h; }
+    if (hf_mode == 6) { F.hF = F.hD = F.hP = g.h * g.h; }
     F.lam = oc.lam;
     F.mu = oc.mu;
     F.alpha = oc.alpha;

@@ -35,11 +35,11 @@ ap.add_argument("--E", type=float, default=20000.0)
 ap.add_argument("--tol", type=float, default=1e-8)
 ap.add_argument("--abs", action="store_true")
 ap.add_argument("--T", type=float, default=4.0)
-ap.add_argument("--hf", default="measure", choices=["measure", "edge", "dir_edge", "frozen"])
+ap.add_argument("--hf", default="measure", choices=["measure", "edge", "dir_edge", "frozen", "u_meas_p_edge", "u_edge_p_meas", "face"])
 a = ap.parse_args()
 tau = 0.01
 t0 = time.perf_counter()
-s = LShapeSolver(a.ref, a.ref - a.coarse + 1, a.r, a.k, tau, params(a.r, a.E), hF_mode={"measure": 0, "edge": 1, "dir_edge": 2, "frozen": 3}[a.hf])
+s = LShapeSolver(a.ref, a.ref - a.coarse + 1, a.r, a.k, tau, params(a.r, a.E), hF_mode={"measure": 0, "edge": 1, "dir_edge": 2, "frozen": 3, "u_meas_p_edge": 4, "u_edge_p_meas": 5, "face": 6}[a.hf])
 setup = time.perf_counter() - t0
 N = s.size()
 X = torch.zeros(N, dtype=torch.float64, device="cuda")
