@@ -185,6 +185,13 @@ class LForms:
             self.hF = float(self.h[0]) if params.get("hF_mode", 0) == 1 else self.vol
         # penalty length of the directional faces: h_F (reading R4), or the literal h of a^d_gamma (hF_mode = 2)
         self.hD = float(self.h[0]) if params.get("hF_mode", 0) in (1, 2) else self.hF
+        # penalty length of the SIP faces of B_gamma: h_F as the u faces, except for the experiment modes of DESIGN.md
+        # §7.6 (4: h^3 for u, h for p; 5: h for u, h^3 for p; 6: the face measure h^2 for both)
+        self.hP = self.hF
+        mode, hh = params.get("hF_mode", 0), float(self.h[0])
+        if params.get("hF_fixed") is None and mode in (4, 5, 6):
+            self.hF = self.hD = {4: self.vol, 5: hh, 6: hh * hh}[mode]
+            self.hP = {4: hh, 5: self.vol, 6: hh * hh}[mode]
         self.K = np.asarray(params["K"], dtype=np.float64).reshape(3, 3)
 
     def _pts(self, face=None):
@@ -242,7 +249,7 @@ class LForms:
         """SIP boundary face (reading R3): -<K grad q.n, psi> - <q, K grad psi.n> + gamma/h_F <q, psi>."""
         _, _, php, gp, w, n = self._pts(f)
         Kgn = np.einsum("ab,sqb,a->sq", self.K, gp, n)
-        pen = self.p["gamma_b"] / self.hF
+        pen = self.p["gamma_b"] / self.hP
         return (-np.einsum("sq,rq,q->rs", Kgn, php, w) - np.einsum("sq,rq,q->rs", php, Kgn, w)
                 + pen * np.einsum("sq,rq,q->rs", php, php, w))
 
@@ -258,7 +265,7 @@ class LForms:
         ph = [pm[2], pp[2]]
         kgn = [np.einsum("ab,sqb,a->sq", self.K, pm[3], n), np.einsum("ab,sqb,a->sq", self.K, pp[3], n)]
         sg = [1.0, -1.0]
-        pen = self.p["gamma_b"] / self.hF
+        pen = self.p["gamma_b"] / self.hP
         Bf = [[None, None], [None, None]]
         for i in range(2):
             for j in range(2):

@@ -159,3 +159,29 @@ def test_table4_ref2_iterations():
           % (avg, min(its), max(its), g[:, 0].min(), g[:, 0].max(), g[:, 1].min(), g[:, 1].max()))
     assert abs(avg - 11.0) <= 2.0, its
     s.close()
+
+
+@pytest.mark.parametrize("mode", [4, 5, 6])
+def test_penalty_length_modes_operator_and_vcycle(mode):
+    """The penalty-length experiment modes of DESIGN.md §7.6 (separate u-Nitsche / SIP lengths, face measure): the
+    operator on every level (1e-13) and one V-cycle (1e-8) against the oracle with the same mode, ref_0 -> ref_1."""
+    import torch
+    from oracle import lshape as LS
+    from paper_2303_06742_b200 import LShapeSolver
+    params = dict(LS.lshape_params(2), hF_mode=mode)
+    H = LS.LHierarchy(0, 2, 2, 1, 0.01, params=params)
+    s = LShapeSolver(1, 2, 2, 1, 0.01, params, hF_mode=mode)
+    rng = np.random.default_rng(40 + mode)
+    for l, lv in enumerate(H.levels):
+        x = rng.uniform(-1, 1, lv.N)
+        y = torch.zeros(lv.N, dtype=torch.float64, device="cuda")
+        s.apply(to_gpu(x), y, level=l)
+        torch.cuda.synchronize()
+        assert rel(to_np(y), H.A[l] @ x) <= 1e-13
+    N = H.levels[-1].N
+    b = rng.uniform(-1, 1, N)
+    x = torch.zeros(N, dtype=torch.float64, device="cuda")
+    s.vcycle(to_gpu(b), x)
+    torch.cuda.synchronize()
+    assert rel(to_np(x), H.vcycle(b)) <= 1e-8
+    s.close()

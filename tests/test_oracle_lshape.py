@@ -232,3 +232,22 @@ def test_L9_goal_quantities_of_constants():
     x[o + 2 * lv.R:o + lv.block:4] = 1.0         # p = 1
     bu, bp = LS.goal_quantities(lv, x)
     assert abs(bu - 0.25) <= 1e-14 and abs(bp - 0.25) <= 1e-14
+
+
+def test_penalty_length_modes_enter_as_gamma_over_hF():
+    """The experiment modes of DESIGN.md §7.6 change only the penalty lengths: B_gamma(mode) - B_gamma(|K|_d) =
+    gamma_b (1 / h_P - 1 / h^3) M_pen with ONE penalty form M_pen for every mode (4: h_P = h, 6: h_P = h^2), and
+    mode 5 leaves B_gamma unchanged; likewise A_gamma for the u lengths (5: h, 6: h^2) — Def:ab / Def:B."""
+    lv = LS.LLevel(1, 2, 1)
+    h = lv.h[0]
+    S = {m: LS.LSpatial(lv, dict(LS.lshape_params(2), hF_mode=m)) for m in (0, 4, 5, 6)}
+    dB4 = (S[4].B - S[0].B).toarray() / (1.0 / h - 1.0 / h ** 3)
+    dB6 = (S[6].B - S[0].B).toarray() / (1.0 / h ** 2 - 1.0 / h ** 3)
+    assert np.abs(dB4).max() > 0
+    assert np.allclose(dB4, dB6, rtol=0, atol=1e-9 * np.abs(dB4).max())
+    assert np.abs((S[5].B - S[0].B).toarray()).max() == 0.0
+    dA5 = (S[5].A - S[0].A).toarray() / (1.0 / h - 1.0 / h ** 3)
+    dA6 = (S[6].A - S[0].A).toarray() / (1.0 / h ** 2 - 1.0 / h ** 3)
+    assert np.abs(dA5).max() > 0
+    assert np.allclose(dA5, dA6, rtol=0, atol=1e-9 * np.abs(dA5).max())
+    assert np.abs((S[4].A - S[0].A).toarray()).max() == 0.0
