@@ -450,6 +450,19 @@ struct stgmg_handle {
   bool graphable = true;
   bool op_gemm = false;            // runtime K1 = element GEMM on the tensor pipe + node gather (3D; large 2D elements)
   GjScratch gj;                    // blocked Gauss–Jordan scratch, reused by every setup inverse, freed after setup
+  // K4 inverses of stgmg_setup in flight: the coarse inverse and every level's class inverses run on their own
+  // non-blocking streams, overlapping each other and the host-side setup of the next levels; finish_inverses joins
+  // them (swizzle, singularity check) before the V-cycle graph is captured.  STGMG_SETUP_SERIAL=1: on h->s.
+  struct PendingInv {
+    int level = 0;                 // 0 = coarse inverse (A0inv), >= 1 = class inverses of that level
+    int n = 0, lda = 0;            // matrices, leading dimension
+    cudaStream_t st = nullptr;     // owned unless it is h->s
+    cudaEvent_t done = nullptr;
+    GjScratch scr;
+    double* inv_rm = nullptr;      // row-major class inverses (level >= 1), swizzled into Lv.inv_dev at the join
+    int* status = nullptr;         // device, n entries (h->allocs)
+  };
+  std::vector<PendingInv> pend;
   int fg_on = 1;                   // K1 element GEMM in the factored form (STGMG_K1_FGEMM=0: the full element matrix;
                                    // 2: on every element-route level regardless of size, for tests)
   int sf_on = 1;                   // 3D Q2: volume-only cell types by sum factorisation on levels with >= 128k cells
@@ -480,6 +493,14 @@ struct stgmg_handle {
     for (void* p : allocs) cudaFree(p);
     if (gj.buf) cudaFree(gj.buf);
     if (gj.pi) cudaFree(gj.pi);
+    for (auto& p : pend) {
+      if (p.st) cudaStreamSynchronize(p.st);
+      if (p.st && p.st != s) cudaStreamDestroy(p.st);
+      if (p.done) cudaEventDestroy(p.done);
+      if (p.scr.buf) cudaFree(p.scr.buf);
+      if (p.scr.pi) cudaFree(p.scr.pi);
+      if (p.inv_rm) cudaFree(p.inv_rm);
+    }
     delete tr;
     if (pinned) cudaFreeHost(pinned);
     if (e0) cudaEventDestroy(e0);
@@ -977,6 +998,71 @@ struct SetupMarks {
   }
 };
 
+// Enqueues the batched Gauss–Jordan inverse (K4) of nmat matrices behind the work already on h->s, on a stream of
+// its own (see stgmg_handle::PendingInv); finish_inverses joins it.
+static int launch_inverse_async(stgmg_handle* h, int level, double* mats, int nmat, int n_max, const int* n_each,
+                                int lda, int* perm, double* colk, double* scale, int* status, double* inv_rm) {
+  static const bool serial = std::getenv("STGMG_SETUP_SERIAL") != nullptr;
+  h->pend.emplace_back();
+  stgmg_handle::PendingInv& p = h->pend.back();
+  p.level = level;
+  p.n = nmat;
+  p.lda = lda;
+  p.status = status;
+  p.inv_rm = inv_rm;
+  CKE(cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming));
+  if (serial) {
+    p.st = h->s;
+  } else {
+    CKE(cudaStreamCreateWithFlags(&p.st, cudaStreamNonBlocking));
+    CKE(cudaEventRecord(p.done, h->s));   // inputs ready
+    CKE(cudaStreamWaitEvent(p.st, p.done, 0));
+  }
+  if (gauss_jordan_inverse(mats, nmat, n_max, n_each, lda, perm, colk, scale, status, p.st, &p.scr)) {
+    set_error(level ? "gauss_jordan_inverse launch failed" : "coarse gauss_jordan_inverse launch failed");
+    return STGMG_ECUDA;
+  }
+  CKE(cudaEventRecord(p.done, p.st));
+  return 0;
+}
+
+// Joins the inverses launched by launch_inverse_async: class inverses into the chunk-major K2 layout, singular
+// matrices reported (level and pivot step), scratch released.
+static int finish_inverses(stgmg_handle* h) {
+  if (h->pend.empty()) return 0;
+  std::vector<std::vector<int>> st(h->pend.size());
+  for (size_t i = 0; i < h->pend.size(); ++i) {
+    auto& p = h->pend[i];
+    CKE(cudaStreamWaitEvent(h->s, p.done, 0));
+    if (p.level > 0) CKE(launch_chunk_swizzle(p.inv_rm, h->lev[p.level].inv_dev, p.n, p.lda, h->s));
+    st[i].resize(p.n);
+    CKE(cudaMemcpyAsync(st[i].data(), p.status, sizeof(int) * p.n, cudaMemcpyDeviceToHost, h->s));
+  }
+  CKE(cudaStreamSynchronize(h->s));
+  std::string err;
+  for (size_t i = 0; i < h->pend.size() && err.empty(); ++i) {
+    const auto& p = h->pend[i];
+    for (int c = 0; c < p.n && err.empty(); ++c)
+      if (st[i][c] != 0)
+        err = p.level == 0 ? "singular coarse matrix (pivot step " + std::to_string(st[i][c]) + ")"
+                           : "singular patch matrix: level " + std::to_string(p.level) + " class " +
+                                 std::to_string(c) + " (pivot step " + std::to_string(st[i][c]) + ")";
+  }
+  for (auto& p : h->pend) {
+    if (p.st != h->s) CKE(cudaStreamDestroy(p.st));
+    CKE(cudaEventDestroy(p.done));
+    if (p.scr.buf) CKE(cudaFree(p.scr.buf));
+    if (p.scr.pi) CKE(cudaFree(p.scr.pi));
+    if (p.inv_rm) CKE(cudaFree(p.inv_rm));
+  }
+  h->pend.clear();
+  if (!err.empty()) {
+    set_error(err);
+    return STGMG_ESINGULAR;
+  }
+  return 0;
+}
+
 static int build_patches(stgmg_handle* h, int l) {
   NvtxRange nv("stgmg setup: patch classes + inverses (K4)");
   SetupMarks sm;
@@ -1200,19 +1286,20 @@ static int build_patches(stgmg_handle* h, int l) {
   CKE(cudaMalloc(&inv_rm, sizeof(double) * (size_t)ncls * Lv.lda * Lv.lda));
   CK(dalloc(h, &Lv.inv_dev, (size_t)ncls * Lv.lda * Lv.lda + kK2Slack));
   CKE(cudaMemsetAsync(Lv.inv_dev, 0, sizeof(double) * ((size_t)ncls * Lv.lda * Lv.lda + kK2Slack), h->s));
-  // dense mini-level operator: column j = A_mini e_j
+  // dense mini-level operator: column j = A_mini e_j (stream-ordered scratch: a cudaFree would wait for the
+  // inverses of the previous levels still running on their own streams)
   const long long Nm = mini.N;
   double *X = nullptr, *Ym = nullptr;
-  CKE(cudaMalloc(&X, sizeof(double) * Nm * Nm));
-  CKE(cudaMalloc(&Ym, sizeof(double) * Nm * Nm));
+  CKE(cudaMallocAsync(&X, sizeof(double) * Nm * Nm, h->s));
+  CKE(cudaMallocAsync(&Ym, sizeof(double) * Nm * Nm, h->s));
   CKE(cudaMemsetAsync(X, 0, sizeof(double) * Nm * Nm, h->s));
   CKE(cudaMemsetAsync(Ym, 0, sizeof(double) * Nm * Nm, h->s));
   CKE(launch_identity(X, Nm, h->s));
   {
     double* Ycb = nullptr;
-    if (h->d == 2) CKE(cudaMalloc(&Ycb, sizeof(double) * Nm * cell_count(mini) * elem_dofs(h)));
+    if (h->d == 2) CKE(cudaMallocAsync(&Ycb, sizeof(double) * Nm * cell_count(mini) * elem_dofs(h), h->s));
     int rc = apply_into(h, mini, X, Ym, (int)Nm, Nm, Ycb);
-    if (Ycb) { CKE(cudaStreamSynchronize(h->s)); CKE(cudaFree(Ycb)); }
+    if (Ycb) CKE(cudaFreeAsync(Ycb, h->s));
     if (rc) return rc;
   }
   sm.mark("mini-level dense operator", l);
@@ -1230,25 +1317,11 @@ static int build_patches(stgmg_handle* h, int l) {
   CK(dalloc(h, &colk, (size_t)ncls * Lv.lda));
   CK(dalloc(h, &scale, (size_t)ncls * Lv.lda));
   CKE(cudaMemsetAsync(status, 0, sizeof(int) * ncls, h->s));
+  CKE(cudaFreeAsync(X, h->s));
+  CKE(cudaFreeAsync(Ym, h->s));
   sm.mark("extraction", l);
-  if (gauss_jordan_inverse(inv_rm, ncls, Lv.maxcp, cps_dev, Lv.lda, perm, colk, scale, status, h->s, &h->gj)) {
-    set_error("gauss_jordan_inverse launch failed");
-    return STGMG_ECUDA;
-  }
+  CK(launch_inverse_async(h, l, inv_rm, ncls, Lv.maxcp, cps_dev, Lv.lda, perm, colk, scale, status, inv_rm));
   sm.mark("Gauss-Jordan", l);
-  CKE(launch_chunk_swizzle(inv_rm, Lv.inv_dev, ncls, Lv.lda, h->s));
-  std::vector<int> st(ncls);
-  CKE(cudaMemcpyAsync(st.data(), status, sizeof(int) * ncls, cudaMemcpyDeviceToHost, h->s));
-  CKE(cudaStreamSynchronize(h->s));
-  CKE(cudaFree(X));
-  CKE(cudaFree(Ym));
-  CKE(cudaFree(inv_rm));
-  for (int c = 0; c < ncls; ++c)
-    if (st[c] != 0) {
-      set_error("singular patch matrix: level " + std::to_string(l) + " class " + std::to_string(c) +
-                " (pivot step " + std::to_string(st[c]) + ")");
-      return STGMG_ESINGULAR;
-    }
   return 0;
 }
 
@@ -1346,7 +1419,7 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
     CKE(cudaMemsetAsync(Lv.E_dev, 0, sizeof(double) * ((size_t)nt * Lv.elda * Lv.elda + kK2Slack), h->s));
   }
   double* E_rm = nullptr;   // row-major element matrices (setup scratch); the GEMM reads the chunk-major Lv.E_dev
-  CKE(cudaMalloc(&E_rm, sizeof(double) * (size_t)nt * Lv.elda * Lv.elda));
+  CKE(cudaMallocAsync(&E_rm, sizeof(double) * (size_t)nt * Lv.elda * Lv.elda, h->s));
   // element results of the mini level for every unit vector
   const long long Nm = mini.N;
   long long nvm = 1;
@@ -1355,8 +1428,8 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
   double *X = nullptr, *Ycb = nullptr;
   long long* reps_dev = nullptr;
   int* mdofs_dev = nullptr;
-  CKE(cudaMalloc(&X, sizeof(double) * Nm * Nm));
-  CKE(cudaMalloc(&Ycb, sizeof(double) * Nm * ycs));
+  CKE(cudaMallocAsync(&X, sizeof(double) * Nm * Nm, h->s));
+  CKE(cudaMallocAsync(&Ycb, sizeof(double) * Nm * ycs, h->s));
   CKE(cudaMemsetAsync(X, 0, sizeof(double) * Nm * Nm, h->s));
   CKE(cudaMemsetAsync(Ycb, 0, sizeof(double) * Nm * ycs, h->s));
   CKE(launch_identity(X, Nm, h->s));
@@ -1413,9 +1486,9 @@ static int build_cells(stgmg_handle* h, int l, bool gemm, std::vector<double>* E
     Ehost->resize((size_t)nt * Lv.elda * Lv.elda);
     CKE(cudaMemcpy(Ehost->data(), E_rm, sizeof(double) * Ehost->size(), cudaMemcpyDeviceToHost));
   }
-  CKE(cudaFree(E_rm));
-  CKE(cudaFree(X));
-  CKE(cudaFree(Ycb));
+  CKE(cudaFreeAsync(E_rm, h->s));   // stream-ordered: no device-wide wait on the inverses in flight
+  CKE(cudaFreeAsync(X, h->s));
+  CKE(cudaFreeAsync(Ycb, h->s));
   return 0;
 }
 
@@ -1425,16 +1498,16 @@ static int build_coarse(stgmg_handle* h) {
   const long long N = g.N;
   h->n0 = (int)N;
   double *X = nullptr, *Ym = nullptr;
-  CKE(cudaMalloc(&X, sizeof(double) * N * N));
-  CKE(cudaMalloc(&Ym, sizeof(double) * N * N));
+  CKE(cudaMallocAsync(&X, sizeof(double) * N * N, h->s));
+  CKE(cudaMallocAsync(&Ym, sizeof(double) * N * N, h->s));
   CKE(cudaMemsetAsync(X, 0, sizeof(double) * N * N, h->s));
   CKE(cudaMemsetAsync(Ym, 0, sizeof(double) * N * N, h->s));
   CKE(launch_identity(X, N, h->s));
   {
     double* Ycb = nullptr;
-    if (h->d == 2) CKE(cudaMalloc(&Ycb, sizeof(double) * N * cell_count(g) * elem_dofs(h)));
+    if (h->d == 2) CKE(cudaMallocAsync(&Ycb, sizeof(double) * N * cell_count(g) * elem_dofs(h), h->s));
     int rc = apply_into(h, g, X, Ym, (int)N, N, Ycb);
-    if (Ycb) { CKE(cudaStreamSynchronize(h->s)); CKE(cudaFree(Ycb)); }
+    if (Ycb) CKE(cudaFreeAsync(Ycb, h->s));
     if (rc) return rc;
   }
   std::vector<int> dofs(N);
@@ -1454,20 +1527,9 @@ static int build_coarse(stgmg_handle* h) {
   CK(dalloc(h, &colk, (size_t)N));
   CK(dalloc(h, &scale, (size_t)N));
   CKE(cudaMemsetAsync(status, 0, sizeof(int), h->s));
-  if (gauss_jordan_inverse(h->A0inv, 1, (int)N, cps_dev, (int)N, perm, colk, scale, status, h->s, &h->gj)) {
-    set_error("coarse gauss_jordan_inverse launch failed");
-    return STGMG_ECUDA;
-  }
-  int st = 0;
-  CKE(cudaMemcpyAsync(&st, status, sizeof(int), cudaMemcpyDeviceToHost, h->s));
-  CKE(cudaStreamSynchronize(h->s));
-  CKE(cudaFree(X));
-  CKE(cudaFree(Ym));
-  if (st != 0) {
-    set_error("singular coarse matrix (pivot step " + std::to_string(st) + ")");
-    return STGMG_ESINGULAR;
-  }
-  return 0;
+  CKE(cudaFreeAsync(X, h->s));
+  CKE(cudaFreeAsync(Ym, h->s));
+  return launch_inverse_async(h, 0, h->A0inv, 1, (int)N, cps_dev, (int)N, perm, colk, scale, status, nullptr);
 }
 
 static int build_transfer(stgmg_handle* h, int l) {
@@ -1502,7 +1564,8 @@ static int build_transfer(stgmg_handle* h, int l) {
   // measured (R+P, one B200): cfg2 fine (7.9M) 368 -> 156 us, cfg3 level 3 (441k) 80 -> 31 us, cfg3 fine (3.4M)
   // 97 -> 81 us, but cfg4 fine (26.6M) 489 -> 542 us (its first pass is latency-bound on the table chain): the gather
   // form stays on levels above 16M DoFs
-  if (!sep_off && F.g.N >= 200000 && F.g.N < 16000000) CK(dalloc(h, &F.rtmp, (size_t)F.g.N));
+  const bool sep_all = sep_env && std::atoi(sep_env) == 2;   // every level >= 200k DoFs (measurement)
+  if (!sep_off && F.g.N >= 200000 && (F.g.N < 16000000 || sep_all)) CK(dalloc(h, &F.rtmp, (size_t)F.g.N));
   return 0;
 }
 
@@ -1802,6 +1865,7 @@ const char* stgmg_last_error(void) { return g_last_error.c_str(); }
 // Setup steps shared by every hierarchy: Krylov / reduction workspace, events, the folded coarse sub-cycle, the
 // V-cycle graph.
 static int finish_setup(stgmg_handle* h) {
+  CK(finish_inverses(h));
   if (h->gj.buf || h->gj.pi) {   // setup scratch of the class inverses
     CKE(cudaStreamSynchronize(h->s));
     if (h->gj.buf) CKE(cudaFree(h->gj.buf));
