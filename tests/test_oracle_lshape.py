@@ -251,3 +251,58 @@ def test_penalty_length_modes_enter_as_gamma_over_hF():
     assert np.abs(dA5).max() > 0
     assert np.allclose(dA5, dA6, rtol=0, atol=1e-9 * np.abs(dA5).max())
     assert np.abs((S[4].A - S[0].A).toarray()).max() == 0.0
+
+
+def test_L10_slab_energy_identity():
+    """L10: the homogeneous slab problem (P:L233-256 with f = 0, no traction) dissipates the energy
+    E(v, u, p) = (rho |v|^2 + a_gamma(u, u) + c0 |p|^2) / 2 exactly as the continuous system does, up to the dG(k)
+    jump: testing the rows (phi, chi, psi) with (M_rho^-1 A_gamma u, v, p) — polynomials of degree k in time, so
+    admissible rows of the algebraic system — and using that the k+1 point right Radau rule integrates d/dt E
+    (degree 2k - 1) and b_gamma(p, p) (degree 2k) exactly gives
+
+        E(x(t_n)) - E(x(t_{n-1}^-)) + E(x(t_{n-1}^+) - x(t_{n-1}^-)) + Q_n(b_gamma(p, p)) = 0.
+
+    The coupling terms cancel only if C enters the chi row as +C^T p and the psi row as -C v: a sign
+    slip in either, a wrong T, a wrong chi_hat(-1) or a wrong jump term in slab_rhs breaks the identity at O(1).
+    Radau data typed from the textbook rule for k = 1: nodes (-1/3, 1), weights (3/2, 1/2), chi_hat(-1) = (3/2, -1/2).
+    """
+    tau = 0.05
+    H = LS.LHierarchy(0, 1, 2, 1, tau)
+    lev, S = H.fine, H.spatial[-1]
+    R, blk = lev.R, lev.block
+    th = 0.5 * tau * np.array([1.5, 0.5])
+    cm1 = np.array([1.5, -0.5])
+    lu = spla.splu(H.A[-1].tocsc())
+
+    def split(xb):
+        return xb[:R], xb[R:2 * R], xb[2 * R:]
+
+    def energy(xb):
+        V, U, P = split(xb)
+        return 0.5 * (V @ (S.Mr @ V) + U @ (S.A @ U) + P @ (S.Mc @ P))
+
+    rng = np.random.default_rng(11)
+    x_prev = np.zeros(lev.N)
+    x_prev[blk:] = rng.uniform(-1, 1, blk)
+    # scale the three fields so that the three energies and the coupling are of comparable size
+    V, U, P = split(x_prev[blk:])
+    V *= 1.0 / np.sqrt(V @ (S.Mr @ V))
+    U *= 1.0 / np.sqrt(U @ (S.A @ U))
+    P *= 1.0 / np.sqrt(P @ (S.Mc @ P))
+    coupling = 0.0
+    for _ in range(3):
+        F = LS.slab_rhs(H, np.zeros(lev.N), x_prev)
+        x = lu.solve(F)
+        xm = x_prev[blk:]
+        xp = cm1[0] * x[:blk] + cm1[1] * x[blk:]
+        diss = sum(th[b] * (split(x[b * blk:(b + 1) * blk])[2] @ (S.B @ split(x[b * blk:(b + 1) * blk])[2]))
+                   for b in range(2))
+        coupling = max(coupling, max(abs(split(x[b * blk:(b + 1) * blk])[0] @ (S.C.T @ split(x[b * blk:(b + 1) * blk])[2]))
+                                     * th[b] for b in range(2)))
+        E0, E1 = energy(xm), energy(x[blk:])
+        defect = E1 - E0 + energy(xp - xm) + diss
+        assert diss > 0 and E1 < E0
+        assert abs(defect) <= 1e-9 * E0, (defect, E0)
+        x_prev = x
+    # the identity is a real constraint on the coupling sign: the terms that cancel are 10^5 tolerances large
+    assert coupling >= 1e-4
