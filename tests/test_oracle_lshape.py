@@ -306,3 +306,39 @@ def test_L10_slab_energy_identity():
         x_prev = x
     # the identity is a real constraint on the coupling sign: the terms that cancel are 10^5 tolerances large
     assert coupling >= 1e-4
+
+
+def test_L11_slab_load_is_radau_quadrature_of_sin():
+    """L11: L_n = Q_n(<sin(8 pi t) t_N, chi>) (P:L241-251 with the load of P:L757-783): summed over the Radau rows
+    it is F times the (k+1)-point Radau value of int_{I_n} sin(8 pi t) dt, and weighted with (t_{n,b} - t_{n-1})
+    the first moment; the rule is exact to degree 2k, so both approach the closed forms
+    (cos(8 pi t0) - cos(8 pi t1)) / (8 pi) and int (t - t0) sin(8 pi t) dt at relative O(tau^(2k+1)) — halving tau
+    gains 2^(2k+1) — and only the chi rows carry load.  Nodes typed from the textbook rule (k = 1: -1/3, 1)."""
+    w8 = 8.0 * np.pi
+    t0 = 0.013
+
+    def moments(tau):
+        t1 = t0 + tau
+        m0 = (np.cos(w8 * t0) - np.cos(w8 * t1)) / w8
+        # int (t - t0) sin(w t) dt = [-(t - t0) cos(w t) / w + sin(w t) / w^2]
+        m1 = -(t1 - t0) * np.cos(w8 * t1) / w8 + (np.sin(w8 * t1) - np.sin(w8 * t0)) / w8 ** 2
+        return m0, m1
+
+    errs = []
+    for tau in (0.01, 0.005):
+        H = LS.LHierarchy(0, 1, 2, 1, tau)
+        lev = H.fine
+        fN = LS.traction_vector(lev, H.params)
+        L = LS.slab_load(H, t0).reshape(2, lev.block)
+        chi = L[:, lev.R:2 * lev.R]
+        assert np.all(L[:, :lev.R] == 0) and np.all(L[:, 2 * lev.R:] == 0)      # phi and psi rows carry no load
+        nodes = t0 + 0.5 * tau * (1.0 + np.array([-1.0 / 3.0, 1.0]))
+        m0, m1 = moments(tau)
+        s0 = chi.sum(axis=0)
+        s1 = ((nodes - t0)[:, None] * chi).sum(axis=0)
+        j = int(np.argmax(abs(fN)))
+        assert np.allclose(s0 * fN[j], s0[j] * fN, rtol=0, atol=1e-12 * abs(s0[j] * fN[j]))   # parallel to F
+        errs.append((abs(s0[j] / fN[j] - m0) / abs(m0), abs(s1[j] / fN[j] - m1) / abs(m1)))
+    (e0a, e1a), (e0b, e1b) = errs
+    assert e0a <= 2e-4 and e1a <= 2e-3, errs
+    assert 5.0 <= e0a / e0b <= 12.0, errs                                        # O(tau^3) for k = 1
