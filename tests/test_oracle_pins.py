@@ -121,6 +121,27 @@ def test_element_invariants_2d():
     assert np.abs(interior["B"] @ np.ones(interior["B"].shape[0])).max() < 1e-12
 
 
+@pytest.mark.parametrize("d,h", [(2, (0.5, 0.125)), (3, (0.5, 0.25, 0.0625))])
+def test_penalty_length_is_cell_measure(d, h):
+    """"For boundary faces we set h_F := |K|_d" (reading A6).  On constants the consistency terms of
+    a_gamma / b_gamma vanish (sigma(const) = 0, grad const = 0) and the bases are partitions of unity, so the sum of
+    all entries of one component block of the element A with ONE Dirichlet face F (normal to axis a) is
+    gamma_a |F| / h_F = gamma_a / h_a, and the sum of all entries of B is gamma_b / h_a — on an anisotropic cell the
+    edge reading h_F = h_a gives gamma_a |K| / h_a^2 instead."""
+    from oracle.element import ElementForms
+    K = np.eye(d).ravel().tolist()
+    prm = P0 | {"K": K, "gamma_a": 5e4 * 2 * 3, "gamma_b": 0.5 * 2 * 1}      # P:L207-210 with r = 2
+    ef = ElementForms(d, 2, h, prm)
+    nb = 3 ** d
+    for a in range(d):
+        for s in (0, 1):
+            M = ef.matrices((2 * a + s,), (2 * a + s,))
+            for c in range(d):
+                blk = M["A"][c * nb:(c + 1) * nb, c * nb:(c + 1) * nb]
+                assert abs(blk.sum() - prm["gamma_a"] / h[a]) <= 1e-9 * prm["gamma_a"] / h[a]
+            assert abs(M["B"].sum() - prm["gamma_b"] / h[a]) <= 1e-9 * prm["gamma_b"] / h[a]
+
+
 def test_element_rotation_kernel_3d():
     """Infinitesimal rotations are strain-free: volume part of A annihilates (-y, x, 0) on a 3D cell."""
     lev = Level(3, [1, 1, 1], [0, 0, 0], [1, 1, 1], 2, 0)
