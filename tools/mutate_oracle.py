@@ -80,8 +80,31 @@ ELEMENT = [
  ("e_ds_sign", 'blk[sP, sU] = -T[b, a] * C', 'blk[sP, sU] = T[b, a] * C'),
  ("e_pen_a_b", 'pen = ga / self.hF(f)', 'pen = gb / self.hF(f)'),
 ]
+VANKA = [
+ ("v_no_averaging", 'return d + self.omega * z / self.P.p', 'return d + self.omega * z'),
+ ("v_unscale", 'return inv * s[:, None] * s[None, :]', 'return inv * s[:, None]'),
+ ("v_post_from_zero", 'd = np.zeros_like(b) if d is None else d.copy()', 'd = np.zeros_like(b)'),
+ ("v_class_rep_inverse", 'Y = r[Z] @ self.inv[mem[0]].T', 'Y = r[Z] @ self.inv[mem[0]]'),
+]
+TRANSFER = [
+ ("t_child_offset", 'xf = 0.5 * ((cf % 2) + nodes)', 'xf = 0.5 * (((cf + 1) % 2) + nodes)'),
+ ("t_pressure_degree", 'Pp = kron_axes(r - 1)', 'Pp = kron_axes(r - 1) * 2.0'),
+ ("t_transposed_weights", 'P[deg * cf + i, deg * cc + j] = V[j, i]', 'P[deg * cf + i, deg * cc + j] = V[i, j]'),
+]
+TEMPORAL = [
+ ("tm_T_transposed", 'T[b, a] = w[b] * D[a, b] + Vm1[a] * Vm1[b]', 'T[b, a] = w[b] * D[b, a] + Vm1[a] * Vm1[b]'),
+ ("tm_no_jump", 'T[b, a] = w[b] * D[a, b] + Vm1[a] * Vm1[b]', 'T[b, a] = w[b] * D[a, b]'),
+ ("tm_weight_index", 'T[b, a] = w[b] * D[a, b] + Vm1[a] * Vm1[b]', 'T[b, a] = w[a] * D[a, b] + Vm1[a] * Vm1[b]'),
+]
+MG = [
+ ("mg_no_post", 'd = d + self.P[l] @ dc\n        return sm.smooth(b, d, self.jmax, self.colored, self.overwrite)', 'd = d + self.P[l] @ dc\n        return d'),
+ ("mg_restrict_b", 'dc = self.vcycle(self.P[l].T @ r, l - 1)', 'dc = self.vcycle(self.P[l].T @ b, l - 1)'),
+ ("mg_correction_sign", 'd = d + self.P[l] @ dc', 'd = d - self.P[l] @ dc'),
+]
 GROUPS = [("oracle/lshape.py", LSHAPE, LSHAPE_TESTS), ("oracle/loads.py", LOADS, BOX_TESTS),
-          ("oracle/element.py", ELEMENT, BOX_TESTS)]
+          ("oracle/element.py", ELEMENT, BOX_TESTS), ("oracle/vanka.py", VANKA, BOX_TESTS),
+          ("oracle/transfer.py", TRANSFER, BOX_TESTS), ("oracle/temporal.py", TEMPORAL, BOX_TESTS),
+          ("oracle/mg.py", MG, BOX_TESTS)]
 
 
 def main():
