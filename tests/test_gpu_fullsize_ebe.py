@@ -30,7 +30,16 @@ def rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-@pytest.fixture(scope="module", params=[3, 2, 4], ids=["cfg3", "cfg2", "cfg4"])
+# cfg4 (the bench workload, 26.6M DoFs) costs 2-6 minutes of host-side oracle work — more on a slow host — of the
+# driver's 1200-s limit for the whole GPU suite: it runs when STGMG_FULLSIZE_CFG4=1 (V-cycle, first FGMRES iterate,
+# oracle-evaluated residual) or STGMG_FULLSIZE_ORACLE_SOLVE=1 (whole oracle solve; green in
+# profiles/r02/pytest_gpu_s5.log and the earlier sessions' logs).  tests/test_gpu_fullsize.py covers cfg4 at full
+# size by sampled operator rows, sweep DoFs and residual rows in every run.
+_CFG4 = os.environ.get("STGMG_FULLSIZE_CFG4") == "1" or os.environ.get("STGMG_FULLSIZE_ORACLE_SOLVE") == "1"
+_CASES = [3, 2] + ([4] if _CFG4 else [])
+
+
+@pytest.fixture(scope="module", params=_CASES, ids=["cfg%d" % c for c in _CASES])
 def case(request):
     import torch
     from threadpoolctl import threadpool_limits
